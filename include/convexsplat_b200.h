@@ -1,0 +1,182 @@
+/*
+ * convexsplat_b200 -- C ABI of the B200 (sm_100a) convex-splatting rasterizer.
+ *
+ * Drop-in for the hot path of the reference package `convexsplat` 0.1.0
+ * (/root/reference/pkg/src/convexsplat).  Every entry point names the
+ * reference interface it replaces.  The Python host side
+ * (paper_2411_14974_b200/rasterizer.py) binds these with ctypes, exactly as
+ * INTEGRATION.md shows for the reference package.
+ *
+ * Conventions
+ *   - All pointers except the structs themselves are DEVICE pointers
+ *     (cudaMalloc / torch CUDA tensors) unless a name says `host`.
+ *   - The caller owns every buffer, including the workspace; the library
+ *     never allocates, frees or synchronises (except cs_read_counters).
+ *   - Calls are stream-ordered on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  No global mutable state: calls are
+ *     re-entrant given distinct workspaces.
+ *   - Gradients are ACCUMULATED (+=) into caller-zeroed buffers so sums of
+ *     per-view backwards follow GradientBuffer.add (backward.py:65-73).
+ *   - Return codes: CS_OK, or a CS_ERR_* value (cs_error_string).
+ */
+#ifndef CONVEXSPLAT_B200_H
+#define CONVEXSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define CS_API __attribute__((visibility("default")))
+#else
+#define CS_API
+#endif
+
+enum cs_status {
+    CS_OK = 0,
+    CS_ERR_ARG = 1,           /* bad argument (null pointer, K out of range, bad sizes) */
+    CS_ERR_CUDA = 2,          /* a kernel launch failed (cudaGetLastError) */
+    CS_ERR_WORKSPACE = 3,     /* workspace smaller than cs_workspace_size() */
+    CS_ERR_UNSUPPORTED = 4    /* tile size other than 16, sh_degree outside 0..3 */
+};
+
+/* Scaling of delta/sigma with depth: ScalingMode (field.py:17-23). */
+enum cs_scaling { CS_SCALE_NONE = 0, CS_SCALE_SQRT = 1, CS_SCALE_DEPTH = 2, CS_SCALE_DEPTH2 = 3 };
+
+/* Camera (model.py:135-172): x_cam = R p + t; pixel = (fx x/z + cx, fy y/z + cy);
+ * orthographic drops the divide.  R is row-major. */
+typedef struct cs_camera {
+    double fx, fy, cx, cy;
+    double R[9];
+    double t[3];
+    double z_near;
+    int32_t width, height;
+    int32_t ortho;
+    int32_t reserved;
+} cs_camera;
+
+/* RenderSettings (rasterize.py:33-53) + Scene.background + ScalingMode. */
+typedef struct cs_settings {
+    double cutoff;            /* contribution_cutoff (default 2e-4) */
+    double floor;             /* transmittance_floor (default 1e-4) */
+    double background[3];     /* Scene.background */
+    int32_t tile;             /* tile_size; 16 is the supported value */
+    int32_t sh_degree;        /* 0..3 */
+    int32_t scaling_mode;     /* enum cs_scaling */
+    int32_t reserved;
+} cs_settings;
+
+/* Scene parameters in raw form, SoA float32 (SmoothConvex, model.py:57-126). */
+typedef struct cs_params {
+    int64_t n;                /* number of convexes */
+    int32_t k;                /* points per convex, 3..16 (reference requires >= 4) */
+    int32_t reserved;
+    const float *points;      /* [n,k,3] */
+    const float *raw_delta;   /* [n]  delta   = exp(raw)      */
+    const float *raw_sigma;   /* [n]  sigma   = exp(raw)      */
+    const float *raw_opacity; /* [n]  opacity = sigmoid(raw)  */
+    const float *raw_mask;    /* [n]  mask    = sigmoid(raw)  */
+    const float *sh;          /* [n,16,3] */
+} cs_params;
+
+/* RenderOutput (rasterize.py:68-74) + a depth map (sum of T*alpha*depth). */
+typedef struct cs_frame {
+    float *image;             /* [H,W,3] */
+    float *final_T;           /* [H,W] */
+    int32_t *count;           /* [H,W] */
+    float *weight_sum;        /* [H,W] */
+    float *depth;             /* [H,W] or NULL */
+    uint8_t *visible;         /* [n] or NULL, written 0/1 */
+} cs_frame;
+
+/* GradientBuffer (backward.py:39-73); all [+=] accumulated. */
+typedef struct cs_grads {
+    float *d_points;          /* [n,k,3] */
+    float *d_raw_delta;       /* [n] */
+    float *d_raw_sigma;       /* [n] */
+    float *d_raw_opacity;     /* [n] */
+    float *d_raw_mask;        /* [n] */
+    float *d_sh;              /* [n,16,3] */
+} cs_grads;
+
+/* Byte offsets of the named regions inside the caller's workspace. */
+typedef struct cs_layout {
+    size_t total_bytes;
+    size_t counters;          /* uint32[16]: [0] n_visible [1] n_pairs [2] overflow */
+    size_t records;           /* float[n][rec_floats] per-convex blend records */
+    size_t hull;              /* uint8[n][max_k]  hull cycle (indices into the K points) */
+    size_t bbox;              /* int32[n][4]  x0,x1,y0,y1 half-open pixel rect */
+    size_t depth_keys;        /* uint64[n]    f64 bits of the centre depth (~0 culled) */
+    size_t order;             /* uint32[n]    convex ids sorted by (depth, id); first n_visible valid */
+    size_t tiles_touched;     /* uint32[n] */
+    size_t pair_offsets;      /* uint32[n+1]  exclusive scan of tiles_touched in depth order */
+    size_t pair_tiles;        /* uint32[cap]  sorted tile id of each (tile, convex) pair */
+    size_t pair_ids;          /* uint32[cap]  convex id of each pair (tile-major, depth order) */
+    size_t tile_ranges;       /* uint32[tiles][2]  [start,end) into the pair arrays */
+    size_t pixel_last;        /* int32[H*W]  pair index of the last blended candidate (-1 none) */
+    size_t pixel_clamp;       /* uint8[H*W]  bit c set iff channel c of C+T*bg lies in [0,1] */
+    size_t grad_accum;        /* float[n][acc_floats] screen-space gradient accumulators */
+    size_t scratch;           /* private sort/scan scratch */
+    size_t scratch_bytes;
+    int32_t rec_floats, acc_floats, max_k, tiles_x, tiles_y, reserved;
+} cs_layout;
+
+CS_API int cs_abi_version(void);
+CS_API const char *cs_error_string(int code);
+
+/* Workspace size/layout for a frame of this camera at n convexes of k points
+ * and room for `pair_capacity` (tile, convex) pairs. Host-only, no CUDA. */
+CS_API int cs_workspace_layout(const cs_camera *cam, const cs_settings *set, int64_t n, int32_t k,
+                        int64_t pair_capacity, cs_layout *out);
+
+/* Forward render.  Replaces rasterize.render (rasterize.py:156-209) including
+ * prepare_view (rasterize.py:77-122) and bin_tiles (rasterize.py:134-144).
+ * Stream-ordered; writes the frame and keeps, inside the workspace, what the
+ * backward needs.  If the pairs overflow pair_capacity the frame is invalid
+ * and counters[2] != 0: read counters[1] (the required pairs), grow the
+ * workspace and call again. */
+CS_API int cs_forward(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+               void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+               const cs_frame *frame, void *stream);
+
+/* Backward.  Replaces backward.backward (backward.py:76-212) and
+ * _accumulate_primitive_grads (backward.py:215-282).  Needs the workspace of
+ * the cs_forward call for the same (camera, settings, params). */
+CS_API int cs_backward(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                const float *d_image /*[H,W,3]*/, const cs_grads *grads, void *stream);
+
+/* Stage-wise forward for profiling and pipelining: stage 0 = preprocess
+ * (prepare_view), 1 = depth order + tile binning (sort + bin_tiles), 2 =
+ * blend.  cs_forward == stages 0..2.  Later stages need the earlier ones to
+ * have run on the same workspace. */
+CS_API int cs_forward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                             void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                             const cs_frame *frame, int32_t first_stage, int32_t last_stage, void *stream);
+
+/* Stage-wise backward: stage 0 = backward blend (screen-space gradients),
+ * 1 = per-convex chain to the raw parameters.  cs_backward == stages 0..1. */
+CS_API int cs_backward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                              void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                              const float *d_image, const cs_grads *grads, int32_t first_stage,
+                              int32_t last_stage, void *stream);
+
+/* Convenience: copy counters[0..3] to host (synchronises `stream`). */
+CS_API int cs_read_counters(const void *workspace, uint32_t *host_out4, void *stream);
+
+/* Batched 2-D hull.  Replaces projection.graham_scan (projection.py:47-113)
+ * on m point sets of up to npts (<= 32) float64 points: pts [m,npts,2],
+ * counts [m] points used per set (NULL = npts); hull [m,npts] (-1 padded),
+ * hull_n [m] (0 == None). */
+CS_API int cs_graham_scan_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts,
+                         int32_t *hull, int32_t *hull_n, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONVEXSPLAT_B200_H */

@@ -1,0 +1,100 @@
+"""ctypes binding of libconvexsplat_sm100.so (include/convexsplat_b200.h).
+
+There is no CPU fallback: if the library is missing or cannot be loaded the
+import of the renderer fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libconvexsplat_sm100.so")
+
+EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forward", "cs_backward",
+           "cs_forward_stages", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch")
+ABI_VERSION = 1
+
+_vp = ctypes.c_void_p
+
+
+class CsCamera(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_double), ("fy", ctypes.c_double), ("cx", ctypes.c_double),
+                ("cy", ctypes.c_double), ("R", ctypes.c_double * 9), ("t", ctypes.c_double * 3),
+                ("z_near", ctypes.c_double), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("ortho", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class CsSettings(ctypes.Structure):
+    _fields_ = [("cutoff", ctypes.c_double), ("floor", ctypes.c_double),
+                ("background", ctypes.c_double * 3), ("tile", ctypes.c_int32),
+                ("sh_degree", ctypes.c_int32), ("scaling_mode", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class CsParams(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("k", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("points", _vp), ("raw_delta", _vp), ("raw_sigma", _vp), ("raw_opacity", _vp),
+                ("raw_mask", _vp), ("sh", _vp)]
+
+
+class CsFrame(ctypes.Structure):
+    _fields_ = [("image", _vp), ("final_T", _vp), ("count", _vp), ("weight_sum", _vp),
+                ("depth", _vp), ("visible", _vp)]
+
+
+class CsGrads(ctypes.Structure):
+    _fields_ = [("d_points", _vp), ("d_raw_delta", _vp), ("d_raw_sigma", _vp),
+                ("d_raw_opacity", _vp), ("d_raw_mask", _vp), ("d_sh", _vp)]
+
+
+class CsLayout(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_size_t) for name in (
+        "total_bytes", "counters", "records", "hull", "bbox", "depth_keys", "order", "tiles_touched",
+        "pair_offsets", "pair_tiles", "pair_ids", "tile_ranges", "pixel_last", "pixel_clamp",
+        "grad_accum", "scratch", "scratch_bytes")] + [
+        (name, ctypes.c_int32) for name in ("rec_floats", "acc_floats", "max_k", "tiles_x", "tiles_y",
+                                            "reserved")]
+
+
+class CsError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and type the library.  Raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise CsError(f"{path} is missing: run `python -m paper_2411_14974_b200.build` "
+                      "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    L.cs_abi_version.restype = ctypes.c_int
+    L.cs_error_string.restype = ctypes.c_char_p
+    L.cs_error_string.argtypes = [ctypes.c_int]
+    L.cs_workspace_layout.argtypes = [ctypes.POINTER(CsCamera), ctypes.POINTER(CsSettings), ctypes.c_int64,
+                                      ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(CsLayout)]
+    L.cs_forward.argtypes = [ctypes.POINTER(CsCamera), ctypes.POINTER(CsSettings), ctypes.POINTER(CsParams),
+                             _vp, ctypes.c_size_t, ctypes.c_int64, ctypes.POINTER(CsFrame), _vp]
+    L.cs_backward.argtypes = [ctypes.POINTER(CsCamera), ctypes.POINTER(CsSettings), ctypes.POINTER(CsParams),
+                              _vp, ctypes.c_size_t, ctypes.c_int64, _vp, ctypes.POINTER(CsGrads), _vp]
+    L.cs_forward_stages.argtypes = L.cs_forward.argtypes[:-1] + [ctypes.c_int32, ctypes.c_int32, _vp]
+    L.cs_backward_stages.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.c_int32, ctypes.c_int32, _vp]
+    L.cs_read_counters.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), _vp]
+    L.cs_graham_scan_batch.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]
+    for fn in ("cs_workspace_layout", "cs_forward", "cs_backward", "cs_forward_stages", "cs_backward_stages",
+               "cs_read_counters", "cs_graham_scan_batch"):
+        getattr(L, fn).restype = ctypes.c_int
+    if L.cs_abi_version() != ABI_VERSION:
+        raise CsError(f"ABI mismatch: library {L.cs_abi_version()} != {ABI_VERSION}")
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        raise CsError(f"{what}: {load().cs_error_string(rc).decode()} (code {rc})")

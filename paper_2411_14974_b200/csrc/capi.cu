@@ -1,0 +1,153 @@
+// extern "C" boundary of libconvexsplat_sm100.so (include/convexsplat_b200.h).
+#include <cstring>
+
+#include "common.cuh"
+
+namespace cs {
+struct Scratch;
+}
+
+namespace {
+
+int validate(const cs_camera *cam, const cs_settings *set, int64_t n, int32_t k) {
+  if (!cam || !set) return CS_ERR_ARG;
+  if (n < 0 || n > (int64_t)0x7fffffff) return CS_ERR_ARG;
+  if (k < 3 || k > 16) return CS_ERR_ARG;
+  if (cam->width <= 0 || cam->height <= 0) return CS_ERR_ARG;
+  if (cam->width > 32767 || cam->height > 32767) return CS_ERR_UNSUPPORTED;  // 16-bit bbox packing
+  if (set->tile != cs::kTile) return CS_ERR_UNSUPPORTED;
+  if (set->sh_degree < 0 || set->sh_degree > 3) return CS_ERR_UNSUPPORTED;
+  if (set->scaling_mode < 0 || set->scaling_mode > 3) return CS_ERR_ARG;
+  return CS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cs_abi_version(void) { return CS_ABI_VERSION; }
+
+const char *cs_error_string(int code) {
+  switch (code) {
+    case CS_OK: return "ok";
+    case CS_ERR_ARG: return "bad argument";
+    case CS_ERR_CUDA: return "CUDA launch failure";
+    case CS_ERR_WORKSPACE: return "workspace too small";
+    case CS_ERR_UNSUPPORTED: return "unsupported setting (tile size must be 16, sh_degree 0..3)";
+    default: return "unknown error";
+  }
+}
+
+int cs_workspace_layout(const cs_camera *cam, const cs_settings *set, int64_t n, int32_t k,
+                        int64_t pair_capacity, cs_layout *out) {
+  int rc = validate(cam, set, n, k);
+  if (rc) return rc;
+  if (!out || pair_capacity < 0 || pair_capacity > (int64_t)0x3fffffff) return CS_ERR_ARG;
+  cs_layout L;
+  std::memset(&L, 0, sizeof(L));
+  L.max_k = k <= 8 ? 8 : 16;
+  L.rec_floats = cs::R_HEADER + 3 * L.max_k;
+  L.acc_floats = cs::A_LINES + 3 * L.max_k;
+  L.tiles_x = (cam->width + cs::kTile - 1) / cs::kTile;
+  L.tiles_y = (cam->height + cs::kTile - 1) / cs::kTile;
+  const int tiles = L.tiles_x * L.tiles_y;
+  const int pp = cs::pair_sort_passes(tiles);
+  if (pp > 3) return CS_ERR_UNSUPPORTED;
+  const size_t npix = (size_t)cam->width * cam->height;
+  const size_t un = (size_t)n, cap = (size_t)pair_capacity;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = cs::align_up(off + bytes, 256); return o; };
+  L.counters = take(sizeof(uint32_t) * cs::C_COUNT);
+  L.records = take(sizeof(float) * un * L.rec_floats);
+  L.hull = take(un * L.max_k);
+  L.bbox = take(sizeof(int32_t) * 4 * un);
+  L.depth_keys = take(sizeof(uint64_t) * un);
+  L.order = take(sizeof(uint32_t) * un);
+  L.tiles_touched = take(sizeof(uint32_t) * un);
+  L.pair_offsets = take(sizeof(uint32_t) * (un + 1));
+  L.pair_tiles = take(sizeof(uint32_t) * cap);
+  L.pair_ids = take(sizeof(uint32_t) * cap);
+  L.tile_ranges = take(sizeof(uint32_t) * 2 * tiles);
+  L.pixel_last = take(sizeof(int32_t) * npix);
+  L.pixel_clamp = take(npix);
+  L.grad_accum = take(sizeof(float) * un * L.acc_floats);
+  L.scratch_bytes = cs::scratch_bytes(n, pair_capacity, pp, nullptr, nullptr);
+  L.scratch = take(L.scratch_bytes);
+  L.total_bytes = off;
+  *out = L;
+  return CS_OK;
+}
+
+int cs_forward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                      size_t workspace_bytes, int64_t pair_capacity, const cs_frame *frame, int32_t first_stage,
+                      int32_t last_stage, void *stream) {
+  if (!params || !frame || !workspace) return CS_ERR_ARG;
+  if (first_stage < 0 || last_stage > 2 || first_stage > last_stage) return CS_ERR_ARG;
+  cs_layout L;
+  int rc = cs_workspace_layout(cam, set, params->n, params->k, pair_capacity, &L);
+  if (rc) return rc;
+  if (workspace_bytes < L.total_bytes) return CS_ERR_WORKSPACE;
+  if (!frame->image || !frame->final_T || !frame->count || !frame->weight_sum) return CS_ERR_ARG;
+  if (params->n > 0 && (!params->points || !params->raw_delta || !params->raw_sigma || !params->raw_opacity ||
+                        !params->raw_mask || !params->sh))
+    return CS_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char *ws = static_cast<char *>(workspace);
+  if (first_stage <= 0 && last_stage >= 0) {
+    cudaMemsetAsync(ws + L.counters, 0, sizeof(uint32_t) * cs::C_COUNT, s);
+    if ((rc = cs::launch_preprocess(*cam, *set, *params, L, ws, s))) return rc;
+  }
+  if (first_stage <= 1 && last_stage >= 1)
+    if ((rc = cs::launch_binning(*cam, *set, *params, L, ws, pair_capacity, s))) return rc;
+  if (first_stage <= 2 && last_stage >= 2)
+    if ((rc = cs::launch_forward_blend(*cam, *set, *params, L, ws, *frame, s))) return rc;
+  return CS_OK;
+}
+
+int cs_forward(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+               size_t workspace_bytes, int64_t pair_capacity, const cs_frame *frame, void *stream) {
+  return cs_forward_stages(cam, set, params, workspace, workspace_bytes, pair_capacity, frame, 0, 2, stream);
+}
+
+int cs_backward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                       size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
+                       int32_t first_stage, int32_t last_stage, void *stream) {
+  if (!params || !grads || !workspace || !d_image) return CS_ERR_ARG;
+  if (first_stage < 0 || last_stage > 1 || first_stage > last_stage) return CS_ERR_ARG;
+  cs_layout L;
+  int rc = cs_workspace_layout(cam, set, params->n, params->k, pair_capacity, &L);
+  if (rc) return rc;
+  if (workspace_bytes < L.total_bytes) return CS_ERR_WORKSPACE;
+  if (params->n > 0 && (!grads->d_points || !grads->d_raw_delta || !grads->d_raw_sigma ||
+                        !grads->d_raw_opacity || !grads->d_raw_mask || !grads->d_sh))
+    return CS_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char *ws = static_cast<char *>(workspace);
+  if (first_stage == 0)
+    if ((rc = cs::launch_backward_blend(*cam, *set, *params, L, ws, d_image, s))) return rc;
+  if (last_stage == 1) return cs::launch_chain(*cam, *set, *params, L, ws, *grads, s);
+  return CS_OK;
+}
+
+int cs_backward(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
+                void *stream) {
+  return cs_backward_stages(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, 0, 1,
+                            stream);
+}
+
+int cs_read_counters(const void *workspace, uint32_t *host_out4, void *stream) {
+  if (!workspace || !host_out4) return CS_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(host_out4, workspace, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return CS_ERR_CUDA;
+  return cudaStreamSynchronize(s) == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+}
+
+int cs_graham_scan_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts, int32_t *hull,
+                         int32_t *hull_n, void *stream) {
+  if (m < 0 || npts < 0 || npts > 32 || (m > 0 && (!pts || !hull || !hull_n))) return CS_ERR_ARG;
+  return cs::launch_hull_batch(m, npts, counts, pts, hull, hull_n, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// Shared definitions of the sm_100a convex-splatting kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/convexsplat_b200.h"
+
+namespace cs {
+
+constexpr int kTile = 16;                 // rasterize.py:23 TILE_SIZE (only 16 supported)
+constexpr int kTilePixels = kTile * kTile;
+constexpr int kShCoeffs = 16;             // model.py:15
+constexpr double kMaskGate = 0.01;        // rasterize.py:26
+constexpr double kCrossTol = 1e-9;        // projection.py:19
+constexpr double kAlphaMaxD = 1.0 - 1e-6; // rasterize.py:30
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr uint64_t kCulledKey = ~0ull;
+
+// ---------------------------------------------------------------------------
+// Per-convex blend record (float32), written by the preprocess kernel and
+// read by both blend kernels.  Line j evaluates, in log2 units,
+//   z2_j(q) = A_j*(qx-ax) + B_j*(qy-ay) + C_j = delta_s*log2(e)*L_j(q)
+// where L_j = n_j.q + off_j is the reference's signed line distance
+// (projection.py:131-133) and (ax, ay) an integer anchor inside the bbox
+// (keeps fp32 cancellation out of 1080p coordinates).
+enum RecField {
+  R_AX = 0, R_AY = 1, R_SIGMA = 2, R_OPACITY = 3, R_R = 4, R_G = 5, R_B = 6, R_DEPTH = 7,
+  R_ONE_MINUS_O = 8, R_DLS = 9, R_NLINES = 10, R_BBX = 11, R_BBY = 12, R_HEADER = 16
+};
+template <int MAXK> struct Rec {
+  static constexpr int kFloats = R_HEADER + 3 * MAXK;   // 40 for MAXK=8, multiple of 4
+  static_assert(kFloats % 4 == 0, "record must be float4 aligned");
+};
+
+// Screen-space gradient accumulators per convex (backward.py:102-108):
+//   d_color(3), d_opacity_eff, d_sigma_s, d_delta_s, pad(2), then per line
+//   (sum dL*(qx-ax), sum dL*(qy-ay), sum dL).
+enum AccField { A_DC = 0, A_DOEFF = 3, A_DSIG = 4, A_DDEL = 5, A_LINES = 8 };
+template <int MAXK> struct Acc {
+  static constexpr int kFloats = A_LINES + 3 * MAXK;
+};
+
+// Counters at the head of the workspace.
+enum Counter { C_NVISIBLE = 0, C_NPAIRS = 1, C_OVERFLOW = 2, C_NSORT = 3, C_CHUNK0 = 4, C_COUNT = 16 };
+
+struct Layout {
+  cs_layout l;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Order-preserving map of a double to uint64 (ascending).
+__device__ __forceinline__ uint64_t orderable_bits(double d) {
+  if (d == 0.0) d = 0.0;  // -0.0 ties +0.0 as in Python's sort
+  uint64_t b = (uint64_t)__double_as_longlong(d);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Pixel of a 16x16 tile handled by thread t: warps cover 8x4 sub-blocks so
+// a warp's pixels form a compact square (better bbox culling per warp).
+__device__ __forceinline__ void tile_pixel(int t, int &lx, int &ly) {
+  int warp = t >> 5, lane = t & 31;
+  lx = ((warp & 1) << 3) | (lane & 7);
+  ly = ((warp >> 1) << 2) | (lane >> 3);
+}
+
+}  // namespace cs
+
+// Entry points implemented in the .cu files (host side, C++ linkage).
+namespace cs {
+int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_params &p,
+                      const cs_layout &L, char *ws, cudaStream_t s);
+int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params &p,
+                   const cs_layout &L, char *ws, int64_t cap, cudaStream_t s);
+int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
+                         const cs_layout &L, char *ws, const cs_frame &f, cudaStream_t s);
+int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
+                          const cs_layout &L, char *ws, const float *d_image, cudaStream_t s);
+int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
+                 const cs_layout &L, char *ws, const cs_grads &g, cudaStream_t s);
+int launch_hull_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts,
+                      int32_t *hull, int32_t *hull_n, cudaStream_t s);
+size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, struct Scratch *sc, char *base);
+int pair_sort_passes(int tiles);
+}  // namespace cs

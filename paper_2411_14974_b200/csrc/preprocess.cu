@@ -1,0 +1,394 @@
+// K1: per-convex preprocess (one thread per convex).
+//
+// Replaces the Python loop of rasterize.prepare_view (rasterize.py:88-120):
+// mask gate (model.py:105-107), projection (projection.py:22-40), Graham-scan
+// hull (projection.py:47-113), hull lines (projection.py:116-128), depth and
+// depth scaling (rasterize.py:99-103, field.py:26-35), screen bbox with the
+// cutoff margin (projection.py:136-177) and SH colour (harmonics.py:101-109).
+//
+// Everything that feeds a DISCRETE decision (cull, hull cycle, bbox, depth
+// order) is computed in float64 with the reference's operation order; this
+// translation unit is compiled with --fmad=false so that only the explicit
+// fma() of the projection (OpenBLAS dgemm order of `points @ R.T`) fuses.
+// Outputs are a float32 blend record per convex plus the discrete results.
+#include "common.cuh"
+
+namespace cs {
+
+struct PreArgs {
+  cs_camera cam;
+  int64_t n;
+  int k;
+  int sh_degree;
+  int mode;
+  double cutoff;
+  const float *points, *raw_delta, *raw_sigma, *raw_opacity, *raw_mask, *sh;
+  float *records;
+  uint8_t *hull;
+  int4 *bbox;
+  uint64_t *depth_keys;
+  uint32_t *order;
+  uint32_t *touched;
+  uint32_t *counters;
+  double cam_center[3];
+};
+
+// projection.py:43-44 -- no contraction (TU built with --fmad=false)
+__device__ __forceinline__ double cross_d(const double *X, const double *Y, int o, int a, int b) {
+  return (X[a] - X[o]) * (Y[b] - Y[o]) - (Y[a] - Y[o]) * (X[b] - X[o]);
+}
+
+// comparator of projection.py:73-85 reduced to "cmp(a, b) < 0"
+__device__ __forceinline__ bool hull_lt(const double *X, const double *Y, int ref, int a, int b) {
+  double c = cross_d(X, Y, ref, a, b);
+  if (c > kCrossTol) return true;
+  if (c < -kCrossTol) return false;
+  double ax = X[a] - X[ref], ay = Y[a] - Y[ref];
+  double bx = X[b] - X[ref], by = Y[b] - Y[ref];
+  return (ax * ax + ay * ay) < (bx * bx + by * by);
+}
+
+// projection.py:47-113.  The sort reproduces CPython's list.sort for fewer
+// than 64 items (count_run + binary insertion), because the tolerance
+// comparator is not a strict weak order and the result depends on the
+// algorithm.  Returns the hull size (0 == None); out[] gets the CCW cycle
+// starting at the reference point.
+template <int NP>
+__device__ int graham_scan_dev(int n, const double *X, const double *Y, int *out) {
+  if (n < 3) return 0;
+  int uq[NP];
+  int nu = 0;
+  for (int i = 0; i < n; i++) {
+    bool dup = false;
+    for (int j = 0; j < nu; j++) {
+      int u = uq[j];
+      if (X[u] == X[i] && Y[u] == Y[i]) { dup = true; break; }
+    }
+    if (!dup) uq[nu++] = i;
+  }
+  if (nu < 3) return 0;
+  int ref = uq[0];
+  for (int j = 1; j < nu; j++) {
+    int u = uq[j];
+    if (Y[u] < Y[ref] || (Y[u] == Y[ref] && X[u] < X[ref])) ref = u;
+  }
+  int rest[NP];
+  int m = 0;
+  for (int j = 0; j < nu; j++)
+    if (uq[j] != ref) rest[m++] = uq[j];
+  if (m >= 2) {
+    int run = 2;
+    if (hull_lt(X, Y, ref, rest[1], rest[0])) {
+      while (run < m && hull_lt(X, Y, ref, rest[run], rest[run - 1])) run++;
+      for (int a = 0, b = run - 1; a < b; a++, b--) { int t = rest[a]; rest[a] = rest[b]; rest[b] = t; }
+    } else {
+      while (run < m && !hull_lt(X, Y, ref, rest[run], rest[run - 1])) run++;
+    }
+    for (int start = run; start < m; start++) {
+      int pivot = rest[start];
+      int l = 0, r = start;
+      do {
+        int p = l + ((r - l) >> 1);
+        if (hull_lt(X, Y, ref, pivot, rest[p])) r = p; else l = p + 1;
+      } while (l < r);
+      for (int p = start; p > l; p--) rest[p] = rest[p - 1];
+      rest[l] = pivot;
+    }
+  }
+  int st[NP];
+  int sn = 0;
+  st[sn++] = ref;
+  for (int j = 0; j < m; j++) {
+    int c = rest[j];
+    while (sn >= 2 && cross_d(X, Y, st[sn - 2], st[sn - 1], c) <= kCrossTol) sn--;
+    st[sn++] = c;
+  }
+  bool changed = true;
+  while (changed && sn >= 3) {
+    changed = false;
+    for (int q = 0; q < sn; q++) {
+      int a = st[(q - 1 + sn) % sn], b = st[q], c = st[(q + 1) % sn];
+      if (cross_d(X, Y, a, b, c) <= kCrossTol) {
+        for (int r = q; r < sn - 1; r++) st[r] = st[r + 1];
+        sn--;
+        changed = true;
+        break;
+      }
+    }
+  }
+  if (sn < 3) return 0;
+  int start = 0;
+  for (int q = 0; q < sn; q++)
+    if (st[q] == ref) { start = q; break; }
+  for (int q = 0; q < sn; q++) out[q] = st[(start + q) % sn];
+  return sn;
+}
+
+// harmonics.py:7-24 constants
+__constant__ double kSH_C0 = 0.28209479177387814;
+__constant__ double kSH_C1 = 0.4886025119029199;
+__constant__ double kSH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                 -1.0925484305920792, 0.5462742152960396};
+__constant__ double kSH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                                 0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                                 -0.5900435899266435};
+
+// harmonics.py:33-59
+__device__ __forceinline__ void sh_basis(double x, double y, double z, int deg, double *b) {
+  b[0] = kSH_C0;
+  if (deg >= 1) { b[1] = -kSH_C1 * y; b[2] = kSH_C1 * z; b[3] = -kSH_C1 * x; }
+  if (deg >= 2) {
+    double xx = x * x, yy = y * y, zz = z * z;
+    b[4] = kSH_C2[0] * x * y;
+    b[5] = kSH_C2[1] * y * z;
+    b[6] = kSH_C2[2] * (2.0 * zz - xx - yy);
+    b[7] = kSH_C2[3] * x * z;
+    b[8] = kSH_C2[4] * (xx - yy);
+  }
+  if (deg >= 3) {
+    double xx = x * x, yy = y * y, zz = z * z;
+    b[9] = kSH_C3[0] * y * (3.0 * xx - yy);
+    b[10] = kSH_C3[1] * x * y * z;
+    b[11] = kSH_C3[2] * y * (4.0 * zz - xx - yy);
+    b[12] = kSH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    b[13] = kSH_C3[4] * x * (4.0 * zz - xx - yy);
+    b[14] = kSH_C3[5] * z * (xx - yy);
+    b[15] = kSH_C3[6] * x * (xx - 3.0 * yy);
+  }
+}
+
+__device__ __forceinline__ double depth_scale(int mode, double d) {  // field.py:26-35
+  switch (mode) {
+    case CS_SCALE_NONE: return 1.0;
+    case CS_SCALE_SQRT: return sqrt(d);
+    case CS_SCALE_DEPTH: return d;
+    default: return d * d;
+  }
+}
+
+constexpr int kPreThreads = 128;
+
+// One convex.  pts_s / sh_s point at this convex's rows staged in smem.
+template <int MAXK>
+__device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, const float *sh_g) {
+  const int k = a.k;
+  uint8_t *hull_out = a.hull + i * MAXK;
+  a.touched[i] = 0u;
+  a.depth_keys[i] = kCulledKey;
+  a.order[i] = (uint32_t)i;
+  // rasterize.py:89 mask gate (model.py:105-107, expit = 1/(1+exp(-x)))
+  double mask = 1.0 / (1.0 + exp(-(double)a.raw_mask[i]));
+  if (mask <= kMaskGate) return false;
+  // projection.py:22-40
+  double X[MAXK], Y[MAXK];
+  double zsum = 0.0;
+  bool culled = false;
+  const double *R = a.cam.R;
+  for (int j = 0; j < k; j++) {
+    double p0 = pts_s[3 * j], p1 = pts_s[3 * j + 1], p2 = pts_s[3 * j + 2];
+    double xc = fma(p2, R[2], fma(p1, R[1], p0 * R[0])) + a.cam.t[0];
+    double yc = fma(p2, R[5], fma(p1, R[4], p0 * R[3])) + a.cam.t[1];
+    double zc = fma(p2, R[8], fma(p1, R[7], p0 * R[6])) + a.cam.t[2];
+    if (zc <= a.cam.z_near) culled = true;
+    zsum = zsum + zc;  // rasterize.py:99 mean, left-to-right
+    if (a.cam.ortho) {
+      X[j] = a.cam.fx * xc + a.cam.cx;
+      Y[j] = a.cam.fy * yc + a.cam.cy;
+    } else {
+      X[j] = (a.cam.fx * xc) / zc + a.cam.cx;
+      Y[j] = (a.cam.fy * yc) / zc + a.cam.cy;
+    }
+  }
+  if (culled) return false;
+  int hidx[MAXK];
+  const int h = graham_scan_dev<MAXK>(k, X, Y, hidx);
+  if (h == 0) return false;
+  // projection.py:116-128
+  double nx[MAXK], ny[MAXK], off[MAXK];
+  for (int j = 0; j < h; j++) {
+    int u = hidx[j], v = hidx[(j + 1) % h];
+    double ex = X[v] - X[u], ey = Y[v] - Y[u];
+    double rx = ey, ry = -ex;
+    double len = sqrt(rx * rx + ry * ry);
+    nx[j] = rx / len;
+    ny[j] = ry / len;
+    off[j] = -(nx[j] * X[u] + ny[j] * Y[u]);
+  }
+  // rasterize.py:99-103
+  const double depth = zsum / k;
+  const double s = depth_scale(a.mode, a.cam.ortho ? 1.0 : depth);
+  const double delta_s = s * exp((double)a.raw_delta[i]);
+  const double sigma_s = s * exp((double)a.raw_sigma[i]);
+  const double ro = (double)a.raw_opacity[i];
+  const double o = 1.0 / (1.0 + exp(-ro));
+  // projection.py:136-177
+  if (o <= a.cutoff) return false;
+  int x0, x1, y0, y1;
+  if (a.cutoff <= 0.0) {
+    x0 = 0; x1 = a.cam.width; y0 = 0; y1 = a.cam.height;
+  } else {
+    double eps = a.cutoff / o;
+    if (0.5 < eps) eps = 0.5;
+    const double margin = log((1.0 - eps) / eps) / (sigma_s * delta_s);
+    double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+    for (int j = 0; j < h; j++) {
+      int pj = (j - 1 + h) % h;
+      double den = 1.0 + (nx[pj] * nx[j] + ny[pj] * ny[j]);
+      if (!(den >= 1e-12)) den = 1e-12;
+      double ix = X[hidx[j]] + (margin * (nx[pj] + nx[j])) / den;
+      double iy = Y[hidx[j]] + (margin * (ny[pj] + ny[j])) / den;
+      xmin = fmin(xmin, ix); xmax = fmax(xmax, ix);
+      ymin = fmin(ymin, iy); ymax = fmax(ymax, iy);
+    }
+    double fx0 = ceil(xmin - 0.5), fx1 = floor(xmax - 0.5) + 1.0;
+    double fy0 = ceil(ymin - 0.5), fy1 = floor(ymax - 0.5) + 1.0;
+    fx0 = fmax(fx0, 0.0); fy0 = fmax(fy0, 0.0);
+    fx1 = fmin(fx1, (double)a.cam.width); fy1 = fmin(fy1, (double)a.cam.height);
+    if (!(fx0 < fx1) || !(fy0 < fy1)) return false;
+    x0 = (int)fx0; x1 = (int)fx1; y0 = (int)fy0; y1 = (int)fy1;
+  }
+  // rasterize.py:110-114 view direction from the point mean (model.py:109-111)
+  double cx = 0.0, cy = 0.0, cz = 0.0;
+  for (int j = 0; j < k; j++) {
+    cx = cx + (double)pts_s[3 * j];
+    cy = cy + (double)pts_s[3 * j + 1];
+    cz = cz + (double)pts_s[3 * j + 2];
+  }
+  double vx = cx / k - a.cam_center[0], vy = cy / k - a.cam_center[1], vz = cz / k - a.cam_center[2];
+  double dist = sqrt(vx * vx + vy * vy + vz * vz);
+  double dx = 0.0, dy = 0.0, dz = 1.0;
+  if (dist > 0.0) { dx = vx / dist; dy = vy / dist; dz = vz / dist; }
+  double basis[kShCoeffs];
+  sh_basis(dx, dy, dz, a.sh_degree, basis);
+  const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
+  double col[3];
+  for (int c = 0; c < 3; c++) {
+    double acc = 0.0;
+    for (int b = 0; b < nb; b++) acc += basis[b] * (double)__ldg(sh_g + 3 * b + c);
+    double raw = 0.5 + acc;
+    col[c] = raw > 0.0 ? raw : 0.0;   // harmonics.py:108-109
+  }
+
+  // ---- outputs ----
+  for (int j = 0; j < MAXK; j++) hull_out[j] = (uint8_t)(j < h ? hidx[j] : 0xff);
+  a.bbox[i] = make_int4(x0, x1, y0, y1);
+  a.touched[i] = (uint32_t)(((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1));
+  a.depth_keys[i] = orderable_bits(depth);
+
+  constexpr int RF = Rec<MAXK>::kFloats;
+  float rec[RF];
+  const int ax = (x0 + x1) >> 1, ay = (y0 + y1) >> 1;
+  const double dls = delta_s * 1.4426950408889634;  // delta_s * log2(e)
+  rec[R_AX] = (float)ax;
+  rec[R_AY] = (float)ay;
+  rec[R_SIGMA] = (float)sigma_s;
+  rec[R_OPACITY] = (float)o;
+  rec[R_R] = (float)col[0];
+  rec[R_G] = (float)col[1];
+  rec[R_B] = (float)col[2];
+  rec[R_DEPTH] = (float)depth;
+  rec[R_ONE_MINUS_O] = (float)(1.0 / (1.0 + exp(ro)));
+  rec[R_DLS] = (float)dls;
+  rec[R_NLINES] = __int_as_float(h);
+  rec[R_BBX] = __int_as_float(x0 | (x1 << 16));
+  rec[R_BBY] = __int_as_float(y0 | (y1 << 16));
+  for (int f = 13; f < R_HEADER; f++) rec[f] = 0.f;
+  for (int j = 0; j < MAXK; j++) {
+    if (j < h) {
+      double c = off[j] + nx[j] * ax + ny[j] * ay;  // anchor-relative offset, fp64
+      rec[R_HEADER + 3 * j] = (float)(dls * nx[j]);
+      rec[R_HEADER + 3 * j + 1] = (float)(dls * ny[j]);
+      rec[R_HEADER + 3 * j + 2] = (float)(dls * c);
+    } else {
+      rec[R_HEADER + 3 * j] = 0.f;
+      rec[R_HEADER + 3 * j + 1] = 0.f;
+      rec[R_HEADER + 3 * j + 2] = -INFINITY;
+    }
+  }
+  float4 *dst = reinterpret_cast<float4 *>(a.records + i * RF);
+#pragma unroll
+  for (int q = 0; q < RF / 4; q++) dst[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
+  return true;
+}
+
+template <int MAXK>
+__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreArgs a) {
+  extern __shared__ float pts_smem[];  // [kPreThreads][k*3]
+  const int64_t base = (int64_t)blockIdx.x * kPreThreads;
+  const int rowf = a.k * 3;
+  const int64_t nblk = min((int64_t)kPreThreads, a.n - base);
+  // coalesced staging of this block's points
+  const float *src = a.points + base * rowf;
+  for (int q = threadIdx.x; q < nblk * rowf; q += kPreThreads) pts_smem[q] = src[q];
+  __syncthreads();
+  const int64_t i = base + threadIdx.x;
+  bool vis = false;
+  if (i < a.n) vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, a.sh + i * kShCoeffs * 3);
+  unsigned b = __ballot_sync(0xffffffffu, vis);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&a.counters[C_NVISIBLE], (unsigned)__popc(b));
+}
+
+// cs_graham_scan_batch: one thread per point set.
+__global__ void hull_batch_kernel(int m, int npts, const int32_t *counts, const double *pts,
+                                  int32_t *hull, int32_t *hull_n) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  int n = counts ? counts[s] : npts;
+  double X[32], Y[32];
+  for (int j = 0; j < n; j++) {
+    X[j] = pts[((int64_t)s * npts + j) * 2];
+    Y[j] = pts[((int64_t)s * npts + j) * 2 + 1];
+  }
+  int out[32];
+  int h = graham_scan_dev<32>(n, X, Y, out);
+  for (int j = 0; j < npts; j++) hull[(int64_t)s * npts + j] = j < h ? out[j] : -1;
+  hull_n[s] = h;
+}
+
+static void camera_center(const cs_camera &cam, double *c) {  // model.py:164-166
+  for (int j = 0; j < 3; j++) {
+    double s = 0.0;
+    for (int r = 0; r < 3; r++) s += (-cam.R[3 * r + j]) * cam.t[r];
+    c[j] = s;
+  }
+}
+
+int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_params &p,
+                      const cs_layout &L, char *ws, cudaStream_t s) {
+  if (p.n == 0) return CS_OK;
+  PreArgs a;
+  a.cam = cam;
+  a.n = p.n;
+  a.k = p.k;
+  a.sh_degree = set.sh_degree;
+  a.mode = set.scaling_mode;
+  a.cutoff = set.cutoff;
+  a.points = p.points; a.raw_delta = p.raw_delta; a.raw_sigma = p.raw_sigma;
+  a.raw_opacity = p.raw_opacity; a.raw_mask = p.raw_mask; a.sh = p.sh;
+  a.records = reinterpret_cast<float *>(ws + L.records);
+  a.hull = reinterpret_cast<uint8_t *>(ws + L.hull);
+  a.bbox = reinterpret_cast<int4 *>(ws + L.bbox);
+  a.depth_keys = reinterpret_cast<uint64_t *>(ws + L.depth_keys);
+  a.order = reinterpret_cast<uint32_t *>(ws + L.order);
+  a.touched = reinterpret_cast<uint32_t *>(ws + L.tiles_touched);
+  a.counters = reinterpret_cast<uint32_t *>(ws + L.counters);
+  camera_center(cam, a.cam_center);
+  const int blocks = (int)((p.n + kPreThreads - 1) / kPreThreads);
+  const size_t smem = (size_t)kPreThreads * p.k * 3 * sizeof(float);
+  if (L.max_k == 8) {
+    preprocess_kernel<8><<<blocks, kPreThreads, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(preprocess_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    preprocess_kernel<16><<<blocks, kPreThreads, smem, s>>>(a);
+  }
+  return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+}
+
+int launch_hull_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts,
+                      int32_t *hull, int32_t *hull_n, cudaStream_t s) {
+  if (m <= 0) return CS_OK;
+  hull_batch_kernel<<<(m + 127) / 128, 128, 0, s>>>(m, npts, counts, pts, hull, hull_n);
+  return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+}
+
+}  // namespace cs

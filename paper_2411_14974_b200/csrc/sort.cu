@@ -1,0 +1,398 @@
+// K2: depth order + tile binning (rasterize.py:121 sort, rasterize.py:134-144).
+//
+//   depth sort   stable LSD radix sort of (orderable f64 depth bits, convex id)
+//                == Python's sort by (depth, index) (rasterize.py:121)
+//   scan         exclusive scan of tiles_touched in depth order -> pair offsets
+//   duplicate    every convex, visited in depth order, emits (tile, id) pairs
+//                for each tile of its bbox (the append loop of bin_tiles)
+//   pair sort    stable radix sort by tile id only: since pairs are emitted in
+//                depth order, a stable sort by tile gives exactly the reference
+//                per-tile lists in (depth, index) order
+//   ranges       [start, end) of every tile in the sorted pairs
+//
+// Both radix sorts are onesweep (Adinets & Merrill): one global histogram
+// pass, then one kernel per 8-bit digit that ranks keys with warp
+// __match_any_sync, publishes per-chunk digit counts and resolves its prefix
+// by decoupled look-back.
+#include "common.cuh"
+
+namespace cs {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 16;
+constexpr int kSortChunk = kSortThreads * kSortItems;  // 4096 keys per chunk
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagPrefix = 2u << 30;
+constexpr uint32_t kValueMask = (1u << 30) - 1;
+
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 4;
+constexpr int kScanChunk = kScanThreads * kScanItems;
+
+// ------------------------------------------------------------------ hist
+template <typename KeyT>
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const KeyT *keys, const uint32_t *count,
+                                                                   uint32_t n_fixed, int passes, int shift0,
+                                                                   uint32_t *hist) {
+  __shared__ uint32_t h[8][kRadix];
+  for (int q = threadIdx.x; q < passes * kRadix; q += kSortThreads) h[q / kRadix][q % kRadix] = 0;
+  __syncthreads();
+  const uint32_t n = count ? *count : n_fixed;
+  for (uint32_t idx = blockIdx.x * kSortThreads + threadIdx.x; idx < n; idx += gridDim.x * kSortThreads) {
+    KeyT k = keys[idx];
+    for (int p = 0; p < passes; p++) atomicAdd(&h[p][(uint32_t)(k >> (shift0 + p * kRadixBits)) & (kRadix - 1)], 1u);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < passes * kRadix; q += kSortThreads) {
+    uint32_t v = h[q / kRadix][q % kRadix];
+    if (v) atomicAdd(&hist[q], v);
+  }
+}
+
+// exclusive scan of each pass's 256-bin histogram (one block per pass)
+__global__ void radix_offsets_kernel(const uint32_t *hist, uint32_t *offsets) {
+  __shared__ uint32_t s[kRadix];
+  const int p = blockIdx.x, t = threadIdx.x;
+  s[t] = hist[p * kRadix + t];
+  __syncthreads();
+  for (int d = 1; d < kRadix; d <<= 1) {
+    uint32_t v = t >= d ? s[t - d] : 0;
+    __syncthreads();
+    s[t] += v;
+    __syncthreads();
+  }
+  offsets[p * kRadix + t] = s[t] - hist[p * kRadix + t];
+}
+
+// ------------------------------------------------------------------ onesweep pass
+template <typename KeyT>
+struct PassArgs {
+  const KeyT *keys_in;
+  KeyT *keys_out;
+  const uint32_t *vals_in;
+  uint32_t *vals_out;
+  const uint32_t *count;  // device item count (or null -> n_fixed)
+  uint32_t n_fixed;
+  int shift;
+  const uint32_t *offsets;  // [256] global exclusive digit offsets of this pass
+  uint32_t *lookback;       // [chunks][256]
+  uint32_t *chunk_counter;
+};
+
+template <typename KeyT>
+__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a) {
+  __shared__ uint32_t s_hist[kSortWarps][kRadix];
+  __shared__ uint32_t s_base[kRadix];
+  __shared__ uint32_t s_chunk;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) s_chunk = atomicAdd(a.chunk_counter, 1u);
+  for (int q = t; q < kSortWarps * kRadix; q += kSortThreads) s_hist[q / kRadix][q % kRadix] = 0;
+  __syncthreads();
+  const uint32_t chunk = s_chunk;
+  const uint32_t n = a.count ? *a.count : a.n_fixed;
+  const uint32_t start = chunk * kSortChunk;
+  if (start >= n) return;  // no later chunk holds items, nobody looks back here
+
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  KeyT key[kSortItems];
+  uint32_t val[kSortItems];
+  uint32_t dig[kSortItems];
+  uint32_t rank[kSortItems];
+  const uint32_t wbase = start + w * (32 * kSortItems);
+#pragma unroll
+  for (int i = 0; i < kSortItems; i++) {
+    uint32_t idx = wbase + i * 32 + lane;
+    bool valid = idx < n;
+    key[i] = valid ? a.keys_in[idx] : (KeyT)0;
+    val[i] = valid ? a.vals_in[idx] : 0u;
+    dig[i] = valid ? (uint32_t)(key[i] >> a.shift) & (kRadix - 1) : kRadix;
+  }
+#pragma unroll
+  for (int i = 0; i < kSortItems; i++) {
+    const uint32_t d = dig[i];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    uint32_t prev = 0;
+    if (d < kRadix) prev = s_hist[w][d];
+    __syncwarp();
+    if (d < kRadix && lane == __ffs(peers) - 1) s_hist[w][d] = prev + __popc(peers);
+    __syncwarp();
+    rank[i] = prev + __popc(peers & lt_mask);
+  }
+  __syncthreads();
+  {
+    // digit t: exclusive offsets across warps, chunk total, decoupled look-back
+    const int d = t;
+    uint32_t sum = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ww++) {
+      uint32_t v = s_hist[ww][d];
+      s_hist[ww][d] = sum;
+      sum += v;
+    }
+    volatile uint32_t *lb = a.lookback;
+    uint32_t excl = 0;
+    if (chunk == 0) {
+      lb[d] = kFlagPrefix | sum;
+    } else {
+      lb[chunk * kRadix + d] = kFlagAgg | sum;
+      int c = (int)chunk - 1;
+      while (true) {
+        uint32_t v = lb[c * kRadix + d];
+        uint32_t flag = v & ~kValueMask;
+        if (flag == 0) continue;
+        excl += v & kValueMask;
+        if (flag == kFlagPrefix) break;
+        c--;
+      }
+      lb[chunk * kRadix + d] = kFlagPrefix | (excl + sum);
+    }
+    s_base[d] = a.offsets[d] + excl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kSortItems; i++) {
+    const uint32_t d = dig[i];
+    if (d < kRadix) {
+      uint32_t pos = s_base[d] + s_hist[w][d] + rank[i];
+      a.keys_out[pos] = key[i];
+      a.vals_out[pos] = val[i];
+    }
+  }
+}
+
+// Full LSD sort over `passes` digits starting at bit shift0.  Ping-pongs
+// (k0,v0) <-> (k1,v1); returns true when the result ends in (k1,v1).
+template <typename KeyT>
+static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uint32_t *count,
+                       uint32_t n_fixed, uint32_t n_cap, int passes, int shift0, uint32_t *hist,
+                       uint32_t *offsets, uint32_t *lookback, uint32_t *chunk_counters, cudaStream_t s) {
+  const int chunks = (int)((n_cap + kSortChunk - 1) / kSortChunk);
+  if (chunks == 0) return false;
+  const int hist_blocks = min(chunks * 4, 148 * 8);
+  radix_hist_kernel<KeyT><<<hist_blocks, kSortThreads, 0, s>>>(k0, count, n_fixed, passes, shift0, hist);
+  radix_offsets_kernel<<<passes, kRadix, 0, s>>>(hist, offsets);
+  for (int p = 0; p < passes; p++) {
+    PassArgs<KeyT> a;
+    bool odd = p & 1;
+    a.keys_in = odd ? k1 : k0;
+    a.vals_in = odd ? v1 : v0;
+    a.keys_out = odd ? k0 : k1;
+    a.vals_out = odd ? v0 : v1;
+    a.count = count;
+    a.n_fixed = n_fixed;
+    a.shift = shift0 + p * kRadixBits;
+    a.offsets = offsets + p * kRadix;
+    a.lookback = lookback + (size_t)p * chunks * kRadix;
+    a.chunk_counter = chunk_counters + p;
+    onesweep_kernel<KeyT><<<chunks, kSortThreads, 0, s>>>(a);
+  }
+  return passes & 1;
+}
+
+// ------------------------------------------------------------------ scan of tiles_touched in depth order
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t *order, const uint32_t *touched,
+                                                                   uint32_t n, uint32_t *block_sums) {
+  __shared__ uint32_t s[kScanThreads / 32];
+  uint32_t base = blockIdx.x * kScanChunk, acc = 0;
+  for (int i = 0; i < kScanItems; i++) {
+    uint32_t r = base + i * kScanThreads + threadIdx.x;
+    if (r < n) acc += touched[order[r]];
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v = threadIdx.x < kScanThreads / 32 ? s[threadIdx.x] : 0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = v;
+  }
+}
+
+// single block: exclusive scan of the block sums (uint64 to detect overflow)
+__global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t *block_sums, int nb, uint32_t *counters,
+                                                        uint64_t cap) {
+  __shared__ unsigned long long s[1024];
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    int i = base + threadIdx.x;
+    unsigned long long v = i < nb ? block_sums[i] : 0;
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {
+      unsigned long long u = threadIdx.x >= d ? s[threadIdx.x - d] : 0;
+      __syncthreads();
+      s[threadIdx.x] += u;
+      __syncthreads();
+    }
+    if (i < nb) block_sums[i] = (uint32_t)(carry + s[threadIdx.x] - v);
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += s[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    counters[C_NPAIRS] = carry > 0xffffffffull ? 0xffffffffu : (uint32_t)carry;
+    counters[C_OVERFLOW] = carry > cap ? 1u : 0u;
+    counters[C_NSORT] = carry > cap ? 0u : (uint32_t)carry;  // pairs the sort may touch
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t *order, const uint32_t *touched,
+                                                                 uint32_t n, const uint32_t *block_sums,
+                                                                 uint32_t *offsets) {
+  __shared__ uint32_t s[kScanThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  uint32_t base = blockIdx.x * kScanChunk + t * kScanItems;
+  uint32_t v[kScanItems], acc = 0;
+  for (int i = 0; i < kScanItems; i++) {
+    uint32_t r = base + i;
+    v[i] = r < n ? touched[order[r]] : 0;
+    acc += v[i];
+  }
+  uint32_t inc = acc;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t x = lane < kScanThreads / 32 ? s[lane] : 0, y = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t u = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += u;
+    }
+    if (lane < kScanThreads / 32) s[lane] = y - x;
+  }
+  __syncthreads();
+  uint32_t run = block_sums[blockIdx.x] + s[w] + inc - acc;
+  for (int i = 0; i < kScanItems; i++) {
+    uint32_t r = base + i;
+    if (r < n) offsets[r] = run;
+    run += v[i];
+  }
+}
+
+// ------------------------------------------------------------------ duplicate
+__global__ void duplicate_kernel(const uint32_t *order, const uint32_t *touched, const int4 *bbox,
+                                 const uint32_t *offsets, uint32_t n, uint32_t cap, int tiles_x,
+                                 uint32_t *pair_tiles, uint32_t *pair_ids) {
+  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  uint32_t id = order[r];
+  uint32_t cnt = touched[id];
+  if (cnt == 0) return;
+  uint32_t off = offsets[r];
+  if ((uint64_t)off + cnt > cap) return;
+  int4 b = bbox[id];
+  int tx0 = b.x / kTile, tx1 = (b.y - 1) / kTile, ty0 = b.z / kTile, ty1 = (b.w - 1) / kTile;
+  for (int ty = ty0; ty <= ty1; ty++)
+    for (int tx = tx0; tx <= tx1; tx++) {
+      pair_tiles[off] = (uint32_t)(ty * tiles_x + tx);
+      pair_ids[off] = id;
+      off++;
+    }
+}
+
+__global__ void ranges_kernel(const uint32_t *pair_tiles, const uint32_t *counters, uint32_t cap, uint2 *ranges) {
+  uint32_t P = counters[C_NSORT];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+    uint32_t t = pair_tiles[i];
+    if (i == 0 || pair_tiles[i - 1] != t) ranges[t].x = i;
+    if (i + 1 == P || pair_tiles[i + 1] != t) ranges[t].y = i + 1;
+  }
+  (void)cap;
+}
+
+// ------------------------------------------------------------------ orchestration
+struct Scratch {
+  uint64_t *dkeys_alt;
+  uint32_t *dvals_alt;
+  uint32_t *ptiles_alt;
+  uint32_t *pids_alt;
+  uint32_t *hist;       // [16][256]
+  uint32_t *offsets;    // [16][256]
+  uint32_t *lookback;   // depth passes then pair passes
+  uint32_t *block_sums;
+  size_t lookback_words;
+};
+
+size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, Scratch *sc, char *base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return base ? base + o : nullptr; };
+  const size_t dchunks = (size_t)((n + kSortChunk - 1) / kSortChunk);
+  const size_t pchunks = (size_t)((cap + kSortChunk - 1) / kSortChunk);
+  const size_t lb_words = (8 * dchunks + pair_passes * pchunks) * kRadix;
+  char *p0 = take(sizeof(uint64_t) * n);
+  char *p1 = take(sizeof(uint32_t) * n);
+  char *p2 = take(sizeof(uint32_t) * cap);
+  char *p3 = take(sizeof(uint32_t) * cap);
+  char *p4 = take(sizeof(uint32_t) * 16 * kRadix);
+  char *p5 = take(sizeof(uint32_t) * 16 * kRadix);
+  char *p6 = take(sizeof(uint32_t) * lb_words);
+  char *p7 = take(sizeof(uint32_t) * ((n + kScanChunk - 1) / kScanChunk + 1));
+  if (sc) {
+    sc->dkeys_alt = (uint64_t *)p0; sc->dvals_alt = (uint32_t *)p1;
+    sc->ptiles_alt = (uint32_t *)p2; sc->pids_alt = (uint32_t *)p3;
+    sc->hist = (uint32_t *)p4; sc->offsets = (uint32_t *)p5; sc->lookback = (uint32_t *)p6;
+    sc->block_sums = (uint32_t *)p7; sc->lookback_words = lb_words;
+  }
+  return off;
+}
+
+int pair_sort_passes(int tiles) {
+  int bits = 0;
+  while ((1 << bits) < tiles) bits++;
+  return bits == 0 ? 1 : (bits + kRadixBits - 1) / kRadixBits;
+}
+
+int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params &p,
+                   const cs_layout &L, char *ws, int64_t cap, cudaStream_t s) {
+  (void)cam; (void)set;
+  const uint32_t n = (uint32_t)p.n;
+  const int tiles = L.tiles_x * L.tiles_y;
+  const int pp = pair_sort_passes(tiles);
+  Scratch sc;
+  scratch_bytes(p.n, cap, pp, &sc, ws + L.scratch);
+  uint32_t *counters = reinterpret_cast<uint32_t *>(ws + L.counters);
+  uint64_t *dkeys = reinterpret_cast<uint64_t *>(ws + L.depth_keys);
+  uint32_t *order = reinterpret_cast<uint32_t *>(ws + L.order);
+  uint32_t *touched = reinterpret_cast<uint32_t *>(ws + L.tiles_touched);
+  uint32_t *offs = reinterpret_cast<uint32_t *>(ws + L.pair_offsets);
+  uint32_t *ptiles = reinterpret_cast<uint32_t *>(ws + L.pair_tiles);
+  uint32_t *pids = reinterpret_cast<uint32_t *>(ws + L.pair_ids);
+  uint2 *ranges = reinterpret_cast<uint2 *>(ws + L.tile_ranges);
+
+  cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 16 * kRadix, s);
+  cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * sc.lookback_words, s);
+  cudaMemsetAsync(ranges, 0, sizeof(uint2) * tiles, s);
+  if (n > 0) {
+    // depth order: 8 passes (even) -> result back in (dkeys, order)
+    radix_sort<uint64_t>(dkeys, order, sc.dkeys_alt, sc.dvals_alt, nullptr, n, n, 8, 0, sc.hist,
+                         sc.offsets, sc.lookback, counters + C_CHUNK0, s);
+    const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
+    scan_reduce_kernel<<<nb, kScanThreads, 0, s>>>(order, touched, n, sc.block_sums);
+    scan_top_kernel<<<1, 1024, 0, s>>>(sc.block_sums, nb, counters, (uint64_t)cap);
+    scan_down_kernel<<<nb, kScanThreads, 0, s>>>(order, touched, n, sc.block_sums, offs);
+    // pairs land in the buffer that makes the sorted result end in (ptiles, pids)
+    uint32_t *dt = (pp & 1) ? sc.ptiles_alt : ptiles;
+    uint32_t *di = (pp & 1) ? sc.pids_alt : pids;
+    duplicate_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, touched, reinterpret_cast<const int4 *>(ws + L.bbox),
+                                                    offs, n, (uint32_t)cap, L.tiles_x, dt, di);
+    if (cap > 0) {
+      uint32_t *ka = (pp & 1) ? sc.ptiles_alt : ptiles, *va = (pp & 1) ? sc.pids_alt : pids;
+      uint32_t *kb = (pp & 1) ? ptiles : sc.ptiles_alt, *vb = (pp & 1) ? pids : sc.pids_alt;
+      radix_sort<uint32_t>(ka, va, kb, vb, counters + C_NSORT, 0, (uint32_t)cap, pp, 0, sc.hist + 8 * kRadix,
+                           sc.offsets + 8 * kRadix, sc.lookback + 8 * ((n + kSortChunk - 1) / kSortChunk) * kRadix,
+                           counters + C_CHUNK0 + 8, s);
+      ranges_kernel<<<148 * 4, 256, 0, s>>>(ptiles, counters, (uint32_t)cap, ranges);
+    }
+  }
+  return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+}
+
+}  // namespace cs

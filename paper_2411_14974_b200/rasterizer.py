@@ -1,0 +1,404 @@
+"""Host side of the sm_100a rasterizer: workspace management, the autograd
+Function and the reference-compatible entry points.
+
+Layering (north_star): Python API with the reference names
+(rasterize.render / render_reference / prepare_view / bin_tiles,
+backward.backward) -> torch.autograd.Function -> ctypes ->
+libconvexsplat_sm100.so (extern "C", include/convexsplat_b200.h) -> kernels.
+There is no CPU path: every call goes through the CUDA library and raises if
+it is unavailable.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .model import (EXACT_SETTINGS, SH_COEFFS, Camera, GradientBuffer, RenderOutput,
+                    RenderSettings, ScalingMode)
+from .scene_tensors import SceneTensors, as_scene_tensors
+
+_COUNTERS = 16
+
+
+def _device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.CsError("the convex-splatting renderer needs a CUDA device (no CPU fallback)")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise _lib.CsError(f"the renderer runs on CUDA devices only, got {device}")
+    return torch.device("cuda", device.index if device.index is not None else torch.cuda.current_device())
+
+
+def camera_struct(cam: Camera) -> _lib.CsCamera:
+    c = _lib.CsCamera()
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.R[:] = [float(v) for v in np.asarray(cam.R, dtype=np.float64).reshape(9)]
+    c.t[:] = [float(v) for v in np.asarray(cam.t, dtype=np.float64).reshape(3)]
+    c.z_near = float(cam.z_near)
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.ortho = int(bool(cam.ortho))
+    return c
+
+
+def settings_struct(settings: RenderSettings, mode: ScalingMode, background) -> _lib.CsSettings:
+    s = _lib.CsSettings()
+    s.cutoff = float(settings.contribution_cutoff)
+    s.floor = float(settings.transmittance_floor)
+    s.background[:] = [float(v) for v in np.asarray(background, dtype=np.float64).reshape(3)]
+    s.tile = int(settings.tile_size)
+    s.sh_degree = int(settings.sh_degree)
+    s.scaling_mode = ScalingMode(mode).code
+    return s
+
+
+def params_struct(st: SceneTensors) -> _lib.CsParams:
+    for name in ("points", "raw_delta", "raw_sigma", "raw_opacity", "raw_mask", "sh"):
+        t = getattr(st, name)
+        if t.dtype != torch.float32 or not t.is_contiguous() or t.device.type != "cuda":
+            raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    p = _lib.CsParams()
+    p.n, p.k = st.n, st.k
+    p.points, p.raw_delta, p.raw_sigma = st.points.data_ptr(), st.raw_delta.data_ptr(), st.raw_sigma.data_ptr()
+    p.raw_opacity, p.raw_mask, p.sh = st.raw_opacity.data_ptr(), st.raw_mask.data_ptr(), st.sh.data_ptr()
+    return p
+
+
+class Workspace:
+    """Caller-owned device workspace of one frame (the C ABI never allocates)."""
+
+    def __init__(self, device=None):
+        self.device = _device(device)
+        self.buffer: Optional[torch.Tensor] = None
+        self.layout: Optional[_lib.CsLayout] = None
+        self.capacity = 0
+
+    def plan(self, cam_c, set_c, n: int, k: int, capacity: int) -> _lib.CsLayout:
+        L = _lib.CsLayout()
+        _lib.check(_lib.load().cs_workspace_layout(ctypes.byref(cam_c), ctypes.byref(set_c), n, k, capacity,
+                                                   ctypes.byref(L)), "cs_workspace_layout")
+        return L
+
+    def ensure(self, cam_c, set_c, n: int, k: int, capacity: int) -> _lib.CsLayout:
+        L = self.plan(cam_c, set_c, n, k, capacity)
+        if self.buffer is None or self.buffer.numel() < L.total_bytes:
+            self.buffer = torch.empty(int(L.total_bytes * 1.05) + 256, dtype=torch.uint8, device=self.device)
+        self.layout, self.capacity = L, capacity
+        return L
+
+    @property
+    def ptr(self) -> int:
+        return self.buffer.data_ptr()
+
+    @property
+    def nbytes(self) -> int:
+        return self.buffer.numel()
+
+    def region(self, name: str, dtype: torch.dtype, count: int) -> torch.Tensor:
+        off = getattr(self.layout, name)
+        nbytes = count * torch.empty((), dtype=dtype).element_size()
+        return self.buffer[off:off + nbytes].view(dtype)
+
+    def counters(self) -> torch.Tensor:
+        return self.region("counters", torch.int32, _COUNTERS)
+
+
+@dataclass
+class Frame:
+    """Result of one forward render (device tensors) + what the backward needs."""
+
+    image: torch.Tensor
+    final_T: torch.Tensor
+    count: torch.Tensor
+    weight_sum: torch.Tensor
+    depth: torch.Tensor
+    visible: torch.Tensor
+    workspace: Workspace
+    scene: SceneTensors
+    cam_c: _lib.CsCamera
+    set_c: _lib.CsSettings
+    params_c: _lib.CsParams
+    capacity: int
+    n_visible: int = -1
+    n_pairs: int = -1
+    extras: dict = field(default_factory=dict)
+
+
+class Rasterizer:
+    """Stateless apart from a pair-capacity hint; each forward gets its own
+    workspace unless one is passed (the benchmark reuses one)."""
+
+    def __init__(self, device=None, growth: float = 1.25):
+        self.device = _device(device)
+        self.growth = growth
+        self._cap_hint = {}
+        _lib.load()
+
+    def _initial_capacity(self, st: SceneTensors, cam: Camera) -> int:
+        key = (st.n, cam.width, cam.height)
+        if key in self._cap_hint:
+            return self._cap_hint[key]
+        tiles = math.ceil(cam.width / 16) * math.ceil(cam.height / 16)
+        return int(min(max(8 * st.n, 4096), max(st.n * tiles, 4096), (1 << 30) - 1))
+
+    def forward(self, scene, cam: Camera, mode=ScalingMode.DEPTH, settings: RenderSettings = RenderSettings(),
+                workspace: Optional[Workspace] = None, capacity: Optional[int] = None, check: bool = True,
+                outputs: Optional[dict] = None) -> Frame:
+        st = as_scene_tensors(scene, self.device)
+        cam_c = camera_struct(cam)
+        set_c = settings_struct(settings, mode, st.background)
+        params_c = params_struct(st)
+        ws = workspace if workspace is not None else Workspace(self.device)
+        cap = capacity if capacity is not None else max(ws.capacity, self._initial_capacity(st, cam))
+        H, W, n = cam.height, cam.width, st.n
+        if outputs is None:
+            dev = self.device
+            outputs = dict(image=torch.empty((H, W, 3), device=dev), final_T=torch.empty((H, W), device=dev),
+                           count=torch.empty((H, W), dtype=torch.int32, device=dev),
+                           weight_sum=torch.empty((H, W), device=dev), depth=torch.empty((H, W), device=dev),
+                           visible=torch.empty((max(n, 1),), dtype=torch.uint8, device=dev))
+        frame_c = _lib.CsFrame(outputs["image"].data_ptr(), outputs["final_T"].data_ptr(),
+                               outputs["count"].data_ptr(), outputs["weight_sum"].data_ptr(),
+                               outputs["depth"].data_ptr(), outputs["visible"].data_ptr())
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        while True:
+            ws.ensure(cam_c, set_c, n, st.k, cap)
+            _lib.check(_lib.load().cs_forward(ctypes.byref(cam_c), ctypes.byref(set_c), ctypes.byref(params_c),
+                                              ws.ptr, ws.nbytes, cap, ctypes.byref(frame_c), stream), "cs_forward")
+            fr = Frame(outputs["image"], outputs["final_T"], outputs["count"], outputs["weight_sum"],
+                       outputs["depth"], outputs["visible"][:n], ws, st, cam_c, set_c, params_c, cap)
+            if not check:
+                return fr
+            counts = (ctypes.c_uint32 * 4)()
+            _lib.check(_lib.load().cs_read_counters(ctypes.c_void_p(ws.ptr), counts, stream), "cs_read_counters")
+            fr.n_visible, fr.n_pairs = int(counts[0]), int(counts[1])
+            if counts[2] == 0:
+                self._cap_hint[(n, W, H)] = max(cap, int(fr.n_pairs * self.growth) + 1024)
+                return fr
+            cap = int(fr.n_pairs * self.growth) + 1024   # overflow: grow and re-render
+            if cap >= (1 << 30):
+                raise _lib.CsError(f"{fr.n_pairs} tile pairs exceed the supported 2^30")
+
+    def backward(self, frame: Frame, d_image: torch.Tensor, grads: dict) -> dict:
+        """Accumulate (+=) gradients of sum(d_image * image) into ``grads``."""
+        d_image = d_image.to(device=self.device, dtype=torch.float32).contiguous()
+        H, W = frame.cam_c.height, frame.cam_c.width
+        if tuple(d_image.shape) != (H, W, 3):
+            raise ValueError(f"d_image must be ({H}, {W}, 3), got {tuple(d_image.shape)}")
+        g = _lib.CsGrads(grads["points"].data_ptr(), grads["raw_delta"].data_ptr(), grads["raw_sigma"].data_ptr(),
+                         grads["raw_opacity"].data_ptr(), grads["raw_mask"].data_ptr(), grads["sh"].data_ptr())
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ws = frame.workspace
+        _lib.check(_lib.load().cs_backward(ctypes.byref(frame.cam_c), ctypes.byref(frame.set_c),
+                                           ctypes.byref(frame.params_c), ws.ptr, ws.nbytes, frame.capacity,
+                                           d_image.data_ptr(), ctypes.byref(g), stream), "cs_backward")
+        return grads
+
+
+def zero_grads(st: SceneTensors) -> dict:
+    return {name: torch.zeros_like(getattr(st, name)) for name in
+            ("points", "raw_delta", "raw_sigma", "raw_opacity", "raw_mask", "sh")}
+
+
+_default: dict = {}
+
+
+def default_rasterizer(device=None) -> Rasterizer:
+    dev = _device(device)
+    if dev not in _default:
+        _default[dev] = Rasterizer(dev)
+    return _default[dev]
+
+
+# ---------------------------------------------------------------------------
+# autograd
+
+
+class _RasterizeFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, rasterizer, cam, mode, settings, background, points, raw_delta, raw_sigma, raw_opacity,
+                raw_mask, sh):
+        st = SceneTensors(points.detach().contiguous(), raw_delta.detach().contiguous(),
+                          raw_sigma.detach().contiguous(), raw_opacity.detach().contiguous(),
+                          raw_mask.detach().contiguous(), sh.detach().contiguous(), background)
+        fr = rasterizer.forward(st, cam, mode, settings)
+        ctx.frame, ctx.rasterizer = fr, rasterizer
+        ctx.mark_non_differentiable(fr.final_T, fr.count, fr.weight_sum, fr.depth, fr.visible)
+        return fr.image, fr.final_T, fr.count, fr.weight_sum, fr.depth, fr.visible
+
+    @staticmethod
+    def backward(ctx, d_image, *_unused):
+        fr = ctx.frame
+        grads = zero_grads(fr.scene)
+        if d_image is not None:
+            ctx.rasterizer.backward(fr, d_image, grads)
+        ctx.frame = None
+        return (None, None, None, None, None, grads["points"], grads["raw_delta"], grads["raw_sigma"],
+                grads["raw_opacity"], grads["raw_mask"], grads["sh"])
+
+
+def rasterize(scene: SceneTensors, cam: Camera, mode=ScalingMode.DEPTH, settings: RenderSettings = RenderSettings(),
+              rasterizer: Optional[Rasterizer] = None):
+    """Differentiable render of SoA tensors.  Returns (image, final_T, count,
+    weight_sum, depth, visible); gradients flow from ``image`` to the six
+    parameter tensors (backward.py:76-282 semantics)."""
+    r = rasterizer or default_rasterizer(scene.device)
+    return _RasterizeFunction.apply(r, cam, mode, settings, scene.background, scene.points, scene.raw_delta,
+                                    scene.raw_sigma, scene.raw_opacity, scene.raw_mask, scene.sh)
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible entry points (numpy in/out, float64 like the reference)
+
+
+def _np(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+def render(scene, cam: Camera, mode: ScalingMode = ScalingMode.DEPTH,
+           settings: RenderSettings = RenderSettings()) -> RenderOutput:
+    """rasterize.render (rasterize.py:156-209) on the GPU."""
+    fr = default_rasterizer().forward(scene, cam, mode, settings)
+    return RenderOutput(image=_np(fr.image).astype(np.float64),
+                        final_transmittance=_np(fr.final_T).astype(np.float64),
+                        per_pixel_count=_np(fr.count), blend_weight_sum=_np(fr.weight_sum).astype(np.float64),
+                        visible=_np(fr.visible).astype(bool), depth=_np(fr.depth).astype(np.float64))
+
+
+def render_reference(scene, cam: Camera, mode: ScalingMode = ScalingMode.DEPTH) -> RenderOutput:
+    """rasterize.render_reference (rasterize.py:212-245): every primitive at
+    every pixel with no bbox, cutoff or termination -- identical semantics to
+    render(EXACT_SETTINGS) (test_rasterize.py:118-128), so it runs the same
+    kernels with full-frame bboxes."""
+    return render(scene, cam, mode, EXACT_SETTINGS)
+
+
+def backward(scene, cam: Camera, d_image, mode: ScalingMode = ScalingMode.DEPTH,
+             settings: RenderSettings = RenderSettings()) -> GradientBuffer:
+    """backward.backward (backward.py:76-212): gradient of sum(d_image*image)."""
+    r = default_rasterizer()
+    st = as_scene_tensors(scene, r.device)
+    fr = r.forward(st, cam, mode, settings)
+    grads = r.backward(fr, torch.as_tensor(np.asarray(d_image), dtype=torch.float32), zero_grads(st))
+    f64 = {k: _np(v).astype(np.float64) for k, v in grads.items()}
+    return GradientBuffer(d_points=f64["points"], d_raw_delta=f64["raw_delta"], d_raw_sigma=f64["raw_sigma"],
+                          d_raw_opacity=f64["raw_opacity"], d_sh=f64["sh"], d_raw_mask=f64["raw_mask"],
+                          visible=_np(fr.visible).astype(bool))
+
+
+# ---------------------------------------------------------------------------
+# discrete state of a frame (prepare_view / bin_tiles equivalents)
+
+
+def _decode_depth(keys: np.ndarray) -> np.ndarray:
+    """Inverse of the order-preserving f64 -> u64 map of csrc/common.cuh."""
+    keys = keys.astype(np.uint64)
+    sign = (keys & np.uint64(1 << 63)) != 0
+    bits = np.where(sign, keys & ~np.uint64(1 << 63), ~keys)
+    return bits.view(np.float64)
+
+
+def inspect_frame(fr: Frame) -> dict:
+    """Copy the frame's discrete state to host: depth order, hull cycles,
+    bboxes and the per-tile candidate lists (CSR over row-major tiles)."""
+    ws, L = fr.workspace, fr.workspace.layout
+    n, V, P = fr.scene.n, fr.n_visible, fr.n_pairs
+    tiles = L.tiles_x * L.tiles_y
+    order = _np(ws.region("order", torch.int32, n))[:V].astype(np.int64)
+    hull = _np(ws.region("hull", torch.uint8, n * L.max_k)).reshape(n, L.max_k).astype(np.int64)
+    hull[hull == 255] = -1
+    bbox = _np(ws.region("bbox", torch.int32, 4 * n)).reshape(n, 4).astype(np.int64)
+    keys = _np(ws.region("depth_keys", torch.int64, n)).view(np.uint64)[:V]
+    ranges = _np(ws.region("tile_ranges", torch.int32, 2 * tiles)).reshape(tiles, 2).astype(np.int64)
+    pair_ids = _np(ws.region("pair_ids", torch.int32, P)).astype(np.int64)
+    pair_tiles = _np(ws.region("pair_tiles", torch.int32, P)).astype(np.int64)
+    recs = _np(ws.region("records", torch.float32, n * L.rec_floats)).reshape(n, L.rec_floats)
+    off = np.zeros(tiles + 1, np.int64)
+    counts = np.zeros(tiles, np.int64)
+    nz = ranges[:, 1] > ranges[:, 0]
+    counts[nz] = ranges[nz, 1] - ranges[nz, 0]
+    off[1:] = np.cumsum(counts)
+    return dict(order=order, hull=hull, bbox=bbox, depth=_decode_depth(keys), tile_ranges=ranges,
+                pair_ids=pair_ids, pair_tiles=pair_tiles, tile_offsets=off, records=recs,
+                tiles_x=L.tiles_x, tiles_y=L.tiles_y, n_visible=V, n_pairs=P)
+
+
+@dataclass
+class ProjectedConvex:
+    """GPU-prepared subset of projection.ProjectedConvex (projection.py:180-203)."""
+
+    index: int
+    depth: float
+    hull_indices: np.ndarray
+    delta_s: float
+    sigma_s: float
+    bbox: tuple
+
+
+@dataclass
+class ViewPrimitive:
+    """rasterize.ViewPrimitive (rasterize.py:56-65); fields from the GPU record."""
+
+    pc: ProjectedConvex
+    opacity: float
+    color: np.ndarray
+    scale: float
+
+
+class PreparedView(list):
+    """prepare_view() result: ViewPrimitives in blend order + the GPU tile lists."""
+
+    bins: list = None
+    tiles_x: int = 0
+    tiles_y: int = 0
+
+
+def prepare_view(scene, cam: Camera, mode: ScalingMode = ScalingMode.DEPTH,
+                 settings: RenderSettings = RenderSettings()) -> PreparedView:
+    """rasterize.prepare_view (rasterize.py:77-122) from the GPU preprocess."""
+    fr = default_rasterizer().forward(scene, cam, mode, settings)
+    info = inspect_frame(fr)
+    out = PreparedView()
+    dls_to_delta = math.log(2.0)
+    for rank, i in enumerate(info["order"]):
+        rec = info["records"][i]
+        h = info["hull"][i]
+        depth = float(info["depth"][rank])
+        d = 1.0 if cam.ortho else depth
+        scale = {ScalingMode.NONE: 1.0, ScalingMode.SQRT_DEPTH: math.sqrt(d), ScalingMode.DEPTH: d,
+                 ScalingMode.DEPTH_SQUARED: d * d}[ScalingMode(mode)]
+        pc = ProjectedConvex(int(i), depth, h[h >= 0].copy(), float(rec[9]) * dls_to_delta, float(rec[2]),
+                             tuple(int(v) for v in info["bbox"][i]))
+        out.append(ViewPrimitive(pc, float(rec[3]), rec[4:7].astype(np.float64), scale))
+    rank_of = {int(i): r for r, i in enumerate(info["order"])}
+    bins = []
+    for t in range(info["tiles_x"] * info["tiles_y"]):
+        s, e = info["tile_ranges"][t]
+        bins.append([rank_of[int(i)] for i in info["pair_ids"][s:e]] if e > s else [])
+    out.bins, out.tiles_x, out.tiles_y = bins, info["tiles_x"], info["tiles_y"]
+    return out
+
+
+def bin_tiles(prepared: PreparedView, width: int, height: int, tile_size: int = 16):
+    """rasterize.bin_tiles (rasterize.py:134-144): per-tile candidate lists of
+    positions in the prepared order, as produced by the GPU binning."""
+    if not isinstance(prepared, PreparedView) or prepared.bins is None:
+        raise TypeError("bin_tiles expects the result of this package's prepare_view()")
+    if tile_size != 16:
+        raise ValueError("the sm_100a binning supports tile_size=16")
+    tx, ty = (width + 15) // 16, (height + 15) // 16
+    if (tx, ty) != (prepared.tiles_x, prepared.tiles_y):
+        raise ValueError("width/height differ from the prepared camera")
+    return prepared.bins, tx, ty
+
+
+__all__ = ["Rasterizer", "Workspace", "Frame", "rasterize", "render", "render_reference", "backward",
+           "prepare_view", "bin_tiles", "inspect_frame", "zero_grads", "default_rasterizer",
+           "camera_struct", "settings_struct", "params_struct", "SH_COEFFS"]

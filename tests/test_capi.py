@@ -1,0 +1,96 @@
+"""CPU-side checks of the C ABI: the library loads, exports every entry point
+declared in include/convexsplat_b200.h, and its host-only functions
+(layout, argument validation, error strings) behave.  No kernel runs here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2411_14974_b200 import _lib, build
+from paper_2411_14974_b200.model import Camera, RenderSettings, ScalingMode
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "convexsplat_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _lib.load()
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"CS_API\s+[\w\s\*]*?\b(cs_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_bound_entry_points():
+    assert declared_functions() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert lib.cs_abi_version() == _lib.ABI_VERSION
+
+
+def test_struct_sizes_match_the_header(lib):
+    # the C structs are plain doubles / int32 / pointers with natural alignment
+    assert ctypes.sizeof(_lib.CsCamera) == 8 * (4 + 9 + 3 + 1) + 4 * 4
+    assert ctypes.sizeof(_lib.CsSettings) == 8 * 5 + 4 * 4
+    assert ctypes.sizeof(_lib.CsParams) == 8 + 4 + 4 + 6 * 8
+    assert ctypes.sizeof(_lib.CsFrame) == 6 * 8
+    assert ctypes.sizeof(_lib.CsGrads) == 6 * 8
+
+
+def _structs(width=1920, height=1080, settings=RenderSettings()):
+    from paper_2411_14974_b200.rasterizer import camera_struct, settings_struct
+    cam = Camera(fx=1000.0, fy=1000.0, cx=width / 2, cy=height / 2, width=width, height=height,
+                 R=np.eye(3), t=np.array([0.0, 0.0, 4.0]))
+    return camera_struct(cam), settings_struct(settings, ScalingMode.DEPTH, np.zeros(3))
+
+
+def test_workspace_layout_regions_are_disjoint_and_aligned(lib):
+    cam, st = _structs()
+    L = _lib.CsLayout()
+    assert lib.cs_workspace_layout(ctypes.byref(cam), ctypes.byref(st), 1_000_000, 6, 8_000_000,
+                                   ctypes.byref(L)) == 0
+    assert (L.tiles_x, L.tiles_y) == (120, 68)
+    assert L.max_k == 8 and L.rec_floats == 40 and L.acc_floats == 32
+    names = ["counters", "records", "hull", "bbox", "depth_keys", "order", "tiles_touched", "pair_offsets",
+             "pair_tiles", "pair_ids", "tile_ranges", "pixel_last", "pixel_clamp", "grad_accum", "scratch"]
+    offs = [getattr(L, n) for n in names]
+    assert offs == sorted(offs)
+    assert all(o % 256 == 0 for o in offs)
+    assert L.total_bytes >= L.scratch + L.scratch_bytes
+    assert L.pair_ids - L.pair_tiles >= 4 * 8_000_000
+
+
+def test_layout_rejects_bad_arguments(lib):
+    cam, st = _structs()
+    L = _lib.CsLayout()
+    assert lib.cs_workspace_layout(ctypes.byref(cam), ctypes.byref(st), 10, 2, 100, ctypes.byref(L)) == 1  # K < 3
+    assert lib.cs_workspace_layout(ctypes.byref(cam), ctypes.byref(st), 10, 17, 100, ctypes.byref(L)) == 1
+    assert lib.cs_workspace_layout(ctypes.byref(cam), ctypes.byref(st), -1, 6, 100, ctypes.byref(L)) == 1
+    cam8, st8 = _structs(settings=RenderSettings(tile_size=8))
+    assert lib.cs_workspace_layout(ctypes.byref(cam8), ctypes.byref(st8), 10, 6, 100, ctypes.byref(L)) == 4
+    camd, std = _structs(settings=RenderSettings(sh_degree=4))
+    assert lib.cs_workspace_layout(ctypes.byref(camd), ctypes.byref(std), 10, 6, 100, ctypes.byref(L)) == 4
+
+
+def test_forward_rejects_small_workspace_without_touching_the_gpu(lib):
+    cam, st = _structs(64, 64)
+    p = _lib.CsParams()
+    p.n, p.k = 0, 6
+    f = _lib.CsFrame(1, 1, 1, 1, 0, 0)   # non-null dummies: validation happens before any launch
+    rc = lib.cs_forward(ctypes.byref(cam), ctypes.byref(st), ctypes.byref(p), ctypes.c_void_p(1), 16, 0,
+                        ctypes.byref(f), None)
+    assert rc == 3
+
+
+def test_error_strings(lib):
+    for code in range(5):
+        assert lib.cs_error_string(code)
+    assert b"unknown" in lib.cs_error_string(99)
