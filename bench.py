@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark of the sm_100a convex-splatting hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3]): G(1M, seed 0) six-point
+convexes, camera C(1920, 1080), DEPTH scaling, RenderSettings() defaults,
+synthetic float32 scene (no dataset), d_image ~ N(0, 1e-3) for the backward.
+
+* ``value``: forward frames/s over all ranks (each rank renders a replica of
+  the single view: one view is not partitioned), scene resident
+  in HBM, L2 flushed before every timed frame (a 512 MB write, untimed).
+* ``fwd_bwd_iters_per_s``: forward + gradient zeroing + backward.
+* ``e2e``: same metric through the C-ABI call with HOST buffers: pinned
+  host->device copy of the six parameter arrays, cs_forward, device->host
+  copy of the image, all inside the timed region.
+* ``roofline``: the dominant kernel of the frame, from live CUDA-event stage
+  timings and the kernels' own work counters.
+* ``cpu_baseline``: the float64 C oracle (port of the reference, oracle/)
+  on this box's host cores over a bounded sample of tiles.
+
+``--impl reference`` times only the CPU reference path (the oracle port) on
+the host cores and prints the same JSON line with ``"impl": "reference"``.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd FPS & fwd+bwd iters/s, 1M 6-pt convexes @1080p; % of roofline"
+UNIT = "frames/s"
+MUFU_PER_CLK_PER_SM = 16     # CUDA arithmetic-throughput table, sm_100
+N_SMS = 148
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--n", type=int, default=1_000_000)
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--cpu-budget-s", type=float, default=15.0, help="CPU-baseline sample budget")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def workload(args):
+    from paper_2411_14974_b200 import synthetic
+    arrays = synthetic.quantize32(synthetic.generate_scene(args.n, args.seed))
+    cam = synthetic.bench_camera(args.width, args.height)
+    return arrays, cam
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for name, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+        except OSError:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline (oracle port)
+def cpu_sample(arrays, cam, budget_s: float, threads: int, with_backward: bool = True) -> dict:
+    """Time the float64 oracle (C port of the reference) on a bounded sample:
+    full prepare_view + bin_tiles, then a spread-out subset of tiles whose
+    size is chosen from a probe so the sample takes ~budget_s.  The frame
+    time is extrapolated linearly in the number of tiles."""
+    import numpy as np
+
+    import oracle
+    from paper_2411_14974_b200 import synthetic
+    cam_d = synthetic.camera_dict(cam)
+    o_set = dict(cutoff=2e-4, floor=1e-4, tile=16, sh_degree=3, mode="depth", background=np.zeros(3))
+    t0 = time.perf_counter()
+    view = oracle.prepare_view(arrays, cam_d, o_set, n_threads=threads)
+    t1 = time.perf_counter()
+    tiles = oracle.bin_tiles(view, cam.width, cam.height, 16)
+    t2 = time.perf_counter()
+    T = tiles[0].size - 1
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(T)
+    probe = perm[: max(T // 256, 8)]
+    tp = time.perf_counter()
+    oracle.render(arrays, cam_d, o_set, n_threads=threads, view=view, tiles=tiles, tile_list=probe)
+    per_tile = (time.perf_counter() - tp) / probe.size
+    count = int(min(T, max(probe.size, budget_s / max(per_tile, 1e-9) / (3.0 if with_backward else 1.0))))
+    sample = np.sort(perm[:count])
+    t3 = time.perf_counter()
+    oracle.render(arrays, cam_d, o_set, n_threads=threads, view=view, tiles=tiles, tile_list=sample)
+    t4 = time.perf_counter()
+    fwd_s = (t1 - t0) + (t2 - t1) + (t4 - t3) * T / count
+    out = dict(prepare_s=t1 - t0, bin_s=t2 - t1, tiles_sampled=count, tiles_total=T,
+               render_sample_s=t4 - t3, fwd_frame_s=fwd_s)
+    if with_backward:
+        d_img = np.random.default_rng(0).normal(0.0, 1e-3, size=(cam.height, cam.width, 3))
+        t5 = time.perf_counter()
+        oracle.backward(arrays, cam_d, o_set, d_img, n_threads=threads, view=view, tiles=tiles, tile_list=sample)
+        t6 = time.perf_counter()
+        # the chain over all visible convexes runs once regardless of the sample
+        out.update(backward_sample_s=t6 - t5, fwd_bwd_frame_s=fwd_s + (t6 - t5) * T / count)
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path (oracle port) on the host cores."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    arrays, cam = workload(args)
+    threads = host_cores()
+    times = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        budget = max(2.0, min(args.cpu_budget_s, 120.0 / max(args.warmup + args.steps, 1)))
+        info = cpu_sample(arrays, cam, budget, threads, with_backward=False)
+        if i >= args.warmup:
+            times.append(info["fwd_frame_s"])
+    frame_s = statistics.mean(times)
+    value = 1.0 / frame_s
+    sample = (f"G({args.n},{args.seed}) @{args.width}x{args.height}: full prepare_view+bin_tiles, "
+              f"{info['tiles_sampled']}/{info['tiles_total']} tiles rendered per step, frame time extrapolated")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config4: {args.n} 6-point convexes @ {args.width}x{args.height} forward",
+                       "impl_detail": "oracle/cs_oracle.c float64 C port of convexsplat 0.1.0 (reference is "
+                                      "pure NumPy; not compiled), OpenMP over tiles"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             "cpu": cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2411_14974_b200 import rasterizer as rz
+    from paper_2411_14974_b200.model import RenderSettings, ScalingMode
+    from paper_2411_14974_b200.scene_tensors import SceneTensors
+
+    arrays, cam = workload(args)
+    st = SceneTensors.from_arrays(arrays, dev)
+    r = rz.Rasterizer(dev)
+    ws = rz.Workspace(dev)
+    settings = RenderSettings()
+    fr = r.forward(st, cam, ScalingMode.DEPTH, settings, workspace=ws)      # sizes the pair capacity
+    gen = torch.Generator(device=dev).manual_seed(args.seed)
+    d_image = torch.randn((cam.height, cam.width, 3), generator=gen, device=dev) * 1e-3
+    grads = rz.zero_grads(st)
+    r.launch_backward(fr, d_image, grads)
+    stats = r.read_stats(fr)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)            # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def fwd_step(ev):
+        ev[0].record(stream)
+        r.launch_forward(fr, 0, 0)
+        ev[1].record(stream)
+        r.launch_forward(fr, 1, 1)
+        ev[2].record(stream)
+        r.launch_forward(fr, 2, 2)
+        ev[3].record(stream)
+
+    def fwdbwd_step(ev):
+        ev[0].record(stream)
+        for g in grads.values():
+            g.zero_()
+        r.launch_forward(fr, 0, 2)
+        ev[1].record(stream)
+        r.launch_backward(fr, d_image, grads, 0, 0)
+        ev[2].record(stream)
+        r.launch_backward(fr, d_image, grads, 1, 1)
+        ev[3].record(stream)
+
+    def timed(step_fn, k):
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
+        for i in range(k):
+            flush.zero_()                          # untimed L2 flush between frames
+            step_fn(evs[i])
+        torch.cuda.synchronize(dev)
+        stages = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(3)] for e in evs])
+        return stages                               # ms, [k, 3]
+
+    for _ in range(args.warmup):
+        fwd_step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+        fwdbwd_step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+    barrier()
+    with ClockSampler(local) as clocks:
+        barrier()
+        fwd = timed(fwd_step, args.steps)
+        barrier()
+        fb = timed(fwdbwd_step, args.steps)
+        barrier()
+    clock = clocks.summary()
+    fwd_ms_local = float(fwd.sum(axis=1).mean())
+    fb_ms_local = float(fb.sum(axis=1).mean())
+    t = torch.tensor([fwd_ms_local, fb_ms_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    fwd_ms, fb_ms = float(t[0]), float(t[1])
+
+    # ---- e2e: host buffers through the C-ABI call
+    e2e = None
+    if not args.no_e2e:
+        host = {k: getattr(st, k).detach().cpu().pin_memory() for k in
+                ("points", "raw_delta", "raw_sigma", "raw_opacity", "raw_mask", "sh")}
+        img_host = torch.empty(fr.image.shape, dtype=torch.float32).pin_memory()
+        h2d = sum(v.numel() * v.element_size() for v in host.values())
+        d2h = img_host.numel() * 4
+
+        def e2e_step(ev):
+            ev[0].record(stream)
+            for k2, v in host.items():
+                getattr(st, k2).copy_(v, non_blocking=True)
+            r.launch_forward(fr, 0, 2)
+            img_host.copy_(fr.image, non_blocking=True)
+            ev[3].record(stream)
+
+        for _ in range(args.warmup):
+            e2e_step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+        barrier()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        for i in range(args.steps):
+            e2e_step(evs[i])
+        torch.cuda.synchronize(dev)
+        e2e_local = statistics.mean(e[0].elapsed_time(e[3]) for e in evs)
+        te = torch.tensor([e2e_local], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * 1000.0 / float(te[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(te[0]),
+               "path": "pinned host params -> cs_forward (C ABI) -> pinned host image"}
+
+    # ---- roofline of the frame's kernels
+    L = ws.layout
+    n, V, P = st.n, stats["n_visible"], stats["n_pairs"]
+    pp = max(1, math.ceil(math.log2(max(L.tiles_x * L.tiles_y, 2)) / 8))
+    stage_ms = fwd.mean(axis=0)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    mufu_peak = N_SMS * MUFU_PER_CLK_PER_SM * sm_max * 1e6 / 1e9          # Gop/s
+    k = st.k
+    pre_bytes = n * (k * 12 + 4 * 4 + 48 * 4) + n * (8 + 4 + 4) + V * (L.rec_floats * 4 + L.max_k + 16)
+    bin_bytes = (n * 8 + 8 * n * 12 * 2            # depth sort: histogram + 8 passes of (key, id)
+                 + n * 4 * 2 + n * 4 * 2 + n * 4   # scan: gather touched via order (x2 passes), write offsets
+                 + V * (4 + 4 + 16 + 4) + P * 8    # duplicate
+                 + P * 4 + pp * P * 8 * 2          # pair sort: histogram + passes of (tile, id)
+                 + P * 4)                          # ranges
+    mufu_ops = stats["fwd_line_evals"] + 3 * stats["fwd_evals"]
+    stage_info = {
+        "preprocess": {"ms": float(stage_ms[0]), "bound": "hbm", "work": pre_bytes, "unit": "GB/s",
+                       "achieved": pre_bytes / (stage_ms[0] * 1e-3) / 1e9, "peak": hbm_peak},
+        "binning": {"ms": float(stage_ms[1]), "bound": "hbm", "work": bin_bytes, "unit": "GB/s",
+                    "achieved": bin_bytes / (stage_ms[1] * 1e-3) / 1e9, "peak": hbm_peak},
+        "blend": {"ms": float(stage_ms[2]), "bound": "sfu", "work": mufu_ops, "unit": "Gop/s",
+                  "achieved": mufu_ops / (stage_ms[2] * 1e-3) / 1e9, "peak": mufu_peak},
+    }
+    for s in stage_info.values():
+        s["frac"] = s["achieved"] / s["peak"]
+    bwd_ms = fb.mean(axis=0)
+    dominant = max(stage_info, key=lambda s: stage_info[s]["ms"])
+    dom = stage_info[dominant]
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(dominant)
+        except ValueError:
+            traffic = None
+    roofline = {"kernel": dominant, "bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
+                "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic,
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if dom["bound"] == "hbm" else
+                                f"derived: {N_SMS} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x {sm_max:.0f} MHz "
+                                "(sm_max_mhz of MEASURED_PEAKS.json)"),
+                "stages": stage_info}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = host_cores()
+        cs_ = cpu_sample(arrays, cam, args.cpu_budget_s, threads, with_backward=True)
+        cpu = {"value": 1.0 / cs_["fwd_frame_s"], "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": (f"float64 C oracle (oracle/cs_oracle.c), full prepare_view+bin_tiles of G({args.n}) "
+                          f"+ {cs_['tiles_sampled']}/{cs_['tiles_total']} random tiles, extrapolated"),
+               "fwd_bwd_iters_per_s": 1.0 / cs_["fwd_bwd_frame_s"], "cpu": cpu_model(), "detail": cs_}
+
+    launches_fwd = 19 + pp
+    line = {
+        "metric": METRIC, "value": world * 1000.0 / fwd_ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": fwd_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (f64 preprocess)", "data": "synthetic",
+        "config": {"workload": f"config4: G({args.n},{args.seed}) 6-point convexes @ {args.width}x{args.height}, "
+                               "DEPTH scaling, RenderSettings() defaults; each rank renders a replica view",
+                   "convexes": n, "width": args.width, "height": args.height, "visible": V, "pairs": P,
+                   "l2": "flushed before every timed step (512 MB write, untimed)",
+                   "parallelism": f"replicas x{world}"},
+        "fwd_bwd_iters_per_s": world * 1000.0 / fb_ms, "fwd_bwd_ms": fb_ms,
+        "stage_ms": {"preprocess": float(stage_ms[0]), "binning": float(stage_ms[1]), "blend": float(stage_ms[2]),
+                     "fwd_total": float(fwd.sum(axis=1).mean()), "zero+forward": float(bwd_ms[0]),
+                     "backward_blend": float(bwd_ms[1]), "chain": float(bwd_ms[2])},
+        "work": {k2: int(v) for k2, v in stats.items()},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clock,
+        "gpu_launches": args.steps * launches_fwd + args.steps * (launches_fwd + 2),
+        "gpu_launches_detail": f"{launches_fwd} per forward (1 preprocess, 10 depth sort, 3 scan, 1 duplicate, "
+                               f"{2 + pp} pair sort, 1 ranges, 1 blend), 2 per backward",
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -107,7 +107,9 @@ typedef struct cs_grads {
 /* Byte offsets of the named regions inside the caller's workspace. */
 typedef struct cs_layout {
     size_t total_bytes;
-    size_t counters;          /* uint32[16]: [0] n_visible [1] n_pairs [2] overflow */
+    size_t counters;          /* uint32[32]: [0] n_visible [1] n_pairs [2] overflow;
+                                 uint64[8] at word 16: work stats (forward evaluations,
+                                 line evaluations, blends; backward evaluations, lines) */
     size_t records;           /* float[n][rec_floats] per-convex blend records */
     size_t hull;              /* uint8[n][max_k]  hull cycle (indices into the K points) */
     size_t bbox;              /* int32[n][4]  x0,x1,y0,y1 half-open pixel rect */
@@ -119,6 +121,7 @@ typedef struct cs_layout {
     size_t pair_ids;          /* uint32[cap]  convex id of each pair (tile-major, depth order) */
     size_t tile_ranges;       /* uint32[tiles][2]  [start,end) into the pair arrays */
     size_t pixel_last;        /* int32[H*W]  pair index of the last blended candidate (-1 none) */
+    size_t pixel_T;           /* float[H*W]  final transmittance (kept for the backward) */
     size_t pixel_clamp;       /* uint8[H*W]  bit c set iff channel c of C+T*bg lies in [0,1] */
     size_t grad_accum;        /* float[n][acc_floats] screen-space gradient accumulators */
     size_t scratch;           /* private sort/scan scratch */

@@ -510,7 +510,7 @@ static void render_tile(const or_camera *cam, const or_settings *st, const or_vi
  * trans is initialised here.  tiles [t_begin, t_end) only (bounded CPU
  * samples); the background composite/clip runs over those tiles' pixels. */
 int or_render(const or_camera *cam, const or_settings *st, const or_view *V, const int64_t *tile_off,
-              const int32_t *items, int64_t t_begin, int64_t t_end, or_frame *F) {
+              const int32_t *items, int64_t t_begin, int64_t t_end, const int64_t *tile_list, or_frame *F) {
     const int W = cam->width, H = cam->height, ts = st->tile;
     const int tx_n = (W + ts - 1) / ts;
     for (size_t p = 0; p < (size_t)W * H; p++) F->trans[p] = 1.0;
@@ -519,11 +519,13 @@ int or_render(const or_camera *cam, const or_settings *st, const or_view *V, con
     int nt = st->n_threads > 0 ? st->n_threads : 1;
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : ne, nb) num_threads(nt)
 #endif
-    for (int64_t t = t_begin; t < t_end; t++) render_tile(cam, st, V, tile_off, items, t, F, &ne, &nb);
+    for (int64_t q = t_begin; q < t_end; q++)
+        render_tile(cam, st, V, tile_off, items, tile_list ? tile_list[q] : q, F, &ne, &nb);
     F->n_eval = ne;
     F->n_blend = nb;
     /* rasterize.py:206-209 */
-    for (int64_t t = t_begin; t < t_end; t++) {
+    for (int64_t q = t_begin; q < t_end; q++) {
+        int64_t t = tile_list ? tile_list[q] : q;
         int ty = (int)(t / tx_n), tx = (int)(t % tx_n);
         for (int y = ty * ts; y < ty * ts + ts && y < H; y++)
             for (int x = tx * ts; x < tx * ts + ts && x < W; x++) {
@@ -779,7 +781,8 @@ static void chain_one(const or_camera *cam, const or_settings *st, const or_para
 /* backward.py:76-212.  Gradient buffers must be zeroed by the caller
  * (accumulation semantics of GradientBuffer.add, backward.py:65-73). */
 int or_backward(const or_camera *cam, const or_settings *st, const or_params *P, const or_view *V,
-                const int64_t *tile_off, const int32_t *items, const double *d_image, or_grads *G) {
+                const int64_t *tile_off, const int32_t *items, const double *d_image, const int64_t *tile_list,
+                int64_t n_list, or_grads *G) {
     const int W = cam->width, H = cam->height, ts = st->tile, k = V->k;
     const int64_t T = (int64_t)((W + ts - 1) / ts) * ((H + ts - 1) / ts);
     const int nv = V->n_visible;
@@ -792,11 +795,13 @@ int or_backward(const or_camera *cam, const or_settings *st, const or_params *P,
     S.gn = calloc((size_t)nv * k * 2 + 1, sizeof(double));
     S.gs = calloc((size_t)nv * k + 1, sizeof(double));
     int64_t ne = 0;
+    const int64_t nt_list = tile_list ? n_list : T;
 #ifdef _OPENMP
     int nt = st->n_threads > 0 ? st->n_threads : 1;
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : ne) num_threads(nt)
 #endif
-    for (int64_t t = 0; t < T; t++) backward_tile(cam, st, V, tile_off, items, t, d_image, &S, G->visible, &ne);
+    for (int64_t q = 0; q < nt_list; q++)
+        backward_tile(cam, st, V, tile_off, items, tile_list ? tile_list[q] : q, d_image, &S, G->visible, &ne);
     G->n_eval = ne;
 #ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic, 256) num_threads(nt)

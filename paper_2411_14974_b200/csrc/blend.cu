@@ -37,10 +37,12 @@ struct BlendArgs {
   int32_t *count;
   uint8_t *visible;
   int32_t *pixel_last;
+  float *pixel_T;
   uint8_t *pixel_clamp;
   // backward
   const float *d_image;
   float *accum;
+  unsigned long long *stats;
 };
 
 template <int MAXK>
@@ -81,7 +83,9 @@ __device__ __forceinline__ Eval eval_field(const float *rec, int nl, float dx, f
   const float phi2 = m + lg2(s);
   const float u = ex2(rec[R_SIGMA] * phi2);
   e.I = rcp(1.f + u);
-  e.J = fminf(u * e.I, 1.f);  // 1 - I without cancellation (u = inf -> NaN -> 1)
+  // 1 - I without cancellation: u*I while I >= 1/2, else 1 - I (also covers
+  // u so large that I flushes to zero)
+  e.J = u > 1.f ? 1.f - e.I : u * e.I;
   e.alpha_raw = rec[R_OPACITY] * e.I;
   e.alpha = fminf(e.alpha_raw, (float)kAlphaMaxD);
   e.phi2 = phi2;
@@ -112,6 +116,7 @@ __global__ void __launch_bounds__(kBlendThreads) forward_kernel(BlendArgs a) {
   const float qx = px + 0.5f, qy = py + 0.5f;
   float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Wsum = 0.f, D = 0.f;
   int cnt = 0, last = -1;
+  unsigned n_eval = 0, n_lines = 0;
   bool done = !inside;
   const bool use_floor = a.floor > 0.f;
   float z[MAXK];
@@ -125,6 +130,8 @@ __global__ void __launch_bounds__(kBlendThreads) forward_kernel(BlendArgs a) {
       if (!in_bbox(rec, px, py)) continue;
       const int nl = __float_as_int(rec[R_NLINES]);
       const Eval e = eval_field<MAXK>(rec, nl, qx - rec[R_AX], qy - rec[R_AY], z);
+      n_eval++;
+      n_lines += nl;
       if (!(e.alpha >= a.cutoff)) continue;
       const float w = T * e.alpha;
       C0 = fmaf(w, rec[R_R], C0);
@@ -141,6 +148,9 @@ __global__ void __launch_bounds__(kBlendThreads) forward_kernel(BlendArgs a) {
     __syncthreads();
     if (a.visible && threadIdx.x < nb && s_vis[threadIdx.x]) a.visible[s_id[threadIdx.x]] = 1;
   }
+  block_add_u64(a.stats + S_FWD_EVALS, n_eval);
+  block_add_u64(a.stats + S_FWD_LINES, n_lines);
+  block_add_u64(a.stats + S_FWD_BLENDS, (unsigned)cnt);
   if (!inside) return;
   const size_t p = (size_t)py * a.width + px;
   const float v0 = fmaf(T, a.bg[0], C0), v1 = fmaf(T, a.bg[1], C1), v2 = fmaf(T, a.bg[2], C2);
@@ -148,6 +158,7 @@ __global__ void __launch_bounds__(kBlendThreads) forward_kernel(BlendArgs a) {
   a.image[3 * p + 1] = fminf(fmaxf(v1, 0.f), 1.f);
   a.image[3 * p + 2] = fminf(fmaxf(v2, 0.f), 1.f);
   a.final_T[p] = T;
+  a.pixel_T[p] = T;
   a.weight_sum[p] = Wsum;
   a.count[p] = cnt;
   if (a.depth) a.depth[p] = D;
@@ -189,11 +200,12 @@ __global__ void __launch_bounds__(kBlendThreads) backward_kernel(BlendArgs a) {
   const uint2 range = a.ranges[tile];
   if (range.y <= range.x) return;
   const float qx = px + 0.5f, qy = py + 0.5f;
+  unsigned n_eval = 0, n_lines = 0;
   float T = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
   int last = -1;
   if (inside) {
     const size_t p = (size_t)py * a.width + px;
-    T = a.final_T[p];
+    T = a.pixel_T[p];
     last = a.pixel_last[p];
     const uint32_t cm = a.pixel_clamp[p];
     g0 = (cm & 1) ? a.d_image[3 * p] : 0.f;
@@ -220,6 +232,8 @@ __global__ void __launch_bounds__(kBlendThreads) backward_kernel(BlendArgs a) {
       if (contrib) {
         const float dx = qx - rec[R_AX], dy = qy - rec[R_AY];
         const Eval e = eval_field<MAXK>(rec, nl, dx, dy, z);
+        n_eval++;
+        n_lines += nl;
         contrib = e.alpha >= a.cutoff;
         if (contrib) {
           const float o = rec[R_OPACITY], sig = rec[R_SIGMA], dls = rec[R_DLS];
@@ -271,6 +285,8 @@ __global__ void __launch_bounds__(kBlendThreads) backward_kernel(BlendArgs a) {
     }
     __syncthreads();
   }
+  block_add_u64(a.stats + S_BWD_EVALS, n_eval);
+  block_add_u64(a.stats + S_BWD_LINES, n_lines);
 }
 
 static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const cs_layout &L, char *ws) {
@@ -285,8 +301,10 @@ static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const c
   a.floor = (float)set.floor;
   for (int c = 0; c < 3; c++) a.bg[c] = (float)set.background[c];
   a.pixel_last = reinterpret_cast<int32_t *>(ws + L.pixel_last);
+  a.pixel_T = reinterpret_cast<float *>(ws + L.pixel_T);
   a.pixel_clamp = reinterpret_cast<uint8_t *>(ws + L.pixel_clamp);
   a.accum = reinterpret_cast<float *>(ws + L.grad_accum);
+  a.stats = reinterpret_cast<unsigned long long *>(ws + L.counters + sizeof(uint32_t) * C_STATS);
   a.image = a.final_T = a.weight_sum = a.depth = nullptr;
   a.count = nullptr;
   a.visible = nullptr;

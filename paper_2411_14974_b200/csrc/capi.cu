@@ -69,6 +69,7 @@ int cs_workspace_layout(const cs_camera *cam, const cs_settings *set, int64_t n,
   L.pair_ids = take(sizeof(uint32_t) * cap);
   L.tile_ranges = take(sizeof(uint32_t) * 2 * tiles);
   L.pixel_last = take(sizeof(int32_t) * npix);
+  L.pixel_T = take(sizeof(float) * npix);
   L.pixel_clamp = take(npix);
   L.grad_accum = take(sizeof(float) * un * L.acc_floats);
   L.scratch_bytes = cs::scratch_bytes(n, pair_capacity, pp, nullptr, nullptr);

@@ -42,7 +42,20 @@ template <int MAXK> struct Acc {
 };
 
 // Counters at the head of the workspace.
-enum Counter { C_NVISIBLE = 0, C_NPAIRS = 1, C_OVERFLOW = 2, C_NSORT = 3, C_CHUNK0 = 4, C_COUNT = 16 };
+enum Counter { C_NVISIBLE = 0, C_NPAIRS = 1, C_OVERFLOW = 2, C_NSORT = 3, C_CHUNK0 = 4, C_STATS = 16, C_COUNT = 32 };
+// uint64 work statistics at word C_STATS (roofline accounting, read by the benchmark)
+enum Stat { S_FWD_EVALS = 0, S_FWD_LINES = 1, S_FWD_BLENDS = 2, S_BWD_EVALS = 3, S_BWD_LINES = 4, S_COUNT = 8 };
+
+// Block-wide sum of a per-thread count, added once per block to a global u64.
+__device__ __forceinline__ void block_add_u64(unsigned long long *dst, unsigned v) {
+  __shared__ unsigned long long s_acc;
+  if (threadIdx.x == 0) s_acc = 0;
+  __syncthreads();
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_acc, (unsigned long long)v);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_acc) atomicAdd(dst, s_acc);
+}
 
 struct Layout {
   cs_layout l;

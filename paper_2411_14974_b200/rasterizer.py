@@ -23,7 +23,8 @@ from .model import (EXACT_SETTINGS, SH_COEFFS, Camera, GradientBuffer, RenderOut
                     RenderSettings, ScalingMode)
 from .scene_tensors import SceneTensors, as_scene_tensors
 
-_COUNTERS = 16
+_COUNTERS = 32
+STAT_NAMES = ("fwd_evals", "fwd_line_evals", "fwd_blends", "bwd_evals", "bwd_line_evals")
 
 
 def _device(device=None) -> torch.device:
@@ -174,6 +175,7 @@ class Rasterizer:
                                               ws.ptr, ws.nbytes, cap, ctypes.byref(frame_c), stream), "cs_forward")
             fr = Frame(outputs["image"], outputs["final_T"], outputs["count"], outputs["weight_sum"],
                        outputs["depth"], outputs["visible"][:n], ws, st, cam_c, set_c, params_c, cap)
+            fr.extras["frame_c"] = frame_c
             if not check:
                 return fr
             counts = (ctypes.c_uint32 * 4)()
@@ -185,6 +187,38 @@ class Rasterizer:
             cap = int(fr.n_pairs * self.growth) + 1024   # overflow: grow and re-render
             if cap >= (1 << 30):
                 raise _lib.CsError(f"{fr.n_pairs} tile pairs exceed the supported 2^30")
+
+    def launch_forward(self, fr: Frame, first_stage: int = 0, last_stage: int = 2):
+        """Re-run forward stages of an existing frame (same scene tensors,
+        camera, workspace and outputs) without any host synchronisation;
+        stages: 0 preprocess, 1 depth order + binning, 2 blend."""
+        ws = fr.workspace
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(_lib.load().cs_forward_stages(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
+                                                 ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
+                                                 ctypes.byref(fr.extras["frame_c"]), first_stage, last_stage,
+                                                 stream), "cs_forward_stages")
+
+    def launch_backward(self, fr: Frame, d_image: torch.Tensor, grads: dict, first_stage: int = 0,
+                        last_stage: int = 1):
+        """Backward stages (0 blend, 1 chain) into ``grads`` (+=), no sync."""
+        g = _lib.CsGrads(grads["points"].data_ptr(), grads["raw_delta"].data_ptr(), grads["raw_sigma"].data_ptr(),
+                         grads["raw_opacity"].data_ptr(), grads["raw_mask"].data_ptr(), grads["sh"].data_ptr())
+        ws = fr.workspace
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(_lib.load().cs_backward_stages(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
+                                                  ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
+                                                  d_image.data_ptr(), ctypes.byref(g), first_stage, last_stage,
+                                                  stream), "cs_backward_stages")
+
+    @staticmethod
+    def read_stats(fr: Frame) -> dict:
+        """Work counters of the last forward/backward on this workspace (syncs)."""
+        c = fr.workspace.counters().cpu()
+        stats = c[16:32].view(torch.int64).numpy()
+        out = {name: int(stats[i]) for i, name in enumerate(STAT_NAMES)}
+        out.update(n_visible=int(c[0]), n_pairs=int(c[1]), overflow=int(c[2]))
+        return out
 
     def backward(self, frame: Frame, d_image: torch.Tensor, grads: dict) -> dict:
         """Accumulate (+=) gradients of sum(d_image * image) into ``grads``."""

@@ -60,7 +60,8 @@ def test_workspace_layout_regions_are_disjoint_and_aligned(lib):
     assert (L.tiles_x, L.tiles_y) == (120, 68)
     assert L.max_k == 8 and L.rec_floats == 40 and L.acc_floats == 32
     names = ["counters", "records", "hull", "bbox", "depth_keys", "order", "tiles_touched", "pair_offsets",
-             "pair_tiles", "pair_ids", "tile_ranges", "pixel_last", "pixel_clamp", "grad_accum", "scratch"]
+             "pair_tiles", "pair_ids", "tile_ranges", "pixel_last", "pixel_T", "pixel_clamp", "grad_accum",
+             "scratch"]
     offs = [getattr(L, n) for n in names]
     assert offs == sorted(offs)
     assert all(o % 256 == 0 for o in offs)
