@@ -14,53 +14,13 @@
 
 namespace cs {
 
-__constant__ double kC0 = 0.28209479177387814;
-__constant__ double kC1 = 0.4886025119029199;
-__constant__ double kC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
-                              -1.0925484305920792, 0.5462742152960396};
-__constant__ double kC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
-                              0.3731763325901154, -0.4570457994644658, 1.445305721320277,
-                              -0.5900435899266435};
-
-// harmonics.py:33-59 (basis) and :62-98 (gradient rows)
-__device__ void sh_basis_and_grad(double x, double y, double z, int deg, double *b, double (*g)[3]) {
-  for (int i = 0; i < kShCoeffs; i++) { b[i] = 0.0; g[i][0] = g[i][1] = g[i][2] = 0.0; }
-  b[0] = kC0;
-  if (deg >= 1) {
-    b[1] = -kC1 * y; b[2] = kC1 * z; b[3] = -kC1 * x;
-    g[1][1] = -kC1; g[2][2] = kC1; g[3][0] = -kC1;
-  }
-  const double xx = x * x, yy = y * y, zz = z * z;
-  if (deg >= 2) {
-    b[4] = kC2[0] * x * y;
-    b[5] = kC2[1] * y * z;
-    b[6] = kC2[2] * (2.0 * zz - xx - yy);
-    b[7] = kC2[3] * x * z;
-    b[8] = kC2[4] * (xx - yy);
-    g[4][0] = kC2[0] * y; g[4][1] = kC2[0] * x;
-    g[5][1] = kC2[1] * z; g[5][2] = kC2[1] * y;
-    g[6][0] = -2.0 * kC2[2] * x; g[6][1] = -2.0 * kC2[2] * y; g[6][2] = 4.0 * kC2[2] * z;
-    g[7][0] = kC2[3] * z; g[7][2] = kC2[3] * x;
-    g[8][0] = 2.0 * kC2[4] * x; g[8][1] = -2.0 * kC2[4] * y;
-  }
-  if (deg >= 3) {
-    b[9] = kC3[0] * y * (3.0 * xx - yy);
-    b[10] = kC3[1] * x * y * z;
-    b[11] = kC3[2] * y * (4.0 * zz - xx - yy);
-    b[12] = kC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-    b[13] = kC3[4] * x * (4.0 * zz - xx - yy);
-    b[14] = kC3[5] * z * (xx - yy);
-    b[15] = kC3[6] * x * (xx - 3.0 * yy);
-    g[9][0] = kC3[0] * 6.0 * x * y; g[9][1] = kC3[0] * 3.0 * (xx - yy);
-    g[10][0] = kC3[1] * y * z; g[10][1] = kC3[1] * x * z; g[10][2] = kC3[1] * x * y;
-    g[11][0] = -2.0 * kC3[2] * x * y; g[11][1] = kC3[2] * (4.0 * zz - xx - 3.0 * yy); g[11][2] = 8.0 * kC3[2] * y * z;
-    g[12][0] = -6.0 * kC3[3] * x * z; g[12][1] = -6.0 * kC3[3] * y * z;
-    g[12][2] = kC3[3] * (6.0 * zz - 3.0 * xx - 3.0 * yy);
-    g[13][0] = kC3[4] * (4.0 * zz - 3.0 * xx - yy); g[13][1] = -2.0 * kC3[4] * x * y; g[13][2] = 8.0 * kC3[4] * x * z;
-    g[14][0] = 2.0 * kC3[5] * x * z; g[14][1] = -2.0 * kC3[5] * y * z; g[14][2] = kC3[5] * (xx - yy);
-    g[15][0] = kC3[6] * 3.0 * (xx - yy); g[15][1] = -6.0 * kC3[6] * x * y;
-  }
-}
+// harmonics.py:7-24 constants (fp32: the SH VJP is continuous and small)
+constexpr float kC0 = 0.28209479177387814f, kC1 = 0.4886025119029199f;
+constexpr float kC20 = 1.0925484305920792f, kC21 = -1.0925484305920792f, kC22 = 0.31539156525252005f,
+                kC23 = -1.0925484305920792f, kC24 = 0.5462742152960396f;
+constexpr float kC30 = -0.5900435899266435f, kC31 = 2.890611442640554f, kC32 = -0.4570457994644658f,
+                kC33 = 0.3731763325901154f, kC34 = -0.4570457994644658f, kC35 = 1.445305721320277f,
+                kC36 = -0.5900435899266435f;
 
 struct ChainArgs {
   cs_camera cam;
@@ -74,56 +34,146 @@ struct ChainArgs {
   cs_grads g;
 };
 
+template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 128 : 64; }
+
+// SH colour VJP (harmonics.py:112-128): d_sh += Y (x) d_eff and the
+// direction gradient dY/ddir^T (sh . d_eff), with eval_sh_basis_grad
+// (harmonics.py:62-98) written out per basis function.
+__device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const float *sh, const float *d_color,
+                                       float *d_sh, float *ddir) {
+  float Y[kShCoeffs];
+  Y[0] = kC0;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  if (deg >= 1) { Y[1] = -kC1 * y; Y[2] = kC1 * z; Y[3] = -kC1 * x; }
+  if (deg >= 2) {
+    Y[4] = kC20 * x * y; Y[5] = kC21 * y * z; Y[6] = kC22 * (2.f * zz - xx - yy);
+    Y[7] = kC23 * x * z; Y[8] = kC24 * (xx - yy);
+  }
+  if (deg >= 3) {
+    Y[9] = kC30 * y * (3.f * xx - yy); Y[10] = kC31 * x * y * z; Y[11] = kC32 * y * (4.f * zz - xx - yy);
+    Y[12] = kC33 * z * (2.f * zz - 3.f * xx - 3.f * yy); Y[13] = kC34 * x * (4.f * zz - xx - yy);
+    Y[14] = kC35 * z * (xx - yy); Y[15] = kC36 * x * (xx - 3.f * yy);
+  }
+  const int nb = (deg + 1) * (deg + 1);
+  float deff[3];
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    float raw = 0.f;
+#pragma unroll
+    for (int b = 0; b < kShCoeffs; b++)
+      if (b < nb) raw = fmaf(Y[b], sh[3 * b + c], raw);
+    deff[c] = (0.5f + raw) > 0.f ? d_color[c] : 0.f;
+  }
+  float v[kShCoeffs];
+#pragma unroll
+  for (int b = 0; b < kShCoeffs; b++) {
+    v[b] = 0.f;
+    if (b < nb) {
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        d_sh[3 * b + c] += Y[b] * deff[c];
+        v[b] = fmaf(sh[3 * b + c], deff[c], v[b]);
+      }
+    }
+  }
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+  if (deg >= 1) { gy -= kC1 * v[1]; gz += kC1 * v[2]; gx -= kC1 * v[3]; }
+  if (deg >= 2) {
+    gx += kC20 * y * v[4]; gy += kC20 * x * v[4];
+    gy += kC21 * z * v[5]; gz += kC21 * y * v[5];
+    gx += -2.f * kC22 * x * v[6]; gy += -2.f * kC22 * y * v[6]; gz += 4.f * kC22 * z * v[6];
+    gx += kC23 * z * v[7]; gz += kC23 * x * v[7];
+    gx += 2.f * kC24 * x * v[8]; gy += -2.f * kC24 * y * v[8];
+  }
+  if (deg >= 3) {
+    gx += kC30 * 6.f * x * y * v[9]; gy += kC30 * 3.f * (xx - yy) * v[9];
+    gx += kC31 * y * z * v[10]; gy += kC31 * x * z * v[10]; gz += kC31 * x * y * v[10];
+    gx += -2.f * kC32 * x * y * v[11]; gy += kC32 * (4.f * zz - xx - 3.f * yy) * v[11]; gz += 8.f * kC32 * y * z * v[11];
+    gx += -6.f * kC33 * x * z * v[12]; gy += -6.f * kC33 * y * z * v[12];
+    gz += kC33 * (6.f * zz - 3.f * xx - 3.f * yy) * v[12];
+    gx += kC34 * (4.f * zz - 3.f * xx - yy) * v[13]; gy += -2.f * kC34 * x * y * v[13]; gz += 8.f * kC34 * x * z * v[13];
+    gx += 2.f * kC35 * x * z * v[14]; gy += -2.f * kC35 * y * z * v[14]; gz += kC35 * (xx - yy) * v[14];
+    gx += kC36 * 3.f * (xx - yy) * v[15]; gy += -6.f * kC36 * x * y * v[15];
+  }
+  ddir[0] = gx; ddir[1] = gy; ddir[2] = gz;
+}
+
 template <int MAXK>
-__global__ void __launch_bounds__(128) chain_kernel(ChainArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(chain_threads<MAXK>()) chain_kernel(ChainArgs a) {
+  constexpr int kChainThreads = chain_threads<MAXK>();
+  // per-thread slots for the dynamically indexed per-point arrays
+  __shared__ double s_x[MAXK][kChainThreads], s_y[MAXK][kChainThreads];
+  __shared__ double s_dx[MAXK][kChainThreads], s_dy[MAXK][kChainThreads];
+  const int t = threadIdx.x;
+  const int64_t i = (int64_t)blockIdx.x * kChainThreads + t;
   if (i >= a.n || a.touched[i] == 0) return;  // not prepared for this view
   constexpr int RF = Rec<MAXK>::kFloats;
   constexpr int AF = Acc<MAXK>::kFloats;
   const int k = a.k;
-  const float *acc = a.accum + i * AF;
-  const float *rec = a.records + i * RF;
-  const uint8_t *hull = a.hull + i * MAXK;
+  float acc[AF];
+  const float4 *accv = reinterpret_cast<const float4 *>(a.accum + i * AF);
+#pragma unroll
+  for (int q = 0; q < AF / 4; q++) {
+    const float4 v = accv[q];
+    acc[4 * q] = v.x; acc[4 * q + 1] = v.y; acc[4 * q + 2] = v.z; acc[4 * q + 3] = v.w;
+  }
+  const float2 anchor = *reinterpret_cast<const float2 *>(a.records + i * RF);
+  const double ax = anchor.x, ay = anchor.y;
   const double *R = a.cam.R;
   // recompute the projection (projection.py:22-40)
-  double X[MAXK], Y[MAXK], xc[MAXK], yc[MAXK], zc[MAXK];
   double zsum = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
-  for (int j = 0; j < k; j++) {
-    const float *pp = a.points + (i * k + j) * 3;
-    double p0 = pp[0], p1 = pp[1], p2 = pp[2];
-    cx += p0; cy += p1; cz += p2;
-    xc[j] = fma(p2, R[2], fma(p1, R[1], p0 * R[0])) + a.cam.t[0];
-    yc[j] = fma(p2, R[5], fma(p1, R[4], p0 * R[3])) + a.cam.t[1];
-    zc[j] = fma(p2, R[8], fma(p1, R[7], p0 * R[6])) + a.cam.t[2];
-    zsum += zc[j];
-    if (a.cam.ortho) {
-      X[j] = a.cam.fx * xc[j] + a.cam.cx;
-      Y[j] = a.cam.fy * yc[j] + a.cam.cy;
-    } else {
-      X[j] = (a.cam.fx * xc[j]) / zc[j] + a.cam.cx;
-      Y[j] = (a.cam.fy * yc[j]) / zc[j] + a.cam.cy;
+  double xc[MAXK], yc[MAXK], zc[MAXK];
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) {
+    if (j < k) {
+      const float *pp = a.points + (i * k + j) * 3;
+      const double p0 = pp[0], p1 = pp[1], p2 = pp[2];
+      cx += p0; cy += p1; cz += p2;
+      xc[j] = fma(p2, R[2], fma(p1, R[1], p0 * R[0])) + a.cam.t[0];
+      yc[j] = fma(p2, R[5], fma(p1, R[4], p0 * R[3])) + a.cam.t[1];
+      zc[j] = fma(p2, R[8], fma(p1, R[7], p0 * R[6])) + a.cam.t[2];
+      zsum += zc[j];
+      if (a.cam.ortho) {
+        s_x[j][t] = a.cam.fx * xc[j] + a.cam.cx;
+        s_y[j][t] = a.cam.fy * yc[j] + a.cam.cy;
+      } else {
+        s_x[j][t] = (a.cam.fx * xc[j]) / zc[j] + a.cam.cx;
+        s_y[j][t] = (a.cam.fy * yc[j]) / zc[j] + a.cam.cy;
+      }
+      s_dx[j][t] = 0.0;
+      s_dy[j][t] = 0.0;
     }
   }
+  uint8_t hb[MAXK];
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) hb[j] = a.hull[i * MAXK + j];
   int h = 0;
-  while (h < MAXK && hull[h] != 0xff) h++;
-  const double ax = rec[R_AX], ay = rec[R_AY];
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) h += hb[j] != 0xff;
   // lines -> hull vertices (backward.py:231-246)
-  double dpx[MAXK], dpy[MAXK];
-  for (int j = 0; j < k; j++) dpx[j] = dpy[j] = 0.0;
-  for (int j = 0; j < h; j++) {
-    const int u = hull[j], v = hull[(j + 1) % h];
-    const double ex = X[v] - X[u], ey = Y[v] - Y[u];
-    const double len = hypot(ey, ex);
-    const double nx = ey / len, ny = -ex / len;
-    const double gs = acc[A_LINES + 3 * j + 2];
-    // reference gn = sum dL*q - gs*v = sum dL*(q-a) + gs*(a - v)
-    const double gx = acc[A_LINES + 3 * j] + gs * (ax - X[u]);
-    const double gy = acc[A_LINES + 3 * j + 1] + gs * (ay - Y[u]);
-    const double nd = nx * gx + ny * gy;
-    const double rx = (gx - nx * nd) / len, ry = (gy - ny * nd) / len;
-    const double dex = -ry, dey = rx;
-    dpx[v] += dex; dpy[v] += dey;
-    dpx[u] += -dex - nx * gs; dpy[u] += -dey - ny * gs;
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) {
+    if (j < h) {
+      int v = hb[0];
+#pragma unroll
+      for (int q = 1; q < MAXK; q++)
+        if (q == j + 1) v = q < h ? hb[q] : hb[0];
+      const int u = hb[j];
+      const double ux = s_x[u][t], uy = s_y[u][t];
+      const double ex = s_x[v][t] - ux, ey = s_y[v][t] - uy;
+      const double len = hypot(ey, ex);
+      const double nx = ey / len, ny = -ex / len;
+      const double gs = acc[A_LINES + 3 * j + 2];
+      // reference gn = sum dL*q - gs*v = sum dL*(q-a) + gs*(a - v)
+      const double gx = acc[A_LINES + 3 * j] + gs * (ax - ux);
+      const double gy = acc[A_LINES + 3 * j + 1] + gs * (ay - uy);
+      const double nd = nx * gx + ny * gy;
+      const double rx = (gx - nx * nd) / len, ry = (gy - ny * nd) / len;
+      s_dx[v][t] += -ry;
+      s_dy[v][t] += rx;
+      s_dx[u][t] += ry - nx * gs;
+      s_dy[u][t] += -rx - ny * gs;
+    }
   }
   // depth, scale and activations (rasterize.py:99-103, field.py:26-48)
   const double depth = zsum / k;
@@ -138,52 +188,52 @@ __global__ void __launch_bounds__(128) chain_kernel(ChainArgs a) {
   const double delta = exp((double)a.raw_delta[i]), sigma = exp((double)a.raw_sigma[i]);
   const double ddel = acc[A_DDEL], dsig = acc[A_DSIG];
   const double d_depth = a.cam.ortho ? 0.0 : (ddel * delta + dsig * sigma) * sgrad;
-  // view direction (rasterize.py:110-113)
+  // view direction (rasterize.py:110-113) and SH VJP (harmonics.py:112-128)
   const double vx = cx / k - a.cam_center[0], vy = cy / k - a.cam_center[1], vz = cz / k - a.cam_center[2];
   const double dist = sqrt(vx * vx + vy * vy + vz * vz);
   double dir[3] = {0.0, 0.0, 1.0};
   if (dist > 0.0) { dir[0] = vx / dist; dir[1] = vy / dist; dir[2] = vz / dist; }
-  // SH VJP (harmonics.py:112-128)
-  double basis[kShCoeffs], bg[kShCoeffs][3];
-  sh_basis_and_grad(dir[0], dir[1], dir[2], a.sh_degree, basis, bg);
-  const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
-  const float *sh = a.sh + i * kShCoeffs * 3;
-  double deff[3];
-  for (int c = 0; c < 3; c++) {
-    double raw = 0.0;
-    for (int b = 0; b < nb; b++) raw += basis[b] * (double)sh[3 * b + c];
-    deff[c] = (0.5 + raw) > 0.0 ? (double)acc[A_DC + c] : 0.0;
+  float shf[kShCoeffs * 3], dsh[kShCoeffs * 3];
+  const float4 *shv = reinterpret_cast<const float4 *>(a.sh + i * kShCoeffs * 3);
+  float4 *dshv = reinterpret_cast<float4 *>(a.g.d_sh + i * kShCoeffs * 3);
+#pragma unroll
+  for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
+    const float4 v = __ldg(shv + q);
+    shf[4 * q] = v.x; shf[4 * q + 1] = v.y; shf[4 * q + 2] = v.z; shf[4 * q + 3] = v.w;
+    const float4 d = dshv[q];
+    dsh[4 * q] = d.x; dsh[4 * q + 1] = d.y; dsh[4 * q + 2] = d.z; dsh[4 * q + 3] = d.w;
   }
-  float *dsh = a.g.d_sh + i * kShCoeffs * 3;
-  double ddir[3] = {0.0, 0.0, 0.0};
-  for (int b = 0; b < nb; b++) {
-    double vb = 0.0;
-    for (int c = 0; c < 3; c++) {
-      dsh[3 * b + c] += (float)(basis[b] * deff[c]);
-      vb += (double)sh[3 * b + c] * deff[c];
-    }
-    for (int q = 0; q < 3; q++) ddir[q] += bg[b][q] * vb;
-  }
-  const double dot = dir[0] * ddir[0] + dir[1] * ddir[1] + dir[2] * ddir[2];
+  float ddirf[3];
+  sh_vjp((float)dir[0], (float)dir[1], (float)dir[2], a.sh_degree, shf, acc + A_DC, dsh, ddirf);
+#pragma unroll
+  for (int q = 0; q < kShCoeffs * 3 / 4; q++)
+    dshv[q] = make_float4(dsh[4 * q], dsh[4 * q + 1], dsh[4 * q + 2], dsh[4 * q + 3]);
+  const double dot = dir[0] * ddirf[0] + dir[1] * ddirf[1] + dir[2] * ddirf[2];
   double dcen[3];
-  for (int q = 0; q < 3; q++) dcen[q] = dist > 0.0 ? (ddir[q] - dir[q] * dot) / dist : 0.0;
+#pragma unroll
+  for (int q = 0; q < 3; q++) dcen[q] = dist > 0.0 ? (ddirf[q] - dir[q] * dot) / dist : 0.0;
   // projection Jacobian + depth + centre paths into d_points (backward.py:248-269, 281-282)
   float *dp = a.g.d_points + i * k * 3;
-  for (int j = 0; j < k; j++) {
-    double d0, d1, d2;
-    if (a.cam.ortho) {
-      d0 = a.cam.fx * dpx[j]; d1 = a.cam.fy * dpy[j]; d2 = 0.0;
-    } else {
-      const double z = zc[j];
-      d0 = a.cam.fx / z * dpx[j];
-      d1 = a.cam.fy / z * dpy[j];
-      d2 = -(a.cam.fx * xc[j] / (z * z)) * dpx[j] - (a.cam.fy * yc[j] / (z * z)) * dpy[j];
-    }
-    for (int c = 0; c < 3; c++) {
-      double v = d0 * R[c] + d1 * R[3 + c] + d2 * R[6 + c];
-      v += d_depth * R[6 + c] / k;
-      v += dcen[c] / k;
-      dp[3 * j + c] += (float)v;
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) {
+    if (j < k) {
+      const double gx = s_dx[j][t], gy = s_dy[j][t];
+      double d0, d1, d2;
+      if (a.cam.ortho) {
+        d0 = a.cam.fx * gx; d1 = a.cam.fy * gy; d2 = 0.0;
+      } else {
+        const double z = zc[j];
+        d0 = a.cam.fx / z * gx;
+        d1 = a.cam.fy / z * gy;
+        d2 = -(a.cam.fx * xc[j] / (z * z)) * gx - (a.cam.fy * yc[j] / (z * z)) * gy;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        double v = d0 * R[c] + d1 * R[3 + c] + d2 * R[6 + c];
+        v += d_depth * R[6 + c] / k;
+        v += dcen[c] / k;
+        dp[3 * j + c] += (float)v;
+      }
     }
   }
   a.g.d_raw_delta[i] += (float)(ddel * s * delta);
@@ -216,11 +266,10 @@ int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &
   a.hull = reinterpret_cast<const uint8_t *>(ws + L.hull);
   a.touched = reinterpret_cast<const uint32_t *>(ws + L.tiles_touched);
   a.g = g;
-  const int blocks = (int)((p.n + 127) / 128);
   if (L.max_k == 8)
-    chain_kernel<8><<<blocks, 128, 0, s>>>(a);
+    chain_kernel<8><<<(int)((p.n + 127) / 128), chain_threads<8>(), 0, s>>>(a);
   else
-    chain_kernel<16><<<blocks, 128, 0, s>>>(a);
+    chain_kernel<16><<<(int)((p.n + 63) / 64), chain_threads<16>(), 0, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
 

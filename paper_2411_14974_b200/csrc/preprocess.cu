@@ -168,51 +168,170 @@ __device__ __forceinline__ double depth_scale(int mode, double d) {  // field.py
 
 constexpr int kPreThreads = 128;
 
-// One convex.  pts_s / sh_s point at this convex's rows staged in smem.
+// Index list of up to 16 entries packed as 4-bit nibbles in a register, so
+// the Graham scan's insert / erase / pop keep no per-thread local memory.
+struct NibbleList {
+  uint64_t w = 0;
+  int n = 0;
+  __device__ __forceinline__ static uint64_t low(int i) { return i >= 16 ? ~0ull : ((1ull << (4 * i)) - 1ull); }
+  __device__ __forceinline__ int get(int i) const { return (int)((w >> (4 * i)) & 15ull); }
+  __device__ __forceinline__ void set(int i, int v) { w = (w & ~(15ull << (4 * i))) | ((uint64_t)v << (4 * i)); }
+  __device__ __forceinline__ void push(int v) { w |= (uint64_t)v << (4 * n); n++; }
+  __device__ __forceinline__ void pop() { n--; w &= low(n); }
+  __device__ __forceinline__ void insert(int i, int v) {
+    w = (w & low(i)) | ((uint64_t)v << (4 * i)) | ((w & ~low(i)) << 4);
+    n++;
+  }
+  __device__ __forceinline__ void erase(int i) {
+    w = (w & low(i)) | ((w >> 4) & ~low(i));
+    n--;
+  }
+};
+
+// projection.py:47-113 on points X[j*stride], Y[j*stride] (shared memory),
+// n <= 16.  Same algorithm as graham_scan_dev (CPython list.sort
+// count_run + binary insertion for the tolerance comparator), with the
+// index lists held in registers.
+__device__ int graham_scan_packed(int n, const double *X, const double *Y, int stride, NibbleList &out) {
+#define GX(i) X[(i) * stride]
+#define GY(i) Y[(i) * stride]
+  if (n < 3) return 0;
+  NibbleList uq;
+  for (int i = 0; i < n; i++) {
+    const double xi = GX(i), yi = GY(i);
+    bool dup = false;
+    for (int j = 0; j < uq.n; j++) {
+      const int u = uq.get(j);
+      if (GX(u) == xi && GY(u) == yi) { dup = true; break; }
+    }
+    if (!dup) uq.push(i);
+  }
+  if (uq.n < 3) return 0;
+  int ref = uq.get(0);
+  for (int j = 1; j < uq.n; j++) {
+    const int u = uq.get(j);
+    if (GY(u) < GY(ref) || (GY(u) == GY(ref) && GX(u) < GX(ref))) ref = u;
+  }
+  const double rx = GX(ref), ry = GY(ref);
+  auto lt = [&](int a, int b) -> bool {  // cmp(a, b) < 0, projection.py:73-85
+    const double ax = GX(a) - rx, ay = GY(a) - ry, bx = GX(b) - rx, by = GY(b) - ry;
+    const double c = ax * by - ay * bx;
+    if (c > kCrossTol) return true;
+    if (c < -kCrossTol) return false;
+    return (ax * ax + ay * ay) < (bx * bx + by * by);
+  };
+  NibbleList rest;
+  for (int j = 0; j < uq.n; j++)
+    if (uq.get(j) != ref) rest.push(uq.get(j));
+  const int m = rest.n;
+  if (m >= 2) {
+    int run = 2;
+    if (lt(rest.get(1), rest.get(0))) {
+      while (run < m && lt(rest.get(run), rest.get(run - 1))) run++;
+      for (int a = 0, b = run - 1; a < b; a++, b--) {
+        const int t = rest.get(a);
+        rest.set(a, rest.get(b));
+        rest.set(b, t);
+      }
+    } else {
+      while (run < m && !lt(rest.get(run), rest.get(run - 1))) run++;
+    }
+    for (int start = run; start < m; start++) {
+      const int pivot = rest.get(start);
+      int l = 0, r = start;
+      do {
+        const int p = l + ((r - l) >> 1);
+        if (lt(pivot, rest.get(p))) r = p; else l = p + 1;
+      } while (l < r);
+      rest.erase(start);
+      rest.insert(l, pivot);
+    }
+  }
+  auto cross = [&](int o, int a, int b) -> double {  // projection.py:43-44
+    return (GX(a) - GX(o)) * (GY(b) - GY(o)) - (GY(a) - GY(o)) * (GX(b) - GX(o));
+  };
+  NibbleList st;
+  st.push(ref);
+  for (int j = 0; j < m; j++) {
+    const int c = rest.get(j);
+    while (st.n >= 2 && cross(st.get(st.n - 2), st.get(st.n - 1), c) <= kCrossTol) st.pop();
+    st.push(c);
+  }
+  bool changed = true;
+  while (changed && st.n >= 3) {
+    changed = false;
+    const int sn = st.n;
+    for (int q = 0; q < sn; q++) {
+      if (cross(st.get((q - 1 + sn) % sn), st.get(q), st.get((q + 1) % sn)) <= kCrossTol) {
+        st.erase(q);
+        changed = true;
+        break;
+      }
+    }
+  }
+  if (st.n < 3) return 0;
+  int start = 0;
+  for (int q = 0; q < st.n; q++)
+    if (st.get(q) == ref) { start = q; break; }
+  out = NibbleList();
+  for (int q = 0; q < st.n; q++) out.push(st.get((start + q) % st.n));
+  return out.n;
+#undef GX
+#undef GY
+}
+
+// One convex.  pts_s: this convex's K points staged in smem; X, Y: this
+// thread's projected-pixel slots in smem (stride kPreThreads).
 template <int MAXK>
-__device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, const float *sh_g) {
+__device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, double *X, double *Y) {
   const int k = a.k;
-  uint8_t *hull_out = a.hull + i * MAXK;
   a.touched[i] = 0u;
   a.depth_keys[i] = kCulledKey;
   a.order[i] = (uint32_t)i;
   // rasterize.py:89 mask gate (model.py:105-107, expit = 1/(1+exp(-x)))
-  double mask = 1.0 / (1.0 + exp(-(double)a.raw_mask[i]));
+  const double mask = 1.0 / (1.0 + exp(-(double)a.raw_mask[i]));
   if (mask <= kMaskGate) return false;
   // projection.py:22-40
-  double X[MAXK], Y[MAXK];
-  double zsum = 0.0;
-  bool culled = false;
   const double *R = a.cam.R;
+  double zsum = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+  bool culled = false;
   for (int j = 0; j < k; j++) {
-    double p0 = pts_s[3 * j], p1 = pts_s[3 * j + 1], p2 = pts_s[3 * j + 2];
-    double xc = fma(p2, R[2], fma(p1, R[1], p0 * R[0])) + a.cam.t[0];
-    double yc = fma(p2, R[5], fma(p1, R[4], p0 * R[3])) + a.cam.t[1];
-    double zc = fma(p2, R[8], fma(p1, R[7], p0 * R[6])) + a.cam.t[2];
-    if (zc <= a.cam.z_near) culled = true;
-    zsum = zsum + zc;  // rasterize.py:99 mean, left-to-right
+    const double p0 = pts_s[3 * j], p1 = pts_s[3 * j + 1], p2 = pts_s[3 * j + 2];
+    const double xc = fma(p2, R[2], fma(p1, R[1], p0 * R[0])) + a.cam.t[0];
+    const double yc = fma(p2, R[5], fma(p1, R[4], p0 * R[3])) + a.cam.t[1];
+    const double zc = fma(p2, R[8], fma(p1, R[7], p0 * R[6])) + a.cam.t[2];
+    culled |= zc <= a.cam.z_near;
+    zsum = zsum + zc;  // rasterize.py:99 mean, left to right
+    cx = cx + p0;      // model.py:109-111 centre, left to right
+    cy = cy + p1;
+    cz = cz + p2;
     if (a.cam.ortho) {
-      X[j] = a.cam.fx * xc + a.cam.cx;
-      Y[j] = a.cam.fy * yc + a.cam.cy;
+      X[j * kPreThreads] = a.cam.fx * xc + a.cam.cx;
+      Y[j * kPreThreads] = a.cam.fy * yc + a.cam.cy;
     } else {
-      X[j] = (a.cam.fx * xc) / zc + a.cam.cx;
-      Y[j] = (a.cam.fy * yc) / zc + a.cam.cy;
+      X[j * kPreThreads] = (a.cam.fx * xc) / zc + a.cam.cx;
+      Y[j * kPreThreads] = (a.cam.fy * yc) / zc + a.cam.cy;
     }
   }
   if (culled) return false;
-  int hidx[MAXK];
-  const int h = graham_scan_dev<MAXK>(k, X, Y, hidx);
+  NibbleList hull;
+  const int h = graham_scan_packed(k, X, Y, kPreThreads, hull);
   if (h == 0) return false;
-  // projection.py:116-128
-  double nx[MAXK], ny[MAXK], off[MAXK];
-  for (int j = 0; j < h; j++) {
-    int u = hidx[j], v = hidx[(j + 1) % h];
-    double ex = X[v] - X[u], ey = Y[v] - Y[u];
-    double rx = ey, ry = -ex;
-    double len = sqrt(rx * rx + ry * ry);
-    nx[j] = rx / len;
-    ny[j] = ry / len;
-    off[j] = -(nx[j] * X[u] + ny[j] * Y[u]);
+  // projection.py:116-128 (static register slots, j < h)
+  double nx[MAXK], ny[MAXK], off[MAXK], vx[MAXK], vy[MAXK];
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) {
+    if (j < h) {
+      const int u = hull.get(j), v = hull.get(j + 1 < h ? j + 1 : 0);
+      vx[j] = X[u * kPreThreads];
+      vy[j] = Y[u * kPreThreads];
+      const double ex = X[v * kPreThreads] - vx[j], ey = Y[v * kPreThreads] - vy[j];
+      const double rx = ey, ry = -ex;
+      const double len = sqrt(rx * rx + ry * ry);
+      nx[j] = rx / len;
+      ny[j] = ry / len;
+      off[j] = -(nx[j] * vx[j] + ny[j] * vy[j]);
+    }
   }
   // rasterize.py:99-103
   const double depth = zsum / k;
@@ -230,15 +349,23 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
     double eps = a.cutoff / o;
     if (0.5 < eps) eps = 0.5;
     const double margin = log((1.0 - eps) / eps) / (sigma_s * delta_s);
+    double pnx = 0.0, pny = 0.0;  // normal of the line ending at vertex 0 (line h-1)
+#pragma unroll
+    for (int j = 0; j < MAXK; j++)
+      if (j == h - 1) { pnx = nx[j]; pny = ny[j]; }
     double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
-    for (int j = 0; j < h; j++) {
-      int pj = (j - 1 + h) % h;
-      double den = 1.0 + (nx[pj] * nx[j] + ny[pj] * ny[j]);
-      if (!(den >= 1e-12)) den = 1e-12;
-      double ix = X[hidx[j]] + (margin * (nx[pj] + nx[j])) / den;
-      double iy = Y[hidx[j]] + (margin * (ny[pj] + ny[j])) / den;
-      xmin = fmin(xmin, ix); xmax = fmax(xmax, ix);
-      ymin = fmin(ymin, iy); ymax = fmax(ymax, iy);
+#pragma unroll
+    for (int j = 0; j < MAXK; j++) {
+      if (j < h) {
+        double den = 1.0 + (pnx * nx[j] + pny * ny[j]);
+        if (!(den >= 1e-12)) den = 1e-12;
+        const double ix = vx[j] + (margin * (pnx + nx[j])) / den;
+        const double iy = vy[j] + (margin * (pny + ny[j])) / den;
+        xmin = fmin(xmin, ix); xmax = fmax(xmax, ix);
+        ymin = fmin(ymin, iy); ymax = fmax(ymax, iy);
+        pnx = nx[j];
+        pny = ny[j];
+      }
     }
     double fx0 = ceil(xmin - 0.5), fx1 = floor(xmax - 0.5) + 1.0;
     double fy0 = ceil(ymin - 0.5), fy1 = floor(ymax - 0.5) + 1.0;
@@ -247,30 +374,44 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
     if (!(fx0 < fx1) || !(fy0 < fy1)) return false;
     x0 = (int)fx0; x1 = (int)fx1; y0 = (int)fy0; y1 = (int)fy1;
   }
-  // rasterize.py:110-114 view direction from the point mean (model.py:109-111)
-  double cx = 0.0, cy = 0.0, cz = 0.0;
-  for (int j = 0; j < k; j++) {
-    cx = cx + (double)pts_s[3 * j];
-    cy = cy + (double)pts_s[3 * j + 1];
-    cz = cz + (double)pts_s[3 * j + 2];
-  }
-  double vx = cx / k - a.cam_center[0], vy = cy / k - a.cam_center[1], vz = cz / k - a.cam_center[2];
-  double dist = sqrt(vx * vx + vy * vy + vz * vz);
+  // rasterize.py:110-114 view direction; harmonics.py:101-109 colour
+  const double dvx = cx / k - a.cam_center[0], dvy = cy / k - a.cam_center[1], dvz = cz / k - a.cam_center[2];
+  const double dist = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
   double dx = 0.0, dy = 0.0, dz = 1.0;
-  if (dist > 0.0) { dx = vx / dist; dy = vy / dist; dz = vz / dist; }
+  if (dist > 0.0) { dx = dvx / dist; dy = dvy / dist; dz = dvz / dist; }
   double basis[kShCoeffs];
   sh_basis(dx, dy, dz, a.sh_degree, basis);
+  const float4 *shv = reinterpret_cast<const float4 *>(a.sh + i * kShCoeffs * 3);
+  float shf[kShCoeffs * 3];
+#pragma unroll
+  for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
+    const float4 t = __ldg(shv + q);
+    shf[4 * q] = t.x; shf[4 * q + 1] = t.y; shf[4 * q + 2] = t.z; shf[4 * q + 3] = t.w;
+  }
   const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
   double col[3];
+#pragma unroll
   for (int c = 0; c < 3; c++) {
     double acc = 0.0;
-    for (int b = 0; b < nb; b++) acc += basis[b] * (double)__ldg(sh_g + 3 * b + c);
-    double raw = 0.5 + acc;
-    col[c] = raw > 0.0 ? raw : 0.0;   // harmonics.py:108-109
+#pragma unroll
+    for (int b = 0; b < kShCoeffs; b++)
+      if (b < nb) acc += basis[b] * (double)shf[3 * b + c];
+    const double raw = 0.5 + acc;
+    col[c] = raw > 0.0 ? raw : 0.0;
   }
 
   // ---- outputs ----
-  for (int j = 0; j < MAXK; j++) hull_out[j] = (uint8_t)(j < h ? hidx[j] : 0xff);
+  uint8_t hb[MAXK];
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) hb[j] = (uint8_t)(j < h ? hull.get(j) : 0xff);
+  if (MAXK == 8) {
+    *reinterpret_cast<uint2 *>(a.hull + i * MAXK) =
+        make_uint2(hb[0] | hb[1] << 8 | hb[2] << 16 | (uint32_t)hb[3] << 24,
+                   hb[4] | hb[5] << 8 | hb[6] << 16 | (uint32_t)hb[7] << 24);
+  } else {
+#pragma unroll
+    for (int j = 0; j < MAXK; j++) a.hull[i * MAXK + j] = hb[j];
+  }
   a.bbox[i] = make_int4(x0, x1, y0, y1);
   a.touched[i] = (uint32_t)(((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1));
   a.depth_keys[i] = orderable_bits(depth);
@@ -292,10 +433,12 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
   rec[R_NLINES] = __int_as_float(h);
   rec[R_BBX] = __int_as_float(x0 | (x1 << 16));
   rec[R_BBY] = __int_as_float(y0 | (y1 << 16));
+#pragma unroll
   for (int f = 13; f < R_HEADER; f++) rec[f] = 0.f;
+#pragma unroll
   for (int j = 0; j < MAXK; j++) {
     if (j < h) {
-      double c = off[j] + nx[j] * ax + ny[j] * ay;  // anchor-relative offset, fp64
+      const double c = off[j] + nx[j] * ax + ny[j] * ay;  // anchor-relative offset, fp64
       rec[R_HEADER + 3 * j] = (float)(dls * nx[j]);
       rec[R_HEADER + 3 * j + 1] = (float)(dls * ny[j]);
       rec[R_HEADER + 3 * j + 2] = (float)(dls * c);
@@ -313,7 +456,9 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
 
 template <int MAXK>
 __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreArgs a) {
-  extern __shared__ float pts_smem[];  // [kPreThreads][k*3]
+  extern __shared__ double pre_smem[];  // X[MAXK][threads], Y[MAXK][threads], points[threads][k*3]
+  double *Xs = pre_smem, *Ys = pre_smem + MAXK * kPreThreads;
+  float *pts_smem = reinterpret_cast<float *>(pre_smem + 2 * MAXK * kPreThreads);
   const int64_t base = (int64_t)blockIdx.x * kPreThreads;
   const int rowf = a.k * 3;
   const int64_t nblk = min((int64_t)kPreThreads, a.n - base);
@@ -323,7 +468,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreArgs a) {
   __syncthreads();
   const int64_t i = base + threadIdx.x;
   bool vis = false;
-  if (i < a.n) vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, a.sh + i * kShCoeffs * 3);
+  if (i < a.n) vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, Xs + threadIdx.x, Ys + threadIdx.x);
   unsigned b = __ballot_sync(0xffffffffu, vis);
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(&a.counters[C_NVISIBLE], (unsigned)__popc(b));
 }
@@ -340,7 +485,14 @@ __global__ void hull_batch_kernel(int m, int npts, const int32_t *counts, const 
     Y[j] = pts[((int64_t)s * npts + j) * 2 + 1];
   }
   int out[32];
-  int h = graham_scan_dev<32>(n, X, Y, out);
+  int h;
+  if (n <= 16) {  // the scan the preprocess kernel runs
+    NibbleList l;
+    h = graham_scan_packed(n, X, Y, 1, l);
+    for (int j = 0; j < h; j++) out[j] = l.get(j);
+  } else {
+    h = graham_scan_dev<32>(n, X, Y, out);
+  }
   for (int j = 0; j < npts; j++) hull[(int64_t)s * npts + j] = j < h ? out[j] : -1;
   hull_n[s] = h;
 }
@@ -374,7 +526,7 @@ int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_par
   a.counters = reinterpret_cast<uint32_t *>(ws + L.counters);
   camera_center(cam, a.cam_center);
   const int blocks = (int)((p.n + kPreThreads - 1) / kPreThreads);
-  const size_t smem = (size_t)kPreThreads * p.k * 3 * sizeof(float);
+  const size_t smem = (size_t)kPreThreads * (2 * L.max_k * sizeof(double) + p.k * 3 * sizeof(float));
   if (L.max_k == 8) {
     preprocess_kernel<8><<<blocks, kPreThreads, smem, s>>>(a);
   } else {

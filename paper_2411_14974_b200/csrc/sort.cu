@@ -82,10 +82,47 @@ struct PassArgs {
   uint32_t *chunk_counter;
 };
 
+// exclusive scan of one value per thread over a 256-thread block
+__device__ __forceinline__ uint32_t block_exclusive_scan256(uint32_t v, uint32_t *s_warp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t x = lane < kSortWarps ? s_warp[lane] : 0;
+    uint32_t y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += u;
+    }
+    if (lane < kSortWarps) s_warp[lane] = y - x;
+  }
+  __syncthreads();
+  return s_warp[w] + inc - v;
+}
+
+template <typename KeyT>
+constexpr size_t onesweep_dyn_smem() { return (size_t)kSortChunk * (sizeof(KeyT) + sizeof(uint32_t)); }
+
+// One LSD digit.  Items are ranked per warp with __match_any_sync, the
+// chunk's digit counts are published for decoupled look-back, and the chunk
+// is first scattered into shared memory in digit order so that the global
+// writes come out as contiguous runs per digit (coalesced).
 template <typename KeyT>
 __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a) {
+  extern __shared__ __align__(16) unsigned char onesweep_dyn[];
+  KeyT *s_keys = reinterpret_cast<KeyT *>(onesweep_dyn);
+  uint32_t *s_vals = reinterpret_cast<uint32_t *>(onesweep_dyn + sizeof(KeyT) * kSortChunk);
   __shared__ uint32_t s_hist[kSortWarps][kRadix];
+  __shared__ uint32_t s_dexcl[kRadix];
   __shared__ uint32_t s_base[kRadix];
+  __shared__ uint32_t s_warp[kSortWarps];
   __shared__ uint32_t s_chunk;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (t == 0) s_chunk = atomicAdd(a.chunk_counter, 1u);
@@ -95,6 +132,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a
   const uint32_t n = a.count ? *a.count : a.n_fixed;
   const uint32_t start = chunk * kSortChunk;
   if (start >= n) return;  // no later chunk holds items, nobody looks back here
+  const uint32_t nvalid = min((uint32_t)kSortChunk, n - start);
 
   const uint32_t lt_mask = (1u << lane) - 1u;
   KeyT key[kSortItems];
@@ -104,8 +142,8 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a
   const uint32_t wbase = start + w * (32 * kSortItems);
 #pragma unroll
   for (int i = 0; i < kSortItems; i++) {
-    uint32_t idx = wbase + i * 32 + lane;
-    bool valid = idx < n;
+    const uint32_t idx = wbase + i * 32 + lane;
+    const bool valid = idx < n;
     key[i] = valid ? a.keys_in[idx] : (KeyT)0;
     val[i] = valid ? a.vals_in[idx] : 0u;
     dig[i] = valid ? (uint32_t)(key[i] >> a.shift) & (kRadix - 1) : kRadix;
@@ -122,58 +160,71 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a
     rank[i] = prev + __popc(peers & lt_mask);
   }
   __syncthreads();
-  {
-    // digit t: exclusive offsets across warps, chunk total, decoupled look-back
-    const int d = t;
-    uint32_t sum = 0;
+  // digit t: exclusive offsets across warps and the chunk total
+  const int d = t;
+  uint32_t sum = 0;
 #pragma unroll
-    for (int ww = 0; ww < kSortWarps; ww++) {
-      uint32_t v = s_hist[ww][d];
-      s_hist[ww][d] = sum;
-      sum += v;
-    }
-    volatile uint32_t *lb = a.lookback;
-    uint32_t excl = 0;
-    if (chunk == 0) {
-      lb[d] = kFlagPrefix | sum;
-    } else {
-      lb[chunk * kRadix + d] = kFlagAgg | sum;
-      int c = (int)chunk - 1;
-      while (true) {
-        uint32_t v = lb[c * kRadix + d];
-        uint32_t flag = v & ~kValueMask;
-        if (flag == 0) continue;
-        excl += v & kValueMask;
-        if (flag == kFlagPrefix) break;
-        c--;
-      }
-      lb[chunk * kRadix + d] = kFlagPrefix | (excl + sum);
-    }
-    s_base[d] = a.offsets[d] + excl;
+  for (int ww = 0; ww < kSortWarps; ww++) {
+    const uint32_t v = s_hist[ww][d];
+    s_hist[ww][d] = sum;
+    sum += v;
   }
+  // publish early, then resolve the prefix from the preceding chunks
+  volatile uint32_t *lb = a.lookback;
+  if (chunk == 0) lb[d] = kFlagPrefix | sum;
+  else lb[chunk * kRadix + d] = kFlagAgg | sum;
+  s_dexcl[d] = block_exclusive_scan256(sum, s_warp);
+  uint32_t excl = 0;
+  if (chunk > 0) {
+    int c = (int)chunk - 1;
+    while (true) {
+      const uint32_t v = lb[c * kRadix + d];
+      const uint32_t flag = v & ~kValueMask;
+      if (flag == 0) continue;
+      excl += v & kValueMask;
+      if (flag == kFlagPrefix) break;
+      c--;
+    }
+    lb[chunk * kRadix + d] = kFlagPrefix | (excl + sum);
+  }
+  s_base[d] = a.offsets[d] + excl;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; i++) {
-    const uint32_t d = dig[i];
-    if (d < kRadix) {
-      uint32_t pos = s_base[d] + s_hist[w][d] + rank[i];
-      a.keys_out[pos] = key[i];
-      a.vals_out[pos] = val[i];
+    const uint32_t dd = dig[i];
+    if (dd < kRadix) {
+      const uint32_t pos = s_dexcl[dd] + s_hist[w][dd] + rank[i];
+      s_keys[pos] = key[i];
+      s_vals[pos] = val[i];
     }
+  }
+  __syncthreads();
+  for (uint32_t q = t; q < nvalid; q += kSortThreads) {
+    const KeyT kk = s_keys[q];
+    const uint32_t dd = (uint32_t)(kk >> a.shift) & (kRadix - 1);
+    const uint32_t gpos = s_base[dd] + (q - s_dexcl[dd]);
+    a.keys_out[gpos] = kk;
+    a.vals_out[gpos] = s_vals[q];
   }
 }
 
 // Full LSD sort over `passes` digits starting at bit shift0.  Ping-pongs
-// (k0,v0) <-> (k1,v1); returns true when the result ends in (k1,v1).
+// (k0,v0) <-> (k1,v1); returns true when the result ends in (k1,v1).  With
+// hist_ready the caller has already accumulated the digit histograms.
 template <typename KeyT>
 static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uint32_t *count,
                        uint32_t n_fixed, uint32_t n_cap, int passes, int shift0, uint32_t *hist,
-                       uint32_t *offsets, uint32_t *lookback, uint32_t *chunk_counters, cudaStream_t s) {
+                       uint32_t *offsets, uint32_t *lookback, uint32_t *chunk_counters, bool hist_ready,
+                       cudaStream_t s) {
   const int chunks = (int)((n_cap + kSortChunk - 1) / kSortChunk);
   if (chunks == 0) return false;
-  const int hist_blocks = min(chunks * 4, 148 * 8);
-  radix_hist_kernel<KeyT><<<hist_blocks, kSortThreads, 0, s>>>(k0, count, n_fixed, passes, shift0, hist);
+  if (!hist_ready) {
+    const int hist_blocks = min(chunks * 4, 148 * 8);
+    radix_hist_kernel<KeyT><<<hist_blocks, kSortThreads, 0, s>>>(k0, count, n_fixed, passes, shift0, hist);
+  }
   radix_offsets_kernel<<<passes, kRadix, 0, s>>>(hist, offsets);
+  constexpr size_t dyn = onesweep_dyn_smem<KeyT>();
+  cudaFuncSetAttribute(onesweep_kernel<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   for (int p = 0; p < passes; p++) {
     PassArgs<KeyT> a;
     bool odd = p & 1;
@@ -187,7 +238,7 @@ static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uin
     a.offsets = offsets + p * kRadix;
     a.lookback = lookback + (size_t)p * chunks * kRadix;
     a.chunk_counter = chunk_counters + p;
-    onesweep_kernel<KeyT><<<chunks, kSortThreads, 0, s>>>(a);
+    onesweep_kernel<KeyT><<<chunks, kSortThreads, dyn, s>>>(a);
   }
   return passes & 1;
 }
@@ -278,34 +329,88 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t 
 }
 
 // ------------------------------------------------------------------ duplicate
-__global__ void duplicate_kernel(const uint32_t *order, const uint32_t *touched, const int4 *bbox,
-                                 const uint32_t *offsets, uint32_t n, uint32_t cap, int tiles_x,
-                                 uint32_t *pair_tiles, uint32_t *pair_ids) {
-  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  uint32_t id = order[r];
-  uint32_t cnt = touched[id];
-  if (cnt == 0) return;
-  uint32_t off = offsets[r];
-  if ((uint64_t)off + cnt > cap) return;
-  int4 b = bbox[id];
-  int tx0 = b.x / kTile, tx1 = (b.y - 1) / kTile, ty0 = b.z / kTile, ty1 = (b.w - 1) / kTile;
-  for (int ty = ty0; ty <= ty1; ty++)
-    for (int tx = tx0; tx <= tx1; tx++) {
-      pair_tiles[off] = (uint32_t)(ty * tiles_x + tx);
-      pair_ids[off] = id;
-      off++;
+// A warp takes 32 consecutive depth ranks; their pairs occupy one contiguous
+// range of the pair arrays, which the warp writes cooperatively (coalesced).
+// The 8-bit digit histograms of the tile keys for the pair sort are
+// accumulated on the way (shared-memory atomics, one global add per bin).
+constexpr int kDupThreads = 256;
+
+__global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *order, const uint32_t *touched,
+                                                                const int4 *bbox, const uint32_t *offsets,
+                                                                uint32_t n, uint32_t cap, int tiles_x, int passes,
+                                                                uint32_t *pair_tiles, uint32_t *pair_ids,
+                                                                uint32_t *hist) {
+  __shared__ uint32_t s_h[3][kRadix];
+  for (int q = threadIdx.x; q < passes * kRadix; q += kDupThreads) s_h[q / kRadix][q % kRadix] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t r = blockIdx.x * kDupThreads + threadIdx.x;
+  uint32_t id = 0, cnt = 0, off = 0;
+  int tx0 = 0, ty0 = 0, wdt = 1;
+  if (r < n) {
+    id = order[r];
+    cnt = touched[id];
+    off = offsets[r];
+    if (cnt) {
+      const int4 b = bbox[id];
+      tx0 = b.x / kTile;
+      ty0 = b.z / kTile;
+      wdt = (b.y - 1) / kTile - tx0 + 1;
     }
+  }
+  // inclusive prefix of the counts inside the warp (ranks are contiguous)
+  uint32_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+  const uint32_t base = __shfl_sync(0xffffffffu, off - (inc - cnt), 0);  // offset of the warp's first pair
+  const uint32_t excl = inc - cnt;
+  for (uint32_t p0 = 0; p0 < total; p0 += 32) {  // warp-uniform trip count
+    const uint32_t p = p0 + lane;
+    // owner = last lane whose exclusive prefix is <= p
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const uint32_t e = __shfl_sync(0xffffffffu, excl, (lo + step) & 31);
+      if (lo + step < 32 && e <= p) lo += step;
+    }
+    const uint32_t q = p - __shfl_sync(0xffffffffu, excl, lo);
+    const int w_o = __shfl_sync(0xffffffffu, wdt, lo);
+    const int tx = __shfl_sync(0xffffffffu, tx0, lo) + (int)(q % (uint32_t)w_o);
+    const int ty = __shfl_sync(0xffffffffu, ty0, lo) + (int)(q / (uint32_t)w_o);
+    const uint32_t owner_id = __shfl_sync(0xffffffffu, id, lo);
+    const uint32_t pos = base + p;
+    if (p < total && pos < cap) {
+      const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
+      pair_tiles[pos] = tile;
+      pair_ids[pos] = owner_id;
+      for (int ps = 0; ps < passes; ps++) atomicAdd(&s_h[ps][(tile >> (ps * kRadixBits)) & (kRadix - 1)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < passes * kRadix; q += kDupThreads) {
+    const uint32_t v = s_h[q / kRadix][q % kRadix];
+    if (v) atomicAdd(&hist[q], v);
+  }
 }
 
-__global__ void ranges_kernel(const uint32_t *pair_tiles, const uint32_t *counters, uint32_t cap, uint2 *ranges) {
-  uint32_t P = counters[C_NSORT];
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
-    uint32_t t = pair_tiles[i];
-    if (i == 0 || pair_tiles[i - 1] != t) ranges[t].x = i;
-    if (i + 1 == P || pair_tiles[i + 1] != t) ranges[t].y = i + 1;
-  }
-  (void)cap;
+// [start, end) of every tile in the sorted pair keys, by binary search.
+__global__ void ranges_kernel(const uint32_t *pair_tiles, const uint32_t *counters, int tiles, uint2 *ranges) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= tiles) return;
+  const uint32_t P = counters[C_NSORT];
+  auto lower = [&](uint32_t key) {
+    uint32_t lo = 0, hi = P;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (pair_tiles[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  ranges[t] = make_uint2(lower((uint32_t)t), lower((uint32_t)t + 1));
 }
 
 // ------------------------------------------------------------------ orchestration
@@ -369,11 +474,10 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
 
   cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 16 * kRadix, s);
   cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * sc.lookback_words, s);
-  cudaMemsetAsync(ranges, 0, sizeof(uint2) * tiles, s);
   if (n > 0) {
     // depth order: 8 passes (even) -> result back in (dkeys, order)
     radix_sort<uint64_t>(dkeys, order, sc.dkeys_alt, sc.dvals_alt, nullptr, n, n, 8, 0, sc.hist,
-                         sc.offsets, sc.lookback, counters + C_CHUNK0, s);
+                         sc.offsets, sc.lookback, counters + C_CHUNK0, false, s);
     const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
     scan_reduce_kernel<<<nb, kScanThreads, 0, s>>>(order, touched, n, sc.block_sums);
     scan_top_kernel<<<1, 1024, 0, s>>>(sc.block_sums, nb, counters, (uint64_t)cap);
@@ -381,16 +485,17 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
     // pairs land in the buffer that makes the sorted result end in (ptiles, pids)
     uint32_t *dt = (pp & 1) ? sc.ptiles_alt : ptiles;
     uint32_t *di = (pp & 1) ? sc.pids_alt : pids;
-    duplicate_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, touched, reinterpret_cast<const int4 *>(ws + L.bbox),
-                                                    offs, n, (uint32_t)cap, L.tiles_x, dt, di);
+    duplicate_kernel<<<(n + kDupThreads - 1) / kDupThreads, kDupThreads, 0, s>>>(
+        order, touched, reinterpret_cast<const int4 *>(ws + L.bbox), offs, n, (uint32_t)cap, L.tiles_x, pp, dt, di,
+        sc.hist + 8 * kRadix);
     if (cap > 0) {
       uint32_t *ka = (pp & 1) ? sc.ptiles_alt : ptiles, *va = (pp & 1) ? sc.pids_alt : pids;
       uint32_t *kb = (pp & 1) ? ptiles : sc.ptiles_alt, *vb = (pp & 1) ? pids : sc.pids_alt;
       radix_sort<uint32_t>(ka, va, kb, vb, counters + C_NSORT, 0, (uint32_t)cap, pp, 0, sc.hist + 8 * kRadix,
                            sc.offsets + 8 * kRadix, sc.lookback + 8 * ((n + kSortChunk - 1) / kSortChunk) * kRadix,
-                           counters + C_CHUNK0 + 8, s);
-      ranges_kernel<<<148 * 4, 256, 0, s>>>(ptiles, counters, (uint32_t)cap, ranges);
+                           counters + C_CHUNK0 + 8, true, s);
     }
+    ranges_kernel<<<(tiles + 255) / 256, 256, 0, s>>>(ptiles, counters, tiles, ranges);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
