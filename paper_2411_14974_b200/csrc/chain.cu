@@ -39,11 +39,11 @@ template <int MAXK> __host__ __device__ constexpr int chain_threads() { return M
 // SH colour VJP (harmonics.py:112-128): d_sh += Y (x) d_eff and the
 // direction gradient dY/ddir^T (sh . d_eff), with eval_sh_basis_grad
 // (harmonics.py:62-98) written out per basis function.
-__device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const float *sh, const float *d_color,
-                                       float *d_sh, float *ddir) {
+__device__ __forceinline__ void sh_vjp(double x, double y, double z, int deg, const float *sh, const float *d_color,
+                                       float *d_sh, double *ddir) {
   float Y[kShCoeffs];
   Y[0] = kC0;
-  const float xx = x * x, yy = y * y, zz = z * z;
+  const double xx = x * x, yy = y * y, zz = z * z;
   if (deg >= 1) { Y[1] = -kC1 * y; Y[2] = kC1 * z; Y[3] = -kC1 * x; }
   if (deg >= 2) {
     Y[4] = kC20 * x * y; Y[5] = kC21 * y * z; Y[6] = kC22 * (2.f * zz - xx - yy);
@@ -64,19 +64,19 @@ __device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const
       if (b < nb) raw = fmaf(Y[b], sh[3 * b + c], raw);
     deff[c] = (0.5f + raw) > 0.f ? d_color[c] : 0.f;
   }
-  float v[kShCoeffs];
+  double v[kShCoeffs];
 #pragma unroll
   for (int b = 0; b < kShCoeffs; b++) {
-    v[b] = 0.f;
+    v[b] = 0.0;
     if (b < nb) {
 #pragma unroll
       for (int c = 0; c < 3; c++) {
         d_sh[3 * b + c] += Y[b] * deff[c];
-        v[b] = fmaf(sh[3 * b + c], deff[c], v[b]);
+        v[b] = fma((double)sh[3 * b + c], (double)deff[c], v[b]);
       }
     }
   }
-  float gx = 0.f, gy = 0.f, gz = 0.f;
+  double gx = 0.0, gy = 0.0, gz = 0.0;
   if (deg >= 1) { gy -= kC1 * v[1]; gz += kC1 * v[2]; gx -= kC1 * v[3]; }
   if (deg >= 2) {
     gx += kC20 * y * v[4]; gy += kC20 * x * v[4];
@@ -203,8 +203,8 @@ __global__ void __launch_bounds__(chain_threads<MAXK>()) chain_kernel(ChainArgs 
     const float4 d = dshv[q];
     dsh[4 * q] = d.x; dsh[4 * q + 1] = d.y; dsh[4 * q + 2] = d.z; dsh[4 * q + 3] = d.w;
   }
-  float ddirf[3];
-  sh_vjp((float)dir[0], (float)dir[1], (float)dir[2], a.sh_degree, shf, acc + A_DC, dsh, ddirf);
+  double ddirf[3];
+  sh_vjp(dir[0], dir[1], dir[2], a.sh_degree, shf, acc + A_DC, dsh, ddirf);
 #pragma unroll
   for (int q = 0; q < kShCoeffs * 3 / 4; q++)
     dshv[q] = make_float4(dsh[4 * q], dsh[4 * q + 1], dsh[4 * q + 2], dsh[4 * q + 3]);

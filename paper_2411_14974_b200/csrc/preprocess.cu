@@ -280,10 +280,54 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
 #undef GY
 }
 
-// One convex.  pts_s: this convex's K points staged in smem; X, Y: this
-// thread's projected-pixel slots in smem (stride kPreThreads).
+// SH colour in float32 (harmonics.py:33-59, 101-109): continuous output,
+// checked at 1e-4, so it needs no float64.  sh: 16x3 floats in smem.
+__device__ __forceinline__ void sh_colour(float x, float y, float z, int deg, const float *sh, float *col) {
+  float b[kShCoeffs];
+  b[0] = 0.28209479177387814f;
+  const float c1 = 0.4886025119029199f;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  if (deg >= 1) { b[1] = -c1 * y; b[2] = c1 * z; b[3] = -c1 * x; }
+  if (deg >= 2) {
+    b[4] = 1.0925484305920792f * x * y;
+    b[5] = -1.0925484305920792f * y * z;
+    b[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+    b[7] = -1.0925484305920792f * x * z;
+    b[8] = 0.5462742152960396f * (xx - yy);
+  }
+  if (deg >= 3) {
+    b[9] = -0.5900435899266435f * y * (3.f * xx - yy);
+    b[10] = 2.890611442640554f * x * y * z;
+    b[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+    b[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+    b[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
+    b[14] = 1.445305721320277f * z * (xx - yy);
+    b[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
+  }
+  const int nb = (deg + 1) * (deg + 1);
+  float acc[3] = {0.f, 0.f, 0.f};
+  const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
+#pragma unroll
+  for (int q = 0; q < kShCoeffs * 3 / 4; q++) {  // 4 coefficients of 3 channels = 3 float4
+    if (4 * q < 3 * nb) {
+      const float4 v = sh4[q];
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const int f = 4 * q + r, qb = f / 3, c = f % 3;
+        if (qb < nb) acc[c] = fmaf(b[qb], e[r], acc[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; c++) col[c] = fmaxf(0.5f + acc[c], 0.f);
+}
+
+// One convex.  pts_s / sh_s: this convex's rows staged in smem by TMA;
+// X, Y: this thread's projected-pixel slots in smem (stride kPreThreads).
 template <int MAXK>
-__device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, double *X, double *Y) {
+__device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, const float *sh_s,
+                                               uint64_t *sh_bar, double *X, double *Y) {
   const int k = a.k;
   a.touched[i] = 0u;
   a.depth_keys[i] = kCulledKey;
@@ -318,19 +362,18 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
   const int h = graham_scan_packed(k, X, Y, kPreThreads, hull);
   if (h == 0) return false;
   // projection.py:116-128 (static register slots, j < h)
-  double nx[MAXK], ny[MAXK], off[MAXK], vx[MAXK], vy[MAXK];
+  double nx[MAXK], ny[MAXK], off[MAXK];
 #pragma unroll
   for (int j = 0; j < MAXK; j++) {
     if (j < h) {
       const int u = hull.get(j), v = hull.get(j + 1 < h ? j + 1 : 0);
-      vx[j] = X[u * kPreThreads];
-      vy[j] = Y[u * kPreThreads];
-      const double ex = X[v * kPreThreads] - vx[j], ey = Y[v * kPreThreads] - vy[j];
+      const double ux = X[u * kPreThreads], uy = Y[u * kPreThreads];
+      const double ex = X[v * kPreThreads] - ux, ey = Y[v * kPreThreads] - uy;
       const double rx = ey, ry = -ex;
       const double len = sqrt(rx * rx + ry * ry);
       nx[j] = rx / len;
       ny[j] = ry / len;
-      off[j] = -(nx[j] * vx[j] + ny[j] * vy[j]);
+      off[j] = -(nx[j] * ux + ny[j] * uy);
     }
   }
   // rasterize.py:99-103
@@ -338,8 +381,8 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
   const double s = depth_scale(a.mode, a.cam.ortho ? 1.0 : depth);
   const double delta_s = s * exp((double)a.raw_delta[i]);
   const double sigma_s = s * exp((double)a.raw_sigma[i]);
-  const double ro = (double)a.raw_opacity[i];
-  const double o = 1.0 / (1.0 + exp(-ro));
+  const float ro = a.raw_opacity[i];
+  const double o = 1.0 / (1.0 + exp(-(double)ro));
   // projection.py:136-177
   if (o <= a.cutoff) return false;
   int x0, x1, y0, y1;
@@ -357,10 +400,11 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
 #pragma unroll
     for (int j = 0; j < MAXK; j++) {
       if (j < h) {
+        const int u = hull.get(j);
         double den = 1.0 + (pnx * nx[j] + pny * ny[j]);
         if (!(den >= 1e-12)) den = 1e-12;
-        const double ix = vx[j] + (margin * (pnx + nx[j])) / den;
-        const double iy = vy[j] + (margin * (pny + ny[j])) / den;
+        const double ix = X[u * kPreThreads] + (margin * (pnx + nx[j])) / den;
+        const double iy = Y[u * kPreThreads] + (margin * (pny + ny[j])) / den;
         xmin = fmin(xmin, ix); xmax = fmax(xmax, ix);
         ymin = fmin(ymin, iy); ymax = fmax(ymax, iy);
         pnx = nx[j];
@@ -374,33 +418,7 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
     if (!(fx0 < fx1) || !(fy0 < fy1)) return false;
     x0 = (int)fx0; x1 = (int)fx1; y0 = (int)fy0; y1 = (int)fy1;
   }
-  // rasterize.py:110-114 view direction; harmonics.py:101-109 colour
-  const double dvx = cx / k - a.cam_center[0], dvy = cy / k - a.cam_center[1], dvz = cz / k - a.cam_center[2];
-  const double dist = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
-  double dx = 0.0, dy = 0.0, dz = 1.0;
-  if (dist > 0.0) { dx = dvx / dist; dy = dvy / dist; dz = dvz / dist; }
-  double basis[kShCoeffs];
-  sh_basis(dx, dy, dz, a.sh_degree, basis);
-  const float4 *shv = reinterpret_cast<const float4 *>(a.sh + i * kShCoeffs * 3);
-  float shf[kShCoeffs * 3];
-#pragma unroll
-  for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
-    const float4 t = __ldg(shv + q);
-    shf[4 * q] = t.x; shf[4 * q + 1] = t.y; shf[4 * q + 2] = t.z; shf[4 * q + 3] = t.w;
-  }
-  const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
-  double col[3];
-#pragma unroll
-  for (int c = 0; c < 3; c++) {
-    double acc = 0.0;
-#pragma unroll
-    for (int b = 0; b < kShCoeffs; b++)
-      if (b < nb) acc += basis[b] * (double)shf[3 * b + c];
-    const double raw = 0.5 + acc;
-    col[c] = raw > 0.0 ? raw : 0.0;
-  }
-
-  // ---- outputs ----
+  // ---- outputs: discrete state, then the float32 blend record ----
   uint8_t hb[MAXK];
 #pragma unroll
   for (int j = 0; j < MAXK; j++) hb[j] = (uint8_t)(j < h ? hull.get(j) : 0xff);
@@ -417,60 +435,81 @@ __device__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, 
   a.depth_keys[i] = orderable_bits(depth);
 
   constexpr int RF = Rec<MAXK>::kFloats;
-  float rec[RF];
+  float4 *dst = reinterpret_cast<float4 *>(a.records + i * RF);
   const int ax = (x0 + x1) >> 1, ay = (y0 + y1) >> 1;
   const double dls = delta_s * 1.4426950408889634;  // delta_s * log2(e)
-  rec[R_AX] = (float)ax;
-  rec[R_AY] = (float)ay;
-  rec[R_SIGMA] = (float)sigma_s;
-  rec[R_OPACITY] = (float)o;
-  rec[R_R] = (float)col[0];
-  rec[R_G] = (float)col[1];
-  rec[R_B] = (float)col[2];
-  rec[R_DEPTH] = (float)depth;
-  rec[R_ONE_MINUS_O] = (float)(1.0 / (1.0 + exp(ro)));
-  rec[R_DLS] = (float)dls;
-  rec[R_NLINES] = __int_as_float(h);
-  rec[R_BBX] = __int_as_float(x0 | (x1 << 16));
-  rec[R_BBY] = __int_as_float(y0 | (y1 << 16));
 #pragma unroll
-  for (int f = 13; f < R_HEADER; f++) rec[f] = 0.f;
+  for (int q = 0; q < 3 * MAXK / 4; q++) {  // line coefficients, anchor-relative offset in fp64
+    float e[4];
 #pragma unroll
-  for (int j = 0; j < MAXK; j++) {
-    if (j < h) {
-      const double c = off[j] + nx[j] * ax + ny[j] * ay;  // anchor-relative offset, fp64
-      rec[R_HEADER + 3 * j] = (float)(dls * nx[j]);
-      rec[R_HEADER + 3 * j + 1] = (float)(dls * ny[j]);
-      rec[R_HEADER + 3 * j + 2] = (float)(dls * c);
-    } else {
-      rec[R_HEADER + 3 * j] = 0.f;
-      rec[R_HEADER + 3 * j + 1] = 0.f;
-      rec[R_HEADER + 3 * j + 2] = -INFINITY;
+    for (int r = 0; r < 4; r++) {
+      const int f = 4 * q + r, j = f / 3, c = f % 3;
+      if (j < h) {
+        e[r] = c == 0 ? (float)(dls * nx[j]) : c == 1 ? (float)(dls * ny[j])
+                                                      : (float)(dls * (off[j] + nx[j] * ax + ny[j] * ay));
+      } else {
+        e[r] = c == 2 ? -INFINITY : 0.f;
+      }
     }
+    dst[R_HEADER / 4 + q] = make_float4(e[0], e[1], e[2], e[3]);
   }
-  float4 *dst = reinterpret_cast<float4 *>(a.records + i * RF);
-#pragma unroll
-  for (int q = 0; q < RF / 4; q++) dst[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
+  // rasterize.py:110-114 view direction; harmonics.py:101-109 colour
+  const double dvx = cx / k - a.cam_center[0], dvy = cy / k - a.cam_center[1], dvz = cz / k - a.cam_center[2];
+  const double dist = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
+  float dx = 0.f, dy = 0.f, dz = 1.f;
+  if (dist > 0.0) { dx = (float)(dvx / dist); dy = (float)(dvy / dist); dz = (float)(dvz / dist); }
+  mbar_wait(sh_bar, 0);  // SH rows landed (TMA issued at kernel start)
+  float col[3];
+  sh_colour(dx, dy, dz, a.sh_degree, sh_s, col);
+  dst[0] = make_float4((float)ax, (float)ay, (float)sigma_s, (float)o);
+  dst[1] = make_float4(col[0], col[1], col[2], (float)depth);
+  dst[2] = make_float4(1.f / (1.f + __expf(ro)), (float)dls, __int_as_float(h), __int_as_float(x0 | (x1 << 16)));
+  dst[3] = make_float4(__int_as_float(y0 | (y1 << 16)), 0.f, 0.f, 0.f);
   return true;
 }
 
 template <int MAXK>
-__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreArgs a) {
-  extern __shared__ double pre_smem[];  // X[MAXK][threads], Y[MAXK][threads], points[threads][k*3]
+__global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(PreArgs a) {
+  // dynamic smem: X[MAXK][threads], Y[MAXK][threads] (f64), SH[threads][48], points[threads][k*3] (f32)
+  extern __shared__ __align__(16) double pre_smem[];
+  __shared__ __align__(8) uint64_t bars[2];
   double *Xs = pre_smem, *Ys = pre_smem + MAXK * kPreThreads;
-  float *pts_smem = reinterpret_cast<float *>(pre_smem + 2 * MAXK * kPreThreads);
+  float *sh_smem = reinterpret_cast<float *>(pre_smem + 2 * MAXK * kPreThreads);
+  float *pts_smem = sh_smem + kPreThreads * kShCoeffs * 3;
   const int64_t base = (int64_t)blockIdx.x * kPreThreads;
   const int rowf = a.k * 3;
   const int64_t nblk = min((int64_t)kPreThreads, a.n - base);
-  // coalesced staging of this block's points
-  const float *src = a.points + base * rowf;
-  for (int q = threadIdx.x; q < nblk * rowf; q += kPreThreads) pts_smem[q] = src[q];
+  const bool full = nblk == kPreThreads;  // full blocks: 16B-aligned, in-bounds bulk copies
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
+  if (full) {
+    if (threadIdx.x == 0) {
+      const uint32_t pbytes = kPreThreads * rowf * 4, sbytes = kPreThreads * kShCoeffs * 3 * 4;
+      mbar_expect_tx(&bars[0], pbytes);
+      tma_bulk_g2s(pts_smem, a.points + base * rowf, pbytes, &bars[0]);
+      mbar_expect_tx(&bars[1], sbytes);
+      tma_bulk_g2s(sh_smem, a.sh + base * kShCoeffs * 3, sbytes, &bars[1]);
+    }
+    mbar_wait(&bars[0], 0);
+  } else {  // tail block: plain coalesced loads
+    for (int q = threadIdx.x; q < nblk * rowf; q += kPreThreads) pts_smem[q] = a.points[base * rowf + q];
+    for (int q = threadIdx.x; q < nblk * kShCoeffs * 3; q += kPreThreads)
+      sh_smem[q] = a.sh[base * kShCoeffs * 3 + q];
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[1])) : "memory");
+  }
   const int64_t i = base + threadIdx.x;
   bool vis = false;
-  if (i < a.n) vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, Xs + threadIdx.x, Ys + threadIdx.x);
+  if (i < a.n)
+    vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, sh_smem + threadIdx.x * kShCoeffs * 3, &bars[1],
+                               Xs + threadIdx.x, Ys + threadIdx.x);
   unsigned b = __ballot_sync(0xffffffffu, vis);
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(&a.counters[C_NVISIBLE], (unsigned)__popc(b));
+  if (threadIdx.x == 0) mbar_wait(&bars[1], 0);  // never leave while a bulk copy still targets this smem
 }
 
 // cs_graham_scan_batch: one thread per point set.
@@ -526,8 +565,9 @@ int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_par
   a.counters = reinterpret_cast<uint32_t *>(ws + L.counters);
   camera_center(cam, a.cam_center);
   const int blocks = (int)((p.n + kPreThreads - 1) / kPreThreads);
-  const size_t smem = (size_t)kPreThreads * (2 * L.max_k * sizeof(double) + p.k * 3 * sizeof(float));
+  const size_t smem = (size_t)kPreThreads * (2 * L.max_k * sizeof(double) + (kShCoeffs * 3 + p.k * 3) * sizeof(float));
   if (L.max_k == 8) {
+    cudaFuncSetAttribute(preprocess_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     preprocess_kernel<8><<<blocks, kPreThreads, smem, s>>>(a);
   } else {
     cudaFuncSetAttribute(preprocess_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -383,11 +383,18 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *
     const int ty = __shfl_sync(0xffffffffu, ty0, lo) + (int)(q / (uint32_t)w_o);
     const uint32_t owner_id = __shfl_sync(0xffffffffu, id, lo);
     const uint32_t pos = base + p;
-    if (p < total && pos < cap) {
-      const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
+    const bool ok = p < total && pos < cap;
+    const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
+    if (ok) {
       pair_tiles[pos] = tile;
       pair_ids[pos] = owner_id;
-      for (int ps = 0; ps < passes; ps++) atomicAdd(&s_h[ps][(tile >> (ps * kRadixBits)) & (kRadix - 1)], 1u);
+    }
+    // digit histograms: neighbouring pairs share tiles, so aggregate equal
+    // digits across the warp before the shared-memory atomic
+    for (int ps = 0; ps < passes; ps++) {
+      const uint32_t dg = ok ? (tile >> (ps * kRadixBits)) & (kRadix - 1) : kRadix;
+      const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+      if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_h[ps][dg], (uint32_t)__popc(peers));
     }
   }
   __syncthreads();
