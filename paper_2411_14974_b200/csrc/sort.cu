@@ -176,14 +176,27 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a
   s_dexcl[d] = block_exclusive_scan256(sum, s_warp);
   uint32_t excl = 0;
   if (chunk > 0) {
+    // windowed decoupled look-back: kLookback independent loads per round, so
+    // the walk over not-yet-resolved predecessors costs one L2 round trip per
+    // kLookback chunks instead of one per chunk
+    constexpr int kLookback = 16;
     int c = (int)chunk - 1;
-    while (true) {
-      const uint32_t v = lb[c * kRadix + d];
-      const uint32_t flag = v & ~kValueMask;
-      if (flag == 0) continue;
-      excl += v & kValueMask;
-      if (flag == kFlagPrefix) break;
-      c--;
+    bool done = false;
+    while (!done) {
+      uint32_t v[kLookback];
+#pragma unroll
+      for (int q = 0; q < kLookback; q++) v[q] = c - q >= 0 ? lb[(c - q) * kRadix + d] : kFlagPrefix;
+      int used = 0;
+#pragma unroll
+      for (int q = 0; q < kLookback; q++) {
+        if (done || used < q) continue;              // stopped earlier in this window
+        const uint32_t flag = v[q] & ~kValueMask;
+        if (flag == 0) continue;                     // not published yet: re-read from here
+        excl += v[q] & kValueMask;
+        used = q + 1;
+        done = flag == kFlagPrefix;
+      }
+      c -= used;
     }
     lb[chunk * kRadix + d] = kFlagPrefix | (excl + sum);
   }
@@ -358,6 +371,25 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *
       wdt = (b.y - 1) / kTile - tx0 + 1;
     }
   }
+  // digit histograms of this convex's tile keys: digit 0 per tile, higher
+  // digits per row segment (a row of tiles rarely crosses a 256 boundary)
+  if (cnt && (uint64_t)off + cnt <= cap) {
+    const int4 b = bbox[id];
+    const int ty1 = (b.w - 1) / kTile;
+    for (int ty = ty0; ty <= ty1; ty++) {
+      const uint32_t t0 = (uint32_t)(ty * tiles_x + tx0), t1 = t0 + (uint32_t)wdt - 1;
+      for (uint32_t t = t0; t <= t1; t++) atomicAdd(&s_h[0][t & (kRadix - 1)], 1u);
+      for (int ps = 1; ps < passes; ps++) {
+        const int sh = ps * kRadixBits;
+        uint32_t seg = t0;
+        while (seg <= t1) {
+          const uint32_t blk_end = min(t1, ((seg >> sh) + 1) * (1u << sh) - 1);
+          atomicAdd(&s_h[ps][(seg >> sh) & (kRadix - 1)], blk_end - seg + 1);
+          seg = blk_end + 1;
+        }
+      }
+    }
+  }
   // inclusive prefix of the counts inside the warp (ranks are contiguous)
   uint32_t inc = cnt;
 #pragma unroll
@@ -388,13 +420,6 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *
     if (ok) {
       pair_tiles[pos] = tile;
       pair_ids[pos] = owner_id;
-    }
-    // digit histograms: neighbouring pairs share tiles, so aggregate equal
-    // digits across the warp before the shared-memory atomic
-    for (int ps = 0; ps < passes; ps++) {
-      const uint32_t dg = ok ? (tile >> (ps * kRadixBits)) & (kRadix - 1) : kRadix;
-      const uint32_t peers = __match_any_sync(0xffffffffu, dg);
-      if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_h[ps][dg], (uint32_t)__popc(peers));
     }
   }
   __syncthreads();
