@@ -22,8 +22,7 @@
 
 namespace cs {
 
-constexpr int kBlendThreads = 256;
-constexpr int kBatch = 128;
+constexpr int kBlendThreads = 256;  // 8 warps; warp w owns the 8x4 pixel block of tile_pixel()
 
 struct BlendArgs {
   const float *records;
@@ -45,34 +44,43 @@ struct BlendArgs {
   unsigned long long *stats;
 };
 
-template <int MAXK>
-__device__ __forceinline__ void stage_batch(const BlendArgs &a, uint32_t start, int nb, float4 *s_rec,
-                                            uint32_t *s_id) {
-  constexpr int Q = Rec<MAXK>::kFloats / 4;
-  if (threadIdx.x < nb) s_id[threadIdx.x] = a.pair_ids[start + threadIdx.x];
-  __syncthreads();
-  const float4 *src = reinterpret_cast<const float4 *>(a.records);
-  for (int q = threadIdx.x; q < nb * Q; q += kBlendThreads) {
-    int r = q / Q, part = q - r * Q;
-    s_rec[q] = __ldg(src + (size_t)s_id[r] * Q + part);
-  }
-  __syncthreads();
-}
-
 struct Eval {
   float I, J, alpha, alpha_raw, phi2, m, s;
 };
 
-// field value of record `rec` at anchor-relative pixel (dx, dy); keeps the
-// per-line z2 in z[] for the backward.
+// Candidate record held in registers (loaded with warp-broadcast 128-bit
+// loads: every lane reads the same address, one request per load).
 template <int MAXK>
-__device__ __forceinline__ Eval eval_field(const float *rec, int nl, float dx, float dy, float *z) {
+struct RecRegs {
+  float4 h0, h1, h2;            // ax ay sigma o | r g b depth | 1-o dls nl -
+  float ln[3 * MAXK];           // A_j B_j C_j
+  __device__ __forceinline__ void load(const float *records, uint32_t id) {
+    const float4 *r = reinterpret_cast<const float4 *>(records + (size_t)id * Rec<MAXK>::kFloats);
+    h0 = __ldg(r);
+    h1 = __ldg(r + 1);
+    h2 = __ldg(r + 2);
+#pragma unroll
+    for (int q = 0; q < 3 * MAXK / 4; q++) {
+      const float4 v = __ldg(r + R_HEADER / 4 + q);
+      ln[4 * q] = v.x; ln[4 * q + 1] = v.y; ln[4 * q + 2] = v.z; ln[4 * q + 3] = v.w;
+    }
+  }
+  __device__ __forceinline__ int nl() const { return __float_as_int(h2.z); }
+};
+
+// smooth field of a candidate at anchor-relative pixel (dx, dy):
+// z2_j = A_j dx + B_j dy + C_j, phi2 = max z2 + log2 sum 2^(z2 - max),
+// I = 1 / (1 + 2^(sigma_s phi2)), alpha = min(o I, ALPHA_MAX)
+// (field.py:51-72, rasterize.py:147-153 in log2 units).
+template <int MAXK>
+__device__ __forceinline__ Eval eval_field(const RecRegs<MAXK> &r, float dx, float dy, float *z) {
   Eval e;
+  const int nl = r.nl();
   float m = -INFINITY;
 #pragma unroll
   for (int l = 0; l < MAXK; l++) {
     if (l < nl) {
-      z[l] = fmaf(rec[R_HEADER + 3 * l], dx, fmaf(rec[R_HEADER + 3 * l + 1], dy, rec[R_HEADER + 3 * l + 2]));
+      z[l] = fmaf(r.ln[3 * l], dx, fmaf(r.ln[3 * l + 1], dy, r.ln[3 * l + 2]));
       m = fmaxf(m, z[l]);
     }
   }
@@ -81,12 +89,12 @@ __device__ __forceinline__ Eval eval_field(const float *rec, int nl, float dx, f
   for (int l = 0; l < MAXK; l++)
     if (l < nl) s += ex2(z[l] - m);
   const float phi2 = m + lg2(s);
-  const float u = ex2(rec[R_SIGMA] * phi2);
+  const float u = ex2(r.h0.z * phi2);
   e.I = rcp(1.f + u);
   // 1 - I without cancellation: u*I while I >= 1/2, else 1 - I (also covers
   // u so large that I flushes to zero)
   e.J = u > 1.f ? 1.f - e.I : u * e.I;
-  e.alpha_raw = rec[R_OPACITY] * e.I;
+  e.alpha_raw = r.h0.w * e.I;
   e.alpha = fminf(e.alpha_raw, (float)kAlphaMaxD);
   e.phi2 = phi2;
   e.m = m;
@@ -94,23 +102,33 @@ __device__ __forceinline__ Eval eval_field(const float *rec, int nl, float dx, f
   return e;
 }
 
-__device__ __forceinline__ bool in_bbox(const float *rec, int px, int py) {
-  uint32_t bx = __float_as_uint(rec[R_BBX]), by = __float_as_uint(rec[R_BBY]);
+__device__ __forceinline__ bool in_box(uint32_t bx, uint32_t by, int px, int py) {
   return px >= (int)(bx & 0xffffu) && px < (int)(bx >> 16) && py >= (int)(by & 0xffffu) && py < (int)(by >> 16);
 }
 
+// Does the bbox of candidate id overlap the warp's 8x4 pixel block?
+__device__ __forceinline__ uint2 load_bbox(const float *records, uint32_t id, int rf) {
+  return __ldg(reinterpret_cast<const uint2 *>(records + (size_t)id * rf + R_BBX));
+}
+__device__ __forceinline__ bool box_overlaps(uint2 b, int rx0, int ry0) {
+  return (int)(b.x & 0xffffu) < rx0 + 8 && (int)(b.x >> 16) > rx0 && (int)(b.y & 0xffffu) < ry0 + 4 &&
+         (int)(b.y >> 16) > ry0;
+}
+
+// Forward blend, one tile per block; every warp walks the tile's candidate
+// list on its own (no block barriers): 32 candidates at a time are culled by
+// a ballot against the warp's 8x4 pixel block, survivors are evaluated
+// per pixel, and the warp leaves once all 32 of its pixels are done.
 template <int MAXK>
-__global__ void __launch_bounds__(kBlendThreads) forward_kernel(BlendArgs a) {
-  constexpr int Q = Rec<MAXK>::kFloats / 4;
+__global__ void __launch_bounds__(kBlendThreads, 4) forward_kernel(BlendArgs a) {
   constexpr int RF = Rec<MAXK>::kFloats;
-  __shared__ float4 s_rec[kBatch * Q];
-  __shared__ uint32_t s_id[kBatch];
-  __shared__ int s_vis[kBatch];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int lx, ly;
   tile_pixel(threadIdx.x, lx, ly);
   const int px = tx * kTile + lx, py = ty * kTile + ly;
+  const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2);
   const bool inside = px < a.width && py < a.height;
   const uint2 range = a.ranges[tile];
   const float qx = px + 0.5f, qy = py + 0.5f;
@@ -120,33 +138,45 @@ __global__ void __launch_bounds__(kBlendThreads) forward_kernel(BlendArgs a) {
   bool done = !inside;
   const bool use_floor = a.floor > 0.f;
   float z[MAXK];
-  for (uint32_t start = range.x; start < range.y; start += kBatch) {
-    if (__syncthreads_count(!done) == 0) break;
-    const int nb = min((uint32_t)kBatch, range.y - start);
-    if (threadIdx.x < kBatch) s_vis[threadIdx.x] = 0;
-    stage_batch<MAXK>(a, start, nb, s_rec, s_id);
-    for (int j = 0; j < nb && !done; j++) {
-      const float *rec = reinterpret_cast<const float *>(s_rec) + j * RF;
-      if (!in_bbox(rec, px, py)) continue;
-      const int nl = __float_as_int(rec[R_NLINES]);
-      const Eval e = eval_field<MAXK>(rec, nl, qx - rec[R_AX], qy - rec[R_AY], z);
-      n_eval++;
-      n_lines += nl;
-      if (!(e.alpha >= a.cutoff)) continue;
-      const float w = T * e.alpha;
-      C0 = fmaf(w, rec[R_R], C0);
-      C1 = fmaf(w, rec[R_G], C1);
-      C2 = fmaf(w, rec[R_B], C2);
-      Wsum += w;
-      D = fmaf(w, rec[R_DEPTH], D);
-      T *= fmaxf(fmaf(rec[R_OPACITY], e.J, rec[R_ONE_MINUS_O]), 1e-6f);
-      cnt++;
-      last = (int)(start + j);
-      s_vis[j] = 1;
-      if (use_floor && T < a.floor) done = true;
+  RecRegs<MAXK> r;
+  for (uint32_t base = range.x; base < range.y; base += 32) {
+    if (__all_sync(0xffffffffu, done)) break;
+    const uint32_t idx = base + lane;
+    uint32_t id = 0;
+    bool hit = false;
+    if (idx < range.y) {
+      id = __ldg(a.pair_ids + idx);
+      hit = box_overlaps(load_bbox(a.records, id, RF), rx0, ry0);
     }
-    __syncthreads();
-    if (a.visible && threadIdx.x < nb && s_vis[threadIdx.x]) a.visible[s_id[threadIdx.x]] = 1;
+    uint32_t mask = __ballot_sync(0xffffffffu, hit);
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint32_t cid = __shfl_sync(0xffffffffu, id, j);
+      r.load(a.records, cid);
+      const uint2 bb = load_bbox(a.records, cid, RF);
+      bool blended = false;
+      if (!done && in_box(bb.x, bb.y, px, py)) {
+        const Eval e = eval_field<MAXK>(r, qx - r.h0.x, qy - r.h0.y, z);
+        n_eval++;
+        n_lines += r.nl();
+        if (e.alpha >= a.cutoff) {
+          const float w = T * e.alpha;
+          C0 = fmaf(w, r.h1.x, C0);
+          C1 = fmaf(w, r.h1.y, C1);
+          C2 = fmaf(w, r.h1.z, C2);
+          Wsum += w;
+          D = fmaf(w, r.h1.w, D);
+          T *= fmaxf(fmaf(r.h0.w, e.J, r.h2.x), 1e-6f);
+          cnt++;
+          last = (int)(base + j);
+          blended = true;
+          if (use_floor && T < a.floor) done = true;
+        }
+      }
+      if (__any_sync(0xffffffffu, blended) && lane == 0 && a.visible) a.visible[cid] = 1;
+      if (__all_sync(0xffffffffu, done)) break;
+    }
   }
   block_add_u64(a.stats + S_FWD_EVALS, n_eval);
   block_add_u64(a.stats + S_FWD_LINES, n_lines);
@@ -183,22 +213,25 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
   return v[0];
 }
 
+// Backward blend (backward.py:110-205): every warp walks the tile list back
+// to front from the largest `last` of its pixels, culls 32 candidates at a
+// time by ballot, reconstructs T_prev = T / (1 - alpha) per pixel and
+// reduces the 32 screen-space gradient values of each candidate across the
+// warp (transpose-reduce) into one vector of float atomics.
 template <int MAXK>
 __global__ void __launch_bounds__(kBlendThreads) backward_kernel(BlendArgs a) {
-  constexpr int Q = Rec<MAXK>::kFloats / 4;
   constexpr int RF = Rec<MAXK>::kFloats;
   constexpr int AF = Acc<MAXK>::kFloats;
   constexpr int NG = (AF + 31) / 32;  // 32-value groups
-  __shared__ float4 s_rec[kBatch * Q];
-  __shared__ uint32_t s_id[kBatch];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int lx, ly;
   tile_pixel(threadIdx.x, lx, ly);
   const int px = tx * kTile + lx, py = ty * kTile + ly;
+  const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2);
   const bool inside = px < a.width && py < a.height;
   const uint2 range = a.ranges[tile];
-  if (range.y <= range.x) return;
   const float qx = px + 0.5f, qy = py + 0.5f;
   unsigned n_eval = 0, n_lines = 0;
   float T = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
@@ -215,75 +248,88 @@ __global__ void __launch_bounds__(kBlendThreads) backward_kernel(BlendArgs a) {
     S1 = T * a.bg[1];
     S2 = T * a.bg[2];
   }
-  const int lane = threadIdx.x & 31;
+  // nothing behind the warp's last blended candidate matters
+  const int warp_last = __reduce_max_sync(0xffffffffu, last);
   float z[MAXK];
-  for (int64_t end = range.y; end > (int64_t)range.x; end -= kBatch) {
-    const uint32_t start = (uint32_t)max((int64_t)range.x, end - kBatch);
-    if (__syncthreads_count(last >= (int)start) == 0) continue;
-    const int nb = (int)(end - start);
-    stage_batch<MAXK>(a, start, nb, s_rec, s_id);
-    for (int j = nb - 1; j >= 0; j--) {
-      const float *rec = reinterpret_cast<const float *>(s_rec) + j * RF;
-      const int nl = __float_as_int(rec[R_NLINES]);
-      bool contrib = (int)(start + j) <= last && in_bbox(rec, px, py);
-      float v[NG * 32];
-#pragma unroll
-      for (int f = 0; f < NG * 32; f++) v[f] = 0.f;
-      if (contrib) {
-        const float dx = qx - rec[R_AX], dy = qy - rec[R_AY];
-        const Eval e = eval_field<MAXK>(rec, nl, dx, dy, z);
-        n_eval++;
-        n_lines += nl;
-        contrib = e.alpha >= a.cutoff;
-        if (contrib) {
-          const float o = rec[R_OPACITY], sig = rec[R_SIGMA], dls = rec[R_DLS];
-          const float om = fmaxf(fmaf(o, e.J, rec[R_ONE_MINUS_O]), 1e-6f);
-          const float rom = 1.f / om;
-          const float Tp = T * rom;
-          const float w = Tp * e.alpha;
-          const float c0 = rec[R_R], c1 = rec[R_G], c2 = rec[R_B];
-          v[A_DC] = g0 * w;
-          v[A_DC + 1] = g1 * w;
-          v[A_DC + 2] = g2 * w;
-          float dA = g0 * (Tp * c0 - S0 * rom) + g1 * (Tp * c1 - S1 * rom) + g2 * (Tp * c2 - S2 * rom);
-          if (!(e.alpha_raw < (float)kAlphaMaxD)) dA = 0.f;
-          v[A_DOEFF] = dA * e.I;
-          const float dI = dA * o;
-          const float slope = e.I * e.J;
-          const float dphi = -sig * slope * dI;         // d loss / d phi (natural units)
-          v[A_DSIG] = -(e.phi2 * kLn2) * slope * dI;
-          const float rs = 1.f / e.s;
-          float wz = 0.f;
-#pragma unroll
-          for (int l = 0; l < MAXK; l++) {
-            if (l < nl) {
-              const float wl = ex2(z[l] - e.m) * rs;    // softmax_over_lines (field.py:62-67)
-              wz = fmaf(wl, z[l], wz);
-              const float dL = dphi * (dls * kLn2) * wl;  // dphi * delta_s * w_l
-              v[A_LINES + 3 * l] = dL * dx;
-              v[A_LINES + 3 * l + 1] = dL * dy;
-              v[A_LINES + 3 * l + 2] = dL;
-            }
-          }
-          v[A_DDEL] = dphi * wz / dls;                   // dphi * sum_l w_l L_l
-          S0 = fmaf(w, c0, S0);
-          S1 = fmaf(w, c1, S1);
-          S2 = fmaf(w, c2, S2);
-          T = Tp;
-        }
+  RecRegs<MAXK> r;
+  if (warp_last >= (int)range.x) {
+    for (int64_t end = (int64_t)warp_last + 1; end > (int64_t)range.x; end -= 32) {
+      const int64_t begin = max((int64_t)range.x, end - 32);
+      const int64_t idx = begin + lane;
+      uint32_t id = 0;
+      bool hit = false;
+      if (idx < end) {
+        id = __ldg(a.pair_ids + idx);
+        hit = box_overlaps(load_bbox(a.records, id, RF), rx0, ry0);
       }
-      if (__any_sync(0xffffffffu, contrib)) {
-        float *dst = a.accum + (size_t)s_id[j] * AF;
+      uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      while (mask) {
+        const int j = 31 - __clz(mask);   // back to front
+        mask &= ~(1u << j);
+        const uint32_t cid = __shfl_sync(0xffffffffu, id, j);
+        const int e_idx = (int)(begin + j);
+        r.load(a.records, cid);
+        const uint2 bb = load_bbox(a.records, cid, RF);
+        bool contrib = e_idx <= last && in_box(bb.x, bb.y, px, py);
+        float v[NG * 32];
 #pragma unroll
-        for (int gi = 0; gi < NG; gi++) {
-          float (&vv)[32] = *reinterpret_cast<float (*)[32]>(v + 32 * gi);
-          const float sum = transpose_reduce32(vv);
-          const int f = gi * 32 + lane;
-          if (f < AF && sum != 0.f) atomicAdd(dst + f, sum);
+        for (int f = 0; f < NG * 32; f++) v[f] = 0.f;
+        if (contrib) {
+          const float dx = qx - r.h0.x, dy = qy - r.h0.y;
+          const Eval e = eval_field<MAXK>(r, dx, dy, z);
+          n_eval++;
+          n_lines += r.nl();
+          contrib = e.alpha >= a.cutoff;
+          if (contrib) {
+            const float o = r.h0.w, sig = r.h0.z, dls = r.h2.y;
+            const float om = fmaxf(fmaf(o, e.J, r.h2.x), 1e-6f);
+            const float rom = 1.f / om;
+            const float Tp = T * rom;
+            const float w = Tp * e.alpha;
+            const float c0 = r.h1.x, c1 = r.h1.y, c2 = r.h1.z;
+            v[A_DC] = g0 * w;
+            v[A_DC + 1] = g1 * w;
+            v[A_DC + 2] = g2 * w;
+            float dA = g0 * (Tp * c0 - S0 * rom) + g1 * (Tp * c1 - S1 * rom) + g2 * (Tp * c2 - S2 * rom);
+            if (!(e.alpha_raw < (float)kAlphaMaxD)) dA = 0.f;
+            v[A_DOEFF] = dA * e.I;
+            const float dI = dA * o;
+            const float slope = e.I * e.J;
+            const float dphi = -sig * slope * dI;         // d loss / d phi (natural units)
+            v[A_DSIG] = -(e.phi2 * kLn2) * slope * dI;
+            const float rs = 1.f / e.s;
+            const int nl = r.nl();
+            float wz = 0.f;
+#pragma unroll
+            for (int l = 0; l < MAXK; l++) {
+              if (l < nl) {
+                const float wl = ex2(z[l] - e.m) * rs;    // softmax_over_lines (field.py:62-67)
+                wz = fmaf(wl, z[l], wz);
+                const float dL = dphi * (dls * kLn2) * wl;  // dphi * delta_s * w_l
+                v[A_LINES + 3 * l] = dL * dx;
+                v[A_LINES + 3 * l + 1] = dL * dy;
+                v[A_LINES + 3 * l + 2] = dL;
+              }
+            }
+            v[A_DDEL] = dphi * wz / dls;                   // dphi * sum_l w_l L_l
+            S0 = fmaf(w, c0, S0);
+            S1 = fmaf(w, c1, S1);
+            S2 = fmaf(w, c2, S2);
+            T = Tp;
+          }
+        }
+        if (__any_sync(0xffffffffu, contrib)) {
+          float *dst = a.accum + (size_t)cid * AF;
+#pragma unroll
+          for (int gi = 0; gi < NG; gi++) {
+            float (&vv)[32] = *reinterpret_cast<float (*)[32]>(v + 32 * gi);
+            const float sum = transpose_reduce32(vv);
+            const int f = gi * 32 + lane;
+            if (f < AF && sum != 0.f) atomicAdd(dst + f, sum);
+          }
         }
       }
     }
-    __syncthreads();
   }
   block_add_u64(a.stats + S_BWD_EVALS, n_eval);
   block_add_u64(a.stats + S_BWD_LINES, n_lines);

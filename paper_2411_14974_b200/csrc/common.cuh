@@ -26,7 +26,7 @@ constexpr uint64_t kCulledKey = ~0ull;
 // (keeps fp32 cancellation out of 1080p coordinates).
 enum RecField {
   R_AX = 0, R_AY = 1, R_SIGMA = 2, R_OPACITY = 3, R_R = 4, R_G = 5, R_B = 6, R_DEPTH = 7,
-  R_ONE_MINUS_O = 8, R_DLS = 9, R_NLINES = 10, R_BBX = 11, R_BBY = 12, R_HEADER = 16
+  R_ONE_MINUS_O = 8, R_DLS = 9, R_NLINES = 10, R_BBX = 12, R_BBY = 13, R_HEADER = 16
 };
 template <int MAXK> struct Rec {
   static constexpr int kFloats = R_HEADER + 3 * MAXK;   // 40 for MAXK=8, multiple of 4

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a
     while (!done) {
       uint32_t v[kLookback];
 #pragma unroll
-      for (int q = 0; q < kLookback; q++) v[q] = c - q >= 0 ? lb[(c - q) * kRadix + d] : kFlagPrefix;
+      for (int q = 0; q < kLookback; q++) v[q] = c - q >= 0 ? lb[(c - q) * kRadix + d] : (2u << 30);
       int used = 0;
 #pragma unroll
       for (int q = 0; q < kLookback; q++) {
