@@ -812,3 +812,43 @@ int or_backward(const or_camera *cam, const or_settings *st, const or_params *P,
 }
 
 int or_max_points(void) { return OR_MAXPTS; }
+
+/* Analysis helper (test/tooling only): for each listed tile, the 256-bit
+ * mask (bit = ly*16+lx) of pixels that EVALUATE each candidate of the tile
+ * list in the reference walk (bbox holds the pixel and T >= floor when the
+ * candidate is reached), in list order.  masks: [sum of list lengths][8]. */
+int64_t or_eval_masks(const or_camera *cam, const or_settings *st, const or_view *V, const int64_t *tile_off,
+                      const int32_t *items, const int64_t *tile_list, int64_t n_list, uint32_t *masks) {
+    const int W = cam->width, H = cam->height, ts = st->tile, k = V->k;
+    const int tx_n = (W + ts - 1) / ts;
+    double dist[OR_MAXPTS];
+    int64_t w = 0;
+    if (ts != 16) return -1;
+    for (int64_t q = 0; q < n_list; q++) {
+        int64_t t = tile_list[q];
+        int ty = (int)(t / tx_n), tx = (int)(t % tx_n);
+        int ty0 = ty * ts, tx0 = tx * ts;
+        double T[256];
+        for (int p = 0; p < 256; p++) T[p] = 1.0;
+        for (int64_t e = tile_off[t]; e < tile_off[t + 1]; e++, w++) {
+            uint32_t *m = masks + 8 * w;
+            for (int b = 0; b < 8; b++) m[b] = 0;
+            int i = V->order[items[e]];
+            const int32_t *bb = V->bbox + 4 * i;
+            const int h = V->hull_n[i];
+            const double *nrm = V->normals + (size_t)i * k * 2, *off = V->offsets + (size_t)i * k;
+            for (int ly = 0; ly < 16; ly++) for (int lx = 0; lx < 16; lx++) {
+                int x = tx0 + lx, y = ty0 + ly, p = ly * 16 + lx;
+                if (x >= W || y >= H || x < bb[0] || x >= bb[1] || y < bb[2] || y >= bb[3]) continue;
+                if (st->floor > 0.0 && !(T[p] >= st->floor)) continue;
+                m[p >> 5] |= 1u << (p & 31);
+                double phi, ind;
+                field_at(nrm, off, h, V->delta_s[i], V->sigma_s[i], x + 0.5, y + 0.5, dist, &phi, &ind);
+                double a = V->opacity[i] * ind;
+                if (a > OR_ALPHA_MAX) a = OR_ALPHA_MAX;
+                if (a >= st->cutoff) T[p] *= 1.0 - a;
+            }
+        }
+    }
+    return w;
+}

@@ -48,6 +48,19 @@ struct Eval {
   float I, J, alpha, alpha_raw, phi2, m, s;
 };
 
+__device__ __forceinline__ bool in_box(uint32_t bx, uint32_t by, int px, int py) {
+  return px >= (int)(bx & 0xffffu) && px < (int)(bx >> 16) && py >= (int)(by & 0xffffu) && py < (int)(by >> 16);
+}
+
+// Does the bbox of candidate id overlap the warp's 8x4 pixel block?
+__device__ __forceinline__ uint2 load_bbox(const float *records, uint32_t id, int rf) {
+  return __ldg(reinterpret_cast<const uint2 *>(records + (size_t)id * rf + R_BBX));
+}
+__device__ __forceinline__ bool box_overlaps(uint2 b, int rx0, int ry0) {
+  return (int)(b.x & 0xffffu) < rx0 + 8 && (int)(b.x >> 16) > rx0 && (int)(b.y & 0xffffu) < ry0 + 4 &&
+         (int)(b.y >> 16) > ry0;
+}
+
 // Candidate record held in registers (loaded with warp-broadcast 128-bit
 // loads: every lane reads the same address, one request per load).
 template <int MAXK>
@@ -65,8 +78,50 @@ struct RecRegs {
       ln[4 * q] = v.x; ln[4 * q + 1] = v.y; ln[4 * q + 2] = v.z; ln[4 * q + 3] = v.w;
     }
   }
+  __device__ __forceinline__ void load_smem(const float4 *r) {
+    h0 = r[0];
+    h1 = r[1];
+    h2 = r[2];
+#pragma unroll
+    for (int q = 0; q < 3 * MAXK / 4; q++) {
+      const float4 v = r[R_HEADER / 4 + q];
+      ln[4 * q] = v.x; ln[4 * q + 1] = v.y; ln[4 * q + 2] = v.z; ln[4 * q + 3] = v.w;
+    }
+  }
   __device__ __forceinline__ int nl() const { return __float_as_int(h2.z); }
 };
+
+constexpr int kBatch = 128;  // candidates staged per block iteration (4 ballots per warp)
+
+// Stage the records of pair indices [start, start+nb) into shared memory
+// (coalesced 16-byte gathers; consecutive threads read consecutive pieces of
+// one record) and cull them against this warp's 8x4 pixel block: bit j of
+// mask[q] is set iff candidate 32q+j's bbox overlaps the block.
+template <int MAXK>
+__device__ __forceinline__ void stage_and_cull(const float *records, const uint32_t *pair_ids, uint32_t start,
+                                               int nb, float4 *s_rec, uint32_t *s_id, int rx0, int ry0,
+                                               bool warp_live, uint32_t (&mask)[kBatch / 32]) {
+  constexpr int Q = Rec<MAXK>::kFloats / 4;
+  if (threadIdx.x < nb) s_id[threadIdx.x] = __ldg(pair_ids + start + threadIdx.x);
+  __syncthreads();
+  const float4 *src = reinterpret_cast<const float4 *>(records);
+  for (int q = threadIdx.x; q < nb * Q; q += kBlendThreads) {
+    const int r = q / Q, part = q - r * Q;
+    s_rec[q] = __ldg(src + (size_t)s_id[r] * Q + part);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < kBatch / 32; q++) {
+    const int c = 32 * q + lane;
+    bool hit = false;
+    if (warp_live && c < nb) {
+      const float4 bb = s_rec[c * Q + R_BBX / 4];
+      hit = box_overlaps(make_uint2(__float_as_uint(bb.x), __float_as_uint(bb.y)), rx0, ry0);
+    }
+    mask[q] = __ballot_sync(0xffffffffu, hit);
+  }
+}
 
 // smooth field of a candidate at anchor-relative pixel (dx, dy):
 // z2_j = A_j dx + B_j dy + C_j, phi2 = max z2 + log2 sum 2^(z2 - max),
@@ -102,25 +157,13 @@ __device__ __forceinline__ Eval eval_field(const RecRegs<MAXK> &r, float dx, flo
   return e;
 }
 
-__device__ __forceinline__ bool in_box(uint32_t bx, uint32_t by, int px, int py) {
-  return px >= (int)(bx & 0xffffu) && px < (int)(bx >> 16) && py >= (int)(by & 0xffffu) && py < (int)(by >> 16);
-}
-
-// Does the bbox of candidate id overlap the warp's 8x4 pixel block?
-__device__ __forceinline__ uint2 load_bbox(const float *records, uint32_t id, int rf) {
-  return __ldg(reinterpret_cast<const uint2 *>(records + (size_t)id * rf + R_BBX));
-}
-__device__ __forceinline__ bool box_overlaps(uint2 b, int rx0, int ry0) {
-  return (int)(b.x & 0xffffu) < rx0 + 8 && (int)(b.x >> 16) > rx0 && (int)(b.y & 0xffffu) < ry0 + 4 &&
-         (int)(b.y >> 16) > ry0;
-}
-
-// Forward blend, one tile per block; every warp walks the tile's candidate
-// list on its own (no block barriers): 32 candidates at a time are culled by
-// a ballot against the warp's 8x4 pixel block, survivors are evaluated
-// per pixel, and the warp leaves once all 32 of its pixels are done.
+// Forward blend, one tile per block.  Batches of 128 candidates are staged in
+// shared memory; each warp culls the batch with four ballots against its 8x4
+// pixel block and evaluates only the overlapping candidates, per pixel, in
+// list order.  A warp stops evaluating once its 32 pixels are done; the block
+// leaves the tile when all are.
 template <int MAXK>
-__global__ void __launch_bounds__(kBlendThreads, 4) forward_kernel(BlendArgs a) {
+__global__ void __launch_bounds__(kBlendThreads) forward_kernel(BlendArgs a) {
   constexpr int RF = Rec<MAXK>::kFloats;
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -139,44 +182,52 @@ __global__ void __launch_bounds__(kBlendThreads, 4) forward_kernel(BlendArgs a) 
   const bool use_floor = a.floor > 0.f;
   float z[MAXK];
   RecRegs<MAXK> r;
-  for (uint32_t base = range.x; base < range.y; base += 32) {
-    if (__all_sync(0xffffffffu, done)) break;
-    const uint32_t idx = base + lane;
-    uint32_t id = 0;
-    bool hit = false;
-    if (idx < range.y) {
-      id = __ldg(a.pair_ids + idx);
-      hit = box_overlaps(load_bbox(a.records, id, RF), rx0, ry0);
-    }
-    uint32_t mask = __ballot_sync(0xffffffffu, hit);
-    while (mask) {
-      const int j = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const uint32_t cid = __shfl_sync(0xffffffffu, id, j);
-      r.load(a.records, cid);
-      const uint2 bb = load_bbox(a.records, cid, RF);
-      bool blended = false;
-      if (!done && in_box(bb.x, bb.y, px, py)) {
-        const Eval e = eval_field<MAXK>(r, qx - r.h0.x, qy - r.h0.y, z);
-        n_eval++;
-        n_lines += r.nl();
-        if (e.alpha >= a.cutoff) {
-          const float w = T * e.alpha;
-          C0 = fmaf(w, r.h1.x, C0);
-          C1 = fmaf(w, r.h1.y, C1);
-          C2 = fmaf(w, r.h1.z, C2);
-          Wsum += w;
-          D = fmaf(w, r.h1.w, D);
-          T *= fmaxf(fmaf(r.h0.w, e.J, r.h2.x), 1e-6f);
-          cnt++;
-          last = (int)(base + j);
-          blended = true;
-          if (use_floor && T < a.floor) done = true;
+  __shared__ float4 s_rec[kBatch * (RF / 4)];
+  __shared__ uint32_t s_id[kBatch];
+  __shared__ uint8_t s_vis[kBatch];
+  for (uint32_t start = range.x; start < range.y; start += kBatch) {
+    if (__syncthreads_count(!done) == 0) break;
+    const int nb = (int)min((uint32_t)kBatch, range.y - start);
+    if (threadIdx.x < kBatch) s_vis[threadIdx.x] = 0;
+    uint32_t mask[kBatch / 32];
+    stage_and_cull<MAXK>(a.records, a.pair_ids, start, nb, s_rec, s_id, rx0, ry0,
+                         !__all_sync(0xffffffffu, done), mask);
+    bool warp_done = false;
+#pragma unroll
+    for (int q = 0; q < kBatch / 32; q++) {
+      uint32_t m = warp_done ? 0u : mask[q];
+      while (m) {
+        const int j = 32 * q + __ffs(m) - 1;
+        m &= m - 1;
+        r.load_smem(s_rec + j * (RF / 4));
+        const uint2 bb = make_uint2(__float_as_uint(s_rec[j * (RF / 4) + R_BBX / 4].x),
+                                    __float_as_uint(s_rec[j * (RF / 4) + R_BBX / 4].y));
+        if (!done && in_box(bb.x, bb.y, px, py)) {
+          const Eval e = eval_field<MAXK>(r, qx - r.h0.x, qy - r.h0.y, z);
+          n_eval++;
+          n_lines += r.nl();
+          if (e.alpha >= a.cutoff) {
+            const float w = T * e.alpha;
+            C0 = fmaf(w, r.h1.x, C0);
+            C1 = fmaf(w, r.h1.y, C1);
+            C2 = fmaf(w, r.h1.z, C2);
+            Wsum += w;
+            D = fmaf(w, r.h1.w, D);
+            T *= fmaxf(fmaf(r.h0.w, e.J, r.h2.x), 1e-6f);
+            cnt++;
+            last = (int)(start + j);
+            s_vis[j] = 1;
+            if (use_floor && T < a.floor) done = true;
+          }
+        }
+        if (__all_sync(0xffffffffu, done)) {  // this warp is finished with the tile
+          warp_done = true;
+          m = 0;
         }
       }
-      if (__any_sync(0xffffffffu, blended) && lane == 0 && a.visible) a.visible[cid] = 1;
-      if (__all_sync(0xffffffffu, done)) break;
     }
+    __syncthreads();
+    if (a.visible && threadIdx.x < nb && s_vis[threadIdx.x]) a.visible[s_id[threadIdx.x]] = 1;
   }
   block_add_u64(a.stats + S_FWD_EVALS, n_eval);
   block_add_u64(a.stats + S_FWD_LINES, n_lines);
@@ -213,11 +264,11 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
   return v[0];
 }
 
-// Backward blend (backward.py:110-205): every warp walks the tile list back
-// to front from the largest `last` of its pixels, culls 32 candidates at a
-// time by ballot, reconstructs T_prev = T / (1 - alpha) per pixel and
-// reduces the 32 screen-space gradient values of each candidate across the
-// warp (transpose-reduce) into one vector of float atomics.
+// Backward blend (backward.py:110-205): the block walks the tile list back
+// to front from the largest `last` of its pixels in staged batches; each warp
+// culls a batch by ballot, reconstructs T_prev = T / (1 - alpha) per pixel
+// and reduces the 32 screen-space gradient values of each candidate across
+// the warp (transpose-reduce) into one vector of float atomics.
 template <int MAXK>
 __global__ void __launch_bounds__(kBlendThreads) backward_kernel(BlendArgs a) {
   constexpr int RF = Rec<MAXK>::kFloats;
@@ -248,28 +299,36 @@ __global__ void __launch_bounds__(kBlendThreads) backward_kernel(BlendArgs a) {
     S1 = T * a.bg[1];
     S2 = T * a.bg[2];
   }
-  // nothing behind the warp's last blended candidate matters
+  // nothing behind the last blended candidate of the block matters
   const int warp_last = __reduce_max_sync(0xffffffffu, last);
+  __shared__ int s_wl[kBlendThreads / 32];
+  if (lane == 0) s_wl[warp] = warp_last;
+  __syncthreads();
+  int block_last = s_wl[0];
+#pragma unroll
+  for (int w = 1; w < kBlendThreads / 32; w++) block_last = max(block_last, s_wl[w]);
   float z[MAXK];
   RecRegs<MAXK> r;
-  if (warp_last >= (int)range.x) {
-    for (int64_t end = (int64_t)warp_last + 1; end > (int64_t)range.x; end -= 32) {
-      const int64_t begin = max((int64_t)range.x, end - 32);
-      const int64_t idx = begin + lane;
-      uint32_t id = 0;
-      bool hit = false;
-      if (idx < end) {
-        id = __ldg(a.pair_ids + idx);
-        hit = box_overlaps(load_bbox(a.records, id, RF), rx0, ry0);
-      }
-      uint32_t mask = __ballot_sync(0xffffffffu, hit);
-      while (mask) {
-        const int j = 31 - __clz(mask);   // back to front
-        mask &= ~(1u << j);
-        const uint32_t cid = __shfl_sync(0xffffffffu, id, j);
-        const int e_idx = (int)(begin + j);
-        r.load(a.records, cid);
-        const uint2 bb = load_bbox(a.records, cid, RF);
+  __shared__ float4 s_rec[kBatch * (RF / 4)];
+  __shared__ uint32_t s_id[kBatch];
+  for (int64_t end = (int64_t)block_last + 1; end > (int64_t)range.x; end -= kBatch) {
+    const uint32_t start = (uint32_t)max((int64_t)range.x, end - kBatch);
+    const int nb = (int)(end - start);
+    uint32_t mask[kBatch / 32];
+    __syncthreads();  // previous batch fully consumed before restaging
+    stage_and_cull<MAXK>(a.records, a.pair_ids, start, nb, s_rec, s_id, rx0, ry0,
+                         warp_last >= (int)start, mask);
+#pragma unroll
+    for (int q = kBatch / 32 - 1; q >= 0; q--) {
+      uint32_t m = mask[q];
+      while (m) {
+        const int jj = 31 - __clz(m);   // back to front
+        m &= ~(1u << jj);
+        const int j = 32 * q + jj;
+        const int e_idx = (int)start + j;
+        r.load_smem(s_rec + j * (RF / 4));
+        const uint2 bb = make_uint2(__float_as_uint(s_rec[j * (RF / 4) + R_BBX / 4].x),
+                                    __float_as_uint(s_rec[j * (RF / 4) + R_BBX / 4].y));
         bool contrib = e_idx <= last && in_box(bb.x, bb.y, px, py);
         float v[NG * 32];
 #pragma unroll
@@ -319,7 +378,7 @@ __global__ void __launch_bounds__(kBlendThreads) backward_kernel(BlendArgs a) {
           }
         }
         if (__any_sync(0xffffffffu, contrib)) {
-          float *dst = a.accum + (size_t)cid * AF;
+          float *dst = a.accum + (size_t)s_id[j] * AF;
 #pragma unroll
           for (int gi = 0; gi < NG; gi++) {
             float (&vv)[32] = *reinterpret_cast<float (*)[32]>(v + 32 * gi);
