@@ -54,6 +54,11 @@ def parse_args():
     p.add_argument("--cpu-budget-s", type=float, default=15.0, help="CPU-baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-train", action="store_true", help="skip the config-5 view-sharded training step")
+    p.add_argument("--train-views", type=int, default=64)
+    p.add_argument("--train-width", type=int, default=1297)
+    p.add_argument("--train-height", type=int, default=840)
+    p.add_argument("--train-steps", type=int, default=5)
     return p.parse_args()
 
 
@@ -219,6 +224,58 @@ def run_reference(args):
                              "cpu": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- config 5
+def train_step_bench(args, st, arrays, dev, world, rank):
+    """One optimisation step over a batch of B ring views (1297x840): views
+    sharded round-robin over the ranks, device loss (L1 + D-SSIM + mask),
+    backward through the C ABI into one flat buffer, one NCCL all_reduce,
+    Adam on every rank.  Targets are renders of a perturbed scene."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_14974_b200 import sharded, synthetic
+    from paper_2411_14974_b200.model import RenderSettings, ScalingMode
+    from paper_2411_14974_b200.rasterizer import Rasterizer
+    from paper_2411_14974_b200.scene_tensors import SceneTensors
+
+    cams = synthetic.ring_cameras(args.train_views, args.train_width, args.train_height)
+    mode, settings = ScalingMode.DEPTH, RenderSettings()
+    r = Rasterizer(dev)
+    tgt = SceneTensors.from_arrays(synthetic.quantize32(synthetic.perturb(arrays, seed=1)), dev)
+    mine = set(sharded.shard_views(list(range(len(cams))), rank, world))
+    views = [(c, r.forward(tgt, c, mode, settings).image.clone() if i in mine else None) for i, c in enumerate(cams)]
+    del tgt
+    scene = SceneTensors(*(getattr(st, k).clone() for k in ("points", "raw_delta", "raw_sigma", "raw_opacity",
+                                                            "raw_mask", "sh")), background=st.background)
+    params = {k: getattr(scene, k) for k in sharded.PARAM_ORDER}
+    step = sharded.ViewShardedStep(params, sharded.StepConfig(),
+                                   sharded.rasterizer_view_grad_fn(scene, mode, settings, rasterizer=r))
+    stream = torch.cuda.current_stream(dev)
+    step.step(views)                                   # warm-up (sizes every view's pair capacity)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    times, losses = [], []
+    for _ in range(args.train_steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        info = step.step(views)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        times.append(e0.elapsed_time(e1))
+        losses.append(float(info["local_loss_sum"]))
+    t = torch.tensor([sum(times) / len(times)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    return {"metric": "view-sharded training steps/s (config 5)", "steps_per_s": 1000.0 / ms, "ms_per_step": ms,
+            "views_per_s": args.train_views * 1000.0 / ms, "batch_views": args.train_views,
+            "view_size": [args.train_width, args.train_height], "convexes": st.n, "ranks": world,
+            "views_per_rank": len(mine), "steps": args.train_steps, "scaling": "strong (fixed batch of views)",
+            "collective": "one all_reduce(SUM) of %d float32 per step" % step.flat.buffer.numel(),
+            "rank0_loss_sum_first_last": [losses[0], losses[-1]]}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -388,6 +445,11 @@ def main():
                                 "(sm_max_mhz of MEASURED_PEAKS.json)"),
                 "stages": stage_info}
 
+    # ---- config 5: view-sharded training step (B views, all_reduce of the gradients)
+    train = None
+    if not args.no_train:
+        train = train_step_bench(args, st, arrays, dev, world, rank)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = host_cores()
@@ -412,7 +474,7 @@ def main():
                      "fwd_total": float(fwd.sum(axis=1).mean()), "zero+forward": float(bwd_ms[0]),
                      "backward_blend": float(bwd_ms[1]), "chain": float(bwd_ms[2])},
         "work": {k2: int(v) for k2, v in stats.items()},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clock,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clock, "train_step": train,
         "gpu_launches": args.steps * launches_fwd + args.steps * (launches_fwd + 2),
         "gpu_launches_detail": f"{launches_fwd} per forward (1 preprocess, 10 depth sort, 3 scan, 1 duplicate, "
                                f"{2 + pp} pair sort, 1 ranges, 1 blend), 2 per backward",

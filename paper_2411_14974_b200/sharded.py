@@ -1,0 +1,238 @@
+"""View-sharded training step (north_star item 5).
+
+One process per GPU.  A batch of B views is split round-robin (view i goes to
+rank i mod G).  Each rank renders its views, evaluates the reference training
+loss on the device, and accumulates the per-view gradients straight into one
+flat float32 buffer (the C ABI accumulates, matching GradientBuffer.add,
+backward.py:65-73).  The per-view sigma signal of trainer.py:192-193
+(|d_raw_sigma| * visible and the visible-view count) is accumulated beside it,
+because it cannot be formed from the summed gradient.  One all_reduce(SUM)
+over NCCL combines the buffer; every rank then applies the identical Adam step
+(optim.py:12-35, position schedule optim.py:56-61), so replicas stay equal.
+
+The loss mirrors losses.py:129-155 (L1 + D-SSIM with an 11x11 sigma-1.5
+Gaussian valid window + beta * mean sigmoid(mask)); its gradient w.r.t. the
+rendered image comes from torch autograd of the same expression.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+import torch.nn.functional as F
+
+PARAM_ORDER = ("points", "raw_delta", "raw_sigma", "raw_opacity", "sh", "raw_mask")
+GROUP_OF = {"points": "points", "raw_delta": "delta", "raw_sigma": "sigma", "raw_opacity": "opacity",
+            "sh": "sh", "raw_mask": "mask"}
+
+
+@dataclass
+class StepConfig:
+    """Subset of trainer.TrainConfig (trainer.py:19-62) the step uses."""
+
+    total_iterations: int = 30000
+    lambda_dssim: float = 0.2
+    beta_mask: float = 0.0005
+    lr_position_init: float = 5e-4
+    lr_position_final: float = 5e-6
+    lr_delta: float = 0.005
+    lr_sigma: float = 0.0045
+    lr_opacity: float = 0.05
+    lr_sh: float = 0.0025
+    lr_mask: float = 0.01
+
+
+# --------------------------------------------------------------------------- loss (losses.py)
+SSIM_C1, SSIM_C2 = 0.01 ** 2, 0.03 ** 2
+
+
+def gaussian_window(size: int = 11, sigma: float = 1.5, device=None, dtype=torch.float32) -> torch.Tensor:
+    """losses.py:22-25"""
+    off = torch.arange(size, dtype=torch.float64) - (size - 1) / 2.0
+    g = torch.exp(-(off ** 2) / (2.0 * sigma * sigma))
+    return (g / g.sum()).to(device=device, dtype=dtype)
+
+
+def _filter_valid(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """Separable valid-window Gaussian mean (losses.py:31-42); x: [C, H, W]."""
+    k = w.numel()
+    x = x.unsqueeze(1)
+    x = F.conv2d(x, w.view(1, 1, k, 1))
+    x = F.conv2d(x, w.view(1, 1, 1, k))
+    return x.squeeze(1)
+
+
+def ssim(img: torch.Tensor, target: torch.Tensor, window: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Mean SSIM of two [H, W, 3] images (losses.py:58-84), differentiable."""
+    if img.shape != target.shape:
+        raise ValueError(f"shape mismatch {tuple(img.shape)} vs {tuple(target.shape)}")
+    if img.shape[0] < 11 or img.shape[1] < 11:
+        raise ValueError("image smaller than the 11x11 SSIM window")
+    w = window if window is not None else gaussian_window(device=img.device, dtype=img.dtype)
+    x, y = img.permute(2, 0, 1), target.permute(2, 0, 1)
+    mx, my = _filter_valid(x, w), _filter_valid(y, w)
+    sxx = _filter_valid(x * x, w) - mx * mx
+    syy = _filter_valid(y * y, w) - my * my
+    sxy = _filter_valid(x * y, w) - mx * my
+    smap = ((2 * mx * my + SSIM_C1) * (2 * sxy + SSIM_C2)) / ((mx * mx + my * my + SSIM_C1) * (sxx + syy + SSIM_C2))
+    return smap.mean(dim=(1, 2)).mean()
+
+
+def image_loss(img: torch.Tensor, target: torch.Tensor, raw_mask: torch.Tensor, lambda_dssim: float = 0.2,
+               beta_mask: float = 0.0005) -> dict:
+    """(1-lambda) L1 + lambda (1-SSIM)/2 + beta mean(sigmoid(raw_mask)) (losses.py:129-155)."""
+    l1 = (img - target).abs().mean()
+    dssim = (1.0 - ssim(img, target)) / 2.0
+    mask_term = torch.sigmoid(raw_mask).mean() if raw_mask.numel() else img.new_zeros(())
+    total = (1.0 - lambda_dssim) * l1 + lambda_dssim * dssim + beta_mask * mask_term
+    return {"total": total, "l1": l1, "dssim": dssim, "mask_term": mask_term}
+
+
+# --------------------------------------------------------------------------- optimiser (optim.py)
+def position_lr(iteration: int, lr_init: float, lr_final: float, total: int) -> float:
+    """optim.py:56-61"""
+    if total <= 0:
+        return lr_init
+    frac = min(max(iteration / total, 0.0), 1.0)
+    return float(lr_init * (lr_final / lr_init) ** frac)
+
+
+class Adam:
+    """optim.py:12-35 over the parameter tensors, in place, via foreach kernels."""
+
+    def __init__(self, params: dict, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-15):
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.step_count = 0
+        self.m = {k: torch.zeros_like(v) for k, v in params.items()}
+        self.v = {k: torch.zeros_like(v) for k, v in params.items()}
+
+    @torch.no_grad()
+    def step(self, params: dict, grads: dict, lrs: dict):
+        self.step_count += 1
+        bc1 = 1.0 - self.beta1 ** self.step_count
+        bc2 = 1.0 - self.beta2 ** self.step_count
+        for name, p in params.items():
+            g, m, v = grads[name], self.m[name], self.v[name]
+            m.mul_(self.beta1).add_(g, alpha=1.0 - self.beta1)
+            v.mul_(self.beta2).addcmul_(g, g, value=1.0 - self.beta2)
+            denom = (v / bc2).sqrt_().add_(self.eps)
+            p.addcdiv_(m, denom, value=-lrs[name] / bc1)
+
+
+# --------------------------------------------------------------------------- sharding
+def shard_views(batch: list, rank: int, world: int) -> list:
+    """Round-robin assignment: batch position i goes to rank i mod world."""
+    return [v for i, v in enumerate(batch) if i % world == rank]
+
+
+class FlatGrads:
+    """One contiguous float32 buffer: the six gradient tensors (pack_grads
+    order of backward.py:322-329 per tensor) + sigma-signal sum + view count.
+    A single all_reduce moves all of it."""
+
+    def __init__(self, shapes: dict, n: int, device, dtype=torch.float32):
+        self.names = list(PARAM_ORDER)
+        sizes = [int(math.prod(shapes[k])) for k in self.names] + [n, n]
+        self.buffer = torch.zeros(sum(sizes), dtype=dtype, device=device)
+        self.views, off = {}, 0
+        for k, sz in zip(self.names + ["sigma_signal", "sigma_views"], sizes):
+            shape = shapes[k] if k in shapes else (n,)
+            self.views[k] = self.buffer[off:off + sz].view(shape)
+            off += sz
+
+    def zero_(self):
+        self.buffer.zero_()
+
+    def grads(self) -> dict:
+        return {k: self.views[k] for k in self.names}
+
+
+class ViewShardedStep:
+    """Training step over a batch of views, sharded across the ranks of
+    ``group`` (world size 1 without torch.distributed).
+
+    ``view_grad_fn(view, grads: dict, sigma_scratch) -> (loss, visible)``
+    renders one view and ACCUMULATES its gradients into ``grads``; the default
+    uses the sm_100a rasterizer and the device loss.  Tests substitute a CPU
+    function to exercise the sharding / all-reduce / update logic under gloo.
+    """
+
+    def __init__(self, params: dict, config: StepConfig = StepConfig(), view_grad_fn: Callable = None,
+                 group=None):
+        self.params = params
+        self.config = config
+        self.group = group
+        self.distributed = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.distributed else 0
+        self.world = dist.get_world_size(group) if self.distributed else 1
+        n = params["points"].shape[0]
+        self.flat = FlatGrads({k: tuple(v.shape) for k, v in params.items()}, n, params["points"].device,
+                              params["points"].dtype)
+        self.adam = Adam(params)
+        self.view_grad_fn = view_grad_fn
+        self.iteration = 0
+
+    def lrs(self, iteration: int) -> dict:
+        c = self.config
+        return {"points": position_lr(iteration, c.lr_position_init, c.lr_position_final, c.total_iterations),
+                "raw_delta": c.lr_delta, "raw_sigma": c.lr_sigma, "raw_opacity": c.lr_opacity, "sh": c.lr_sh,
+                "raw_mask": c.lr_mask}
+
+    def accumulate(self, batch: list) -> dict:
+        """Local part: this rank's views, gradients summed into the flat buffer."""
+        self.flat.zero_()
+        grads = self.flat.grads()
+        sigma_prev = torch.empty_like(grads["raw_sigma"])
+        losses = []
+        for view in shard_views(batch, self.rank, self.world):
+            sigma_prev.copy_(grads["raw_sigma"])
+            loss, visible = self.view_grad_fn(view, grads)
+            # trainer.py:192-193: per-view |d_raw_sigma| on the visible primitives
+            vis = visible.to(self.flat.buffer.dtype)
+            self.flat.views["sigma_signal"].add_((grads["raw_sigma"] - sigma_prev).abs_() * vis)
+            self.flat.views["sigma_views"].add_(vis)
+            losses.append(loss.detach().reshape(()))
+        total = torch.stack(losses).sum() if losses else torch.zeros((), device=self.flat.buffer.device)
+        return {"local_views": len(losses), "local_loss_sum": total}
+
+    def reduce(self, batch_size: int):
+        """The single collective: sum of everyone's gradients, then / B."""
+        if self.world > 1:
+            dist.all_reduce(self.flat.buffer, op=dist.ReduceOp.SUM, group=self.group)
+        for k in self.flat.names:
+            self.flat.views[k].div_(batch_size)
+
+    def step(self, batch: list) -> dict:
+        self.iteration += 1
+        info = self.accumulate(batch)
+        self.reduce(len(batch))
+        self.adam.step(self.params, self.flat.grads(), self.lrs(self.iteration))
+        return info
+
+
+def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConfig(), rasterizer=None):
+    """Default per-view function: render with the sm_100a path, device loss,
+    d_image by autograd of the loss, backward through the C ABI accumulating
+    into the given gradient buffers (+ the mask-loss gradient)."""
+    from .rasterizer import default_rasterizer
+
+    r = rasterizer or default_rasterizer(scene.device)
+
+    def fn(view, grads: dict):
+        cam, target = view
+        fr = r.forward(scene, cam, mode, settings)
+        img = fr.image.detach().requires_grad_(True)
+        raw_mask = scene.raw_mask.detach().requires_grad_(True)
+        loss = image_loss(img, target, raw_mask, config.lambda_dssim, config.beta_mask)
+        d_img, d_mask = torch.autograd.grad(loss["total"], (img, raw_mask))
+        r.launch_backward(fr, d_img.contiguous(), grads)
+        grads["raw_mask"].add_(d_mask)          # trainer.py:176 (straight-through mask-loss term)
+        return loss["total"].detach(), fr.visible
+    return fn
+
+
+__all__ = ["StepConfig", "image_loss", "ssim", "gaussian_window", "Adam", "position_lr", "shard_views",
+           "FlatGrads", "ViewShardedStep", "rasterizer_view_grad_fn"]

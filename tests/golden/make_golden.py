@@ -183,9 +183,35 @@ def gen_hulls():
     print(f"hulls: {len(cases)} cases")
 
 
+def gen_loss():
+    """image_loss / ssim_with_grad known answers (losses.py:58-155)."""
+    from convexsplat.optim import Adam, position_lr
+    rng = np.random.default_rng(7)
+    img = rng.uniform(0, 1, size=(23, 31, 3))
+    target = np.clip(img + rng.normal(0, 0.1, size=img.shape), 0, 1)
+    masks = rng.normal(0, 2, size=17)
+    res = image_loss(img, target, masks, 0.2, 0.0005)
+    # two Adam steps on a small parameter set (optim.py:12-35)
+    params = {"a": rng.normal(size=(5, 3)), "b": rng.normal(size=7)}
+    grads1 = {"a": rng.normal(size=(5, 3)), "b": rng.normal(size=7)}
+    grads2 = {"a": rng.normal(size=(5, 3)), "b": rng.normal(size=7)}
+    p0 = {k: v.copy() for k, v in params.items()}
+    adam = Adam({k: v.shape for k, v in params.items()})
+    adam.step(params, grads1, {"a": 0.01, "b": 0.002})
+    adam.step(params, grads2, {"a": 0.01, "b": 0.002})
+    np.savez_compressed(os.path.join(OUT, "loss.npz"), img=img, target=target, masks=masks,
+                        total=res.total, l1=res.l1, dssim=res.dssim, mask_term=res.mask_term,
+                        d_image=res.d_image, d_raw_mask=res.d_raw_mask,
+                        adam_a0=p0["a"], adam_b0=p0["b"], adam_ga1=grads1["a"], adam_gb1=grads1["b"],
+                        adam_ga2=grads2["a"], adam_gb2=grads2["b"], adam_a2=params["a"], adam_b2=params["b"],
+                        plr=np.array([position_lr(i, 5e-4, 5e-6, 1000) for i in (0, 250, 500, 1000, 2000)]))
+    print("loss: ok")
+
+
 def main():
     DEPTH, NONE = ScalingMode.DEPTH, ScalingMode.NONE
     gen_hulls()
+    gen_loss()
 
     # config 1 of BASELINE.json: 1k convexes, 256^2, fwd+bwd (SURVEY 8d)
     s1 = make_scene(1000, 6, seed=0, spread=1.0)
@@ -261,4 +287,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "loss":
+        gen_loss()
+    else:
+        main()

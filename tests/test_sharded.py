@@ -1,0 +1,154 @@
+"""View-sharded training step: loss / optimiser parity with the reference
+(fixtures from tests/golden/make_golden.py gen_loss) and the world-size-2
+sharding + all-reduce logic on CPU with the gloo backend."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2411_14974_b200 import sharded
+from tests import golden_cases as gc
+
+
+def test_image_loss_matches_reference():
+    g = np.load(os.path.join(gc.GOLDEN, "loss.npz"))
+    img = torch.tensor(g["img"], dtype=torch.float64, requires_grad=True)
+    target = torch.tensor(g["target"], dtype=torch.float64)
+    masks = torch.tensor(g["masks"], dtype=torch.float64, requires_grad=True)
+    loss = sharded.image_loss(img, target, masks, 0.2, 0.0005)
+    assert abs(float(loss["total"].detach()) - float(g["total"])) < 1e-12
+    assert abs(float(loss["l1"]) - float(g["l1"])) < 1e-12
+    assert abs(float(loss["dssim"]) - float(g["dssim"])) < 1e-12
+    assert abs(float(loss["mask_term"]) - float(g["mask_term"])) < 1e-12
+    d_img, d_mask = torch.autograd.grad(loss["total"], (img, masks))
+    np.testing.assert_allclose(d_img.numpy(), g["d_image"], rtol=1e-9, atol=1e-13)
+    np.testing.assert_allclose(d_mask.numpy(), g["d_raw_mask"], rtol=1e-9, atol=1e-15)
+
+
+def test_adam_and_position_lr_match_reference():
+    g = np.load(os.path.join(gc.GOLDEN, "loss.npz"))
+    params = {"a": torch.tensor(g["adam_a0"]), "b": torch.tensor(g["adam_b0"])}
+    adam = sharded.Adam(params)
+    adam.step(params, {"a": torch.tensor(g["adam_ga1"]), "b": torch.tensor(g["adam_gb1"])}, {"a": 0.01, "b": 0.002})
+    adam.step(params, {"a": torch.tensor(g["adam_ga2"]), "b": torch.tensor(g["adam_gb2"])}, {"a": 0.01, "b": 0.002})
+    np.testing.assert_allclose(params["a"].numpy(), g["adam_a2"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(params["b"].numpy(), g["adam_b2"], rtol=0, atol=1e-14)
+    got = [sharded.position_lr(i, 5e-4, 5e-6, 1000) for i in (0, 250, 500, 1000, 2000)]
+    np.testing.assert_allclose(got, g["plr"], rtol=1e-15)
+
+
+def test_adam_first_step_is_minus_lr_sign():
+    p = {"x": torch.tensor([1.0, -2.0, 3.0], dtype=torch.float64)}
+    adam = sharded.Adam(p)
+    adam.step(p, {"x": torch.tensor([0.5, -3.0, 0.0], dtype=torch.float64)}, {"x": 0.1})
+    np.testing.assert_allclose(p["x"].numpy(), [0.9, -1.9, 3.0], atol=1e-12)
+
+
+def test_round_robin_sharding_covers_batch_once():
+    batch = list(range(13))
+    parts = [sharded.shard_views(batch, r, 4) for r in range(4)]
+    assert sorted(v for part in parts for v in part) == batch
+    assert parts[1] == [1, 5, 9]
+
+
+def _params(seed=0, n=37, k=6):
+    gen = torch.Generator().manual_seed(seed)
+    f64 = dict(generator=gen, dtype=torch.float64)
+    return {"points": torch.randn(n, k, 3, **f64), "raw_delta": torch.randn(n, **f64),
+            "raw_sigma": torch.randn(n, **f64), "raw_opacity": torch.randn(n, **f64),
+            "sh": torch.randn(n, 16, 3, **f64), "raw_mask": torch.randn(n, **f64)}
+
+
+def _mock_view_grad_fn(params):
+    """Deterministic per-view gradients that depend on the current parameters
+    (stands in for render + loss + backward, which need the GPU)."""
+    def fn(view, grads):
+        v = float(view)
+        for name, g in grads.items():
+            g.add_(torch.sin(params[name] * (1.0 + 0.1 * v) + v))
+        n = params["points"].shape[0]
+        visible = (torch.arange(n) % (int(view) + 2)) != 0
+        return torch.tensor(v), visible
+    return fn
+
+
+def _run_steps(params, batch, steps):
+    step = sharded.ViewShardedStep(params, sharded.StepConfig(total_iterations=100),
+                                   _mock_view_grad_fn(params))
+    for _ in range(steps):
+        step.step(batch)
+    return step
+
+
+def _worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        params = _params()
+        step = _run_steps(params, list(range(6)), 3)
+        torch.save({"params": params, "sigma": step.flat.views["sigma_signal"].clone(),
+                    "views": step.flat.views["sigma_views"].clone()}, f"{out_path}.{rank}")
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_two_rank_gloo_step_equals_single_process():
+    """North_star 5 semantics on CPU: the 2-rank sharded step (one all_reduce
+    per step) leaves both replicas identical and equal to one process
+    summing all six views."""
+    with tempfile.TemporaryDirectory() as tmp:
+        out = os.path.join(tmp, "res")
+        mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+        r0, r1 = torch.load(f"{out}.0"), torch.load(f"{out}.1")
+    single_params = _params()
+    single = _run_steps(single_params, list(range(6)), 3)
+    for name in single_params:
+        torch.testing.assert_close(r0["params"][name], r1["params"][name], rtol=0, atol=0)
+        torch.testing.assert_close(r0["params"][name], single_params[name], rtol=1e-10, atol=1e-12)
+    torch.testing.assert_close(r0["sigma"], single.flat.views["sigma_signal"], rtol=1e-10, atol=1e-12)
+    torch.testing.assert_close(r0["views"], single.flat.views["sigma_views"], rtol=0, atol=0)
+
+
+@pytest.mark.gpu
+def test_sharded_step_gradients_equal_sum_of_view_backwards():
+    """World size 1 on the GPU: the flat buffer after accumulate() equals the
+    sum over views of rasterize-autograd gradients of the same loss."""
+    import paper_2411_14974_b200 as cs
+    from paper_2411_14974_b200 import synthetic
+    arrays = synthetic.quantize32(synthetic.generate_scene(3000, seed=3))
+    cams = synthetic.ring_cameras(3, 96, 72)
+    st = cs.SceneTensors.from_arrays(arrays, "cuda")
+    target_arrays = synthetic.quantize32(synthetic.perturb(arrays, seed=5))
+    tgt = cs.SceneTensors.from_arrays(target_arrays, "cuda")
+    views = [(c, cs.render(tgt, c).image) for c in cams]
+    views = [(c, torch.tensor(t, dtype=torch.float32, device="cuda")) for c, t in views]
+    params = {k: getattr(st, k) for k in sharded.PARAM_ORDER}
+    mode, settings = cs.ScalingMode.DEPTH, cs.RenderSettings()
+    step = sharded.ViewShardedStep(params, sharded.StepConfig(), sharded.rasterizer_view_grad_fn(st, mode, settings))
+    step.accumulate(views)
+    ref = {k: torch.zeros_like(v) for k, v in params.items()}
+    for cam, target in views:
+        leaves = {k: v.detach().clone().requires_grad_(True) for k, v in params.items()}
+        scene = cs.SceneTensors(**{k: leaves[k] for k in ("points", "raw_delta", "raw_sigma", "raw_opacity",
+                                                          "raw_mask", "sh")}, background=st.background)
+        img = cs.rasterize(scene, cam, mode, settings)[0]
+        loss = sharded.image_loss(img, target, leaves["raw_mask"])["total"]
+        loss.backward()
+        for k in ref:
+            ref[k] += leaves[k].grad
+    for k in ref:
+        a, b = step.flat.views[k].cpu().numpy().ravel(), ref[k].cpu().numpy().ravel()
+        den = np.maximum(np.abs(a), np.abs(b))
+        rel = np.abs(a - b) / np.maximum(den, max(1e-4 * den.max(), 1e-12))
+        assert rel.max() < 1e-3, (k, rel.max())
