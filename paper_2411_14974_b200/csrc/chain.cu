@@ -36,70 +36,105 @@ struct ChainArgs {
 
 template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 128 : 64; }
 
+// d(Y_b)/d(dir) . v_b added into (gx, gy, gz): eval_sh_basis_grad
+// (harmonics.py:62-98) row b, written out (b is a compile-time constant).
+__device__ __forceinline__ void add_basis_grad(int b, double v, double x, double y, double z, double &gx, double &gy,
+                                               double &gz) {
+  const double xx = x * x, yy = y * y, zz = z * z;
+  switch (b) {
+    case 1: gy -= kC1 * v; break;
+    case 2: gz += kC1 * v; break;
+    case 3: gx -= kC1 * v; break;
+    case 4: gx += kC20 * y * v; gy += kC20 * x * v; break;
+    case 5: gy += kC21 * z * v; gz += kC21 * y * v; break;
+    case 6: gx += -2.0 * kC22 * x * v; gy += -2.0 * kC22 * y * v; gz += 4.0 * kC22 * z * v; break;
+    case 7: gx += kC23 * z * v; gz += kC23 * x * v; break;
+    case 8: gx += 2.0 * kC24 * x * v; gy += -2.0 * kC24 * y * v; break;
+    case 9: gx += kC30 * 6.0 * x * y * v; gy += kC30 * 3.0 * (xx - yy) * v; break;
+    case 10: gx += kC31 * y * z * v; gy += kC31 * x * z * v; gz += kC31 * x * y * v; break;
+    case 11:
+      gx += -2.0 * kC32 * x * y * v; gy += kC32 * (4.0 * zz - xx - 3.0 * yy) * v; gz += 8.0 * kC32 * y * z * v;
+      break;
+    case 12:
+      gx += -6.0 * kC33 * x * z * v; gy += -6.0 * kC33 * y * z * v; gz += kC33 * (6.0 * zz - 3.0 * xx - 3.0 * yy) * v;
+      break;
+    case 13:
+      gx += kC34 * (4.0 * zz - 3.0 * xx - yy) * v; gy += -2.0 * kC34 * x * y * v; gz += 8.0 * kC34 * x * z * v;
+      break;
+    case 14: gx += 2.0 * kC35 * x * z * v; gy += -2.0 * kC35 * y * z * v; gz += kC35 * (xx - yy) * v; break;
+    case 15: gx += kC36 * 3.0 * (xx - yy) * v; gy += -6.0 * kC36 * x * y * v; break;
+    default: break;
+  }
+}
+
 // SH colour VJP (harmonics.py:112-128): d_sh += Y (x) d_eff and the
-// direction gradient dY/ddir^T (sh . d_eff), with eval_sh_basis_grad
-// (harmonics.py:62-98) written out per basis function.
+// direction gradient dY/ddir^T (sh . d_eff).  Streams the 16x3 rows as
+// float4 (two reads of sh, one read-modify-write of d_sh) so no per-thread
+// 48-float arrays stay live.
 __device__ __forceinline__ void sh_vjp(double x, double y, double z, int deg, const float *sh, const float *d_color,
                                        float *d_sh, double *ddir) {
   float Y[kShCoeffs];
   Y[0] = kC0;
   const double xx = x * x, yy = y * y, zz = z * z;
+#pragma unroll
+  for (int b = 1; b < kShCoeffs; b++) Y[b] = 0.f;
   if (deg >= 1) { Y[1] = -kC1 * y; Y[2] = kC1 * z; Y[3] = -kC1 * x; }
   if (deg >= 2) {
-    Y[4] = kC20 * x * y; Y[5] = kC21 * y * z; Y[6] = kC22 * (2.f * zz - xx - yy);
+    Y[4] = kC20 * x * y; Y[5] = kC21 * y * z; Y[6] = kC22 * (2.0 * zz - xx - yy);
     Y[7] = kC23 * x * z; Y[8] = kC24 * (xx - yy);
   }
   if (deg >= 3) {
-    Y[9] = kC30 * y * (3.f * xx - yy); Y[10] = kC31 * x * y * z; Y[11] = kC32 * y * (4.f * zz - xx - yy);
-    Y[12] = kC33 * z * (2.f * zz - 3.f * xx - 3.f * yy); Y[13] = kC34 * x * (4.f * zz - xx - yy);
-    Y[14] = kC35 * z * (xx - yy); Y[15] = kC36 * x * (xx - 3.f * yy);
+    Y[9] = kC30 * y * (3.0 * xx - yy); Y[10] = kC31 * x * y * z; Y[11] = kC32 * y * (4.0 * zz - xx - yy);
+    Y[12] = kC33 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy); Y[13] = kC34 * x * (4.0 * zz - xx - yy);
+    Y[14] = kC35 * z * (xx - yy); Y[15] = kC36 * x * (xx - 3.0 * yy);
   }
   const int nb = (deg + 1) * (deg + 1);
-  float deff[3];
+  const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
+  float4 *dsh4 = reinterpret_cast<float4 *>(d_sh);
+  float raw[3] = {0.5f, 0.5f, 0.5f};
 #pragma unroll
-  for (int c = 0; c < 3; c++) {
-    float raw = 0.f;
+  for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
+    if (4 * q < 3 * nb) {
+      const float4 v = __ldg(sh4 + q);
+      const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int b = 0; b < kShCoeffs; b++)
-      if (b < nb) raw = fmaf(Y[b], sh[3 * b + c], raw);
-    deff[c] = (0.5f + raw) > 0.f ? d_color[c] : 0.f;
-  }
-  double v[kShCoeffs];
-#pragma unroll
-  for (int b = 0; b < kShCoeffs; b++) {
-    v[b] = 0.0;
-    if (b < nb) {
-#pragma unroll
-      for (int c = 0; c < 3; c++) {
-        d_sh[3 * b + c] += Y[b] * deff[c];
-        v[b] = fma((double)sh[3 * b + c], (double)deff[c], v[b]);
+      for (int r = 0; r < 4; r++) {
+        const int f = 4 * q + r, b = f / 3, c = f % 3;
+        if (b < nb) raw[c] = fmaf(Y[b], e[r], raw[c]);
       }
     }
   }
-  double gx = 0.0, gy = 0.0, gz = 0.0;
-  if (deg >= 1) { gy -= kC1 * v[1]; gz += kC1 * v[2]; gx -= kC1 * v[3]; }
-  if (deg >= 2) {
-    gx += kC20 * y * v[4]; gy += kC20 * x * v[4];
-    gy += kC21 * z * v[5]; gz += kC21 * y * v[5];
-    gx += -2.f * kC22 * x * v[6]; gy += -2.f * kC22 * y * v[6]; gz += 4.f * kC22 * z * v[6];
-    gx += kC23 * z * v[7]; gz += kC23 * x * v[7];
-    gx += 2.f * kC24 * x * v[8]; gy += -2.f * kC24 * y * v[8];
-  }
-  if (deg >= 3) {
-    gx += kC30 * 6.f * x * y * v[9]; gy += kC30 * 3.f * (xx - yy) * v[9];
-    gx += kC31 * y * z * v[10]; gy += kC31 * x * z * v[10]; gz += kC31 * x * y * v[10];
-    gx += -2.f * kC32 * x * y * v[11]; gy += kC32 * (4.f * zz - xx - 3.f * yy) * v[11]; gz += 8.f * kC32 * y * z * v[11];
-    gx += -6.f * kC33 * x * z * v[12]; gy += -6.f * kC33 * y * z * v[12];
-    gz += kC33 * (6.f * zz - 3.f * xx - 3.f * yy) * v[12];
-    gx += kC34 * (4.f * zz - 3.f * xx - yy) * v[13]; gy += -2.f * kC34 * x * y * v[13]; gz += 8.f * kC34 * x * z * v[13];
-    gx += 2.f * kC35 * x * z * v[14]; gy += -2.f * kC35 * y * z * v[14]; gz += kC35 * (xx - yy) * v[14];
-    gx += kC36 * 3.f * (xx - yy) * v[15]; gy += -6.f * kC36 * x * y * v[15];
+  float deff[3];
+#pragma unroll
+  for (int c = 0; c < 3; c++) deff[c] = raw[c] > 0.f ? d_color[c] : 0.f;
+  double gx = 0.0, gy = 0.0, gz = 0.0, vb = 0.0;
+#pragma unroll
+  for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
+    if (4 * q < 3 * nb) {
+      const float4 v = __ldg(sh4 + q);
+      const float e[4] = {v.x, v.y, v.z, v.w};
+      float4 d = dsh4[q];
+      float de[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const int f = 4 * q + r, b = f / 3, c = f % 3;
+        if (b < nb) {
+          de[r] += Y[b] * deff[c];
+          vb = fma((double)e[r], (double)deff[c], vb);
+          if (c == 2) {  // row b complete: its direction-gradient term
+            add_basis_grad(b, vb, x, y, z, gx, gy, gz);
+            vb = 0.0;
+          }
+        }
+      }
+      dsh4[q] = make_float4(de[0], de[1], de[2], de[3]);
+    }
   }
   ddir[0] = gx; ddir[1] = gy; ddir[2] = gz;
 }
 
 template <int MAXK>
-__global__ void __launch_bounds__(chain_threads<MAXK>()) chain_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(chain_threads<MAXK>(), 4) chain_kernel(ChainArgs a) {
   constexpr int kChainThreads = chain_threads<MAXK>();
   // per-thread slots for the dynamically indexed per-point arrays
   __shared__ double s_x[MAXK][kChainThreads], s_y[MAXK][kChainThreads];
@@ -193,21 +228,9 @@ __global__ void __launch_bounds__(chain_threads<MAXK>()) chain_kernel(ChainArgs 
   const double dist = sqrt(vx * vx + vy * vy + vz * vz);
   double dir[3] = {0.0, 0.0, 1.0};
   if (dist > 0.0) { dir[0] = vx / dist; dir[1] = vy / dist; dir[2] = vz / dist; }
-  float shf[kShCoeffs * 3], dsh[kShCoeffs * 3];
-  const float4 *shv = reinterpret_cast<const float4 *>(a.sh + i * kShCoeffs * 3);
-  float4 *dshv = reinterpret_cast<float4 *>(a.g.d_sh + i * kShCoeffs * 3);
-#pragma unroll
-  for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
-    const float4 v = __ldg(shv + q);
-    shf[4 * q] = v.x; shf[4 * q + 1] = v.y; shf[4 * q + 2] = v.z; shf[4 * q + 3] = v.w;
-    const float4 d = dshv[q];
-    dsh[4 * q] = d.x; dsh[4 * q + 1] = d.y; dsh[4 * q + 2] = d.z; dsh[4 * q + 3] = d.w;
-  }
   double ddirf[3];
-  sh_vjp(dir[0], dir[1], dir[2], a.sh_degree, shf, acc + A_DC, dsh, ddirf);
-#pragma unroll
-  for (int q = 0; q < kShCoeffs * 3 / 4; q++)
-    dshv[q] = make_float4(dsh[4 * q], dsh[4 * q + 1], dsh[4 * q + 2], dsh[4 * q + 3]);
+  sh_vjp(dir[0], dir[1], dir[2], a.sh_degree, a.sh + i * kShCoeffs * 3, acc + A_DC,
+         a.g.d_sh + i * kShCoeffs * 3, ddirf);
   const double dot = dir[0] * ddirf[0] + dir[1] * ddirf[1] + dir[2] * ddirf[2];
   double dcen[3];
 #pragma unroll

@@ -20,9 +20,9 @@ namespace cs {
 
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
-constexpr int kSortThreads = 256;
+constexpr int kSortThreads = 512;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
+constexpr int kSortItems = 8;
 constexpr int kSortChunk = kSortThreads * kSortItems;  // 4096 keys per chunk
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
@@ -82,7 +82,7 @@ struct PassArgs {
   uint32_t *chunk_counter;
 };
 
-// exclusive scan of one value per thread over a 256-thread block
+// exclusive scan of one value per thread over the block (threads >= 256 add 0)
 __device__ __forceinline__ uint32_t block_exclusive_scan256(uint32_t v, uint32_t *s_warp) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t inc = v;
@@ -115,7 +115,7 @@ constexpr size_t onesweep_dyn_smem() { return (size_t)kSortChunk * (sizeof(KeyT)
 // is first scattered into shared memory in digit order so that the global
 // writes come out as contiguous runs per digit (coalesced).
 template <typename KeyT>
-__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a) {
+__global__ void __launch_bounds__(kSortThreads, 2) onesweep_kernel(PassArgs<KeyT> a) {
   extern __shared__ __align__(16) unsigned char onesweep_dyn[];
   KeyT *s_keys = reinterpret_cast<KeyT *>(onesweep_dyn);
   uint32_t *s_vals = reinterpret_cast<uint32_t *>(onesweep_dyn + sizeof(KeyT) * kSortChunk);
@@ -151,7 +151,13 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a
 #pragma unroll
   for (int i = 0; i < kSortItems; i++) {
     const uint32_t d = dig[i];
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    // lanes holding the same digit: AND of 8 bit ballots (cheaper than MATCH)
+    uint32_t peers = __ballot_sync(0xffffffffu, d < kRadix);
+#pragma unroll
+    for (int b = 0; b < kRadixBits; b++) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bal : ~bal;
+    }
     uint32_t prev = 0;
     if (d < kRadix) prev = s_hist[w][d];
     __syncwarp();
@@ -160,22 +166,28 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a
     rank[i] = prev + __popc(peers & lt_mask);
   }
   __syncthreads();
-  // digit t: exclusive offsets across warps and the chunk total
+  // digit t (t < 256): exclusive offsets across warps and the chunk total
   const int d = t;
+  const bool owner = t < kRadix;
   uint32_t sum = 0;
+  if (owner) {
 #pragma unroll
-  for (int ww = 0; ww < kSortWarps; ww++) {
-    const uint32_t v = s_hist[ww][d];
-    s_hist[ww][d] = sum;
-    sum += v;
+    for (int ww = 0; ww < kSortWarps; ww++) {
+      const uint32_t v = s_hist[ww][d];
+      s_hist[ww][d] = sum;
+      sum += v;
+    }
   }
   // publish early, then resolve the prefix from the preceding chunks
   volatile uint32_t *lb = a.lookback;
-  if (chunk == 0) lb[d] = kFlagPrefix | sum;
-  else lb[chunk * kRadix + d] = kFlagAgg | sum;
-  s_dexcl[d] = block_exclusive_scan256(sum, s_warp);
+  if (owner) {
+    if (chunk == 0) lb[d] = kFlagPrefix | sum;
+    else lb[chunk * kRadix + d] = kFlagAgg | sum;
+  }
+  const uint32_t dex = block_exclusive_scan256(sum, s_warp);
+  if (owner) s_dexcl[d] = dex;
   uint32_t excl = 0;
-  if (chunk > 0) {
+  if (owner && chunk > 0) {
     // windowed decoupled look-back: kLookback independent loads per round, so
     // the walk over not-yet-resolved predecessors costs one L2 round trip per
     // kLookback chunks instead of one per chunk
@@ -200,7 +212,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(PassArgs<KeyT> a
     }
     lb[chunk * kRadix + d] = kFlagPrefix | (excl + sum);
   }
-  s_base[d] = a.offsets[d] + excl;
+  if (owner) s_base[d] = a.offsets[d] + excl;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; i++) {
