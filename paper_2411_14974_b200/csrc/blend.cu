@@ -22,8 +22,6 @@
 
 namespace cs {
 
-constexpr int kBlendThreads = 256;  // 8 warps; warp w owns the 8x4 pixel block of tile_pixel()
-
 struct BlendArgs {
   const float *records;
   const uint32_t *pair_ids;
@@ -161,6 +159,7 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK> &sm, const float *re
   constexpr int RB = Rec<MAXK>::kFloats * 4;
   const int lane = threadIdx.x & 31;
   int issued = 0;
+  bool stopped = false;
   for (int b = 0; b < nbatch; b++) {
     const int s = b % kStages, u = b / kStages;
     if (u > 0) mbar_wait(&sm.empty[s], (u - 1) & 1);
@@ -169,6 +168,7 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK> &sm, const float *re
         *reinterpret_cast<volatile int *>(&sm.stop) = 1;
         mbar_arrive(&sm.full[s]);          // wake consumers waiting on batch b; they see stop
       }
+      stopped = true;
       break;
     }
     uint32_t first, count;
@@ -184,8 +184,13 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK> &sm, const float *re
     if (lane < (int)count) tma_bulk_g2s(&sm.rec[s][lane][0], records + (size_t)id * Rec<MAXK>::kFloats, RB, &sm.full[s]);
     issued = b + 1;
   }
-  // drain: no bulk copy may still target this CTA's shared memory at exit
-  for (int b = max(0, issued - kStages); b < issued; b++) mbar_wait(&sm.full[b % kStages], (b / kStages) & 1);
+  // drain: no bulk copy may still target this CTA's shared memory at exit.
+  // After a stop at batch `issued` the stop arrival completed the next phase
+  // of stage issued % kStages, whose previous batch was already consumed
+  // (the empty wait above), so that batch must not be waited on again (its
+  // parity would now name a phase that has not completed).
+  const int lo = stopped ? issued - kStages + 1 : issued - kStages;
+  for (int b = max(0, lo); b < issued; b++) mbar_wait(&sm.full[b % kStages], (b / kStages) & 1);
 }
 
 template <int MAXK>
