@@ -64,11 +64,13 @@ class CsError(RuntimeError):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load (once) and type the library.  Raises if it is absent."""
+def load(path: str = None):
+    """Load (once) and type the library.  Raises if it is absent.  CS_LIB_PATH
+    overrides the in-tree library (used to A/B kernel variants)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("CS_LIB_PATH") or LIB_PATH
     if not os.path.exists(path):
         raise CsError(f"{path} is missing: run `python -m paper_2411_14974_b200.build` "
                       "(there is no CPU fallback)")

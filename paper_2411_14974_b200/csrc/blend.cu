@@ -6,7 +6,7 @@
 //   z_j = delta_s L_j, phi = LSE(z), I = sigmoid(-sigma_s phi),
 //   alpha = min(o I, ALPHA_MAX); blend iff (T >= floor if floor > 0) and
 //   alpha >= cutoff: C += T alpha c, W += T alpha, T *= 1 - alpha, count++.
-// Evaluated in base 2: z2 = log2(e) z, phi2 = max z2 + log2 sum 2^(z2-max),
+// Evaluated in base 2: z2 = log2(e) z, phi2 = log2 sum 2^z2,
 // I = 1 / (1 + 2^(sigma_s phi2)); 1 - alpha = (1-o) + o (1-I) avoids the
 // fp32 cancellation near ALPHA_MAX.  Pixels whose T fell below the floor
 // stop; the block leaves a tile when all its pixels stopped.
@@ -18,6 +18,10 @@
 // sum dL*(q-a), sum dL).  The warp reduces those 32 values with a
 // transpose-reduce (31 shuffles, lane L ends with value L) and issues a single
 // vector of global float atomics.
+//
+// The hull line count of a candidate is uniform across the warp (every lane
+// evaluates the same candidate), so the evaluation is dispatched to a
+// specialisation per count (no per-line predicates).
 #include "common.cuh"
 
 namespace cs {
@@ -43,83 +47,99 @@ struct BlendArgs {
 };
 
 struct Eval {
-  float I, J, alpha, alpha_raw, phi2, m, s;
+  float I, J, alpha, alpha_raw, phi2;
 };
 
-__device__ __forceinline__ bool in_box(uint32_t bx, uint32_t by, int px, int py) {
-  return px >= (int)(bx & 0xffffu) && px < (int)(bx >> 16) && py >= (int)(by & 0xffffu) && py < (int)(by >> 16);
+// Warp block [rx0, rx0+8) x [ry0, ry0+4) vs a candidate's half-open bbox.
+__device__ __forceinline__ bool box_overlaps(int4 b, int rx0, int ry0) {
+  return b.x < rx0 + 8 && b.y > rx0 && b.z < ry0 + 4 && b.w > ry0;
+}
+__device__ __forceinline__ bool in_box(int4 b, int px, int py) {
+  return px >= b.x && px < b.y && py >= b.z && py < b.w;
+}
+__device__ __forceinline__ int4 rec_bbox(const float4 *rec) {
+  const float4 v = rec[R_BBOX / 4];
+  return make_int4(__float_as_int(v.x), __float_as_int(v.y), __float_as_int(v.z), __float_as_int(v.w));
 }
 
-// Does the bbox of candidate id overlap the warp's 8x4 pixel block?
-__device__ __forceinline__ uint2 load_bbox(const float *records, uint32_t id, int rf) {
-  return __ldg(reinterpret_cast<const uint2 *>(records + (size_t)id * rf + R_BBX));
-}
-__device__ __forceinline__ bool box_overlaps(uint2 b, int rx0, int ry0) {
-  return (int)(b.x & 0xffffu) < rx0 + 8 && (int)(b.x >> 16) > rx0 && (int)(b.y & 0xffffu) < ry0 + 4 &&
-         (int)(b.y >> 16) > ry0;
-}
-
-// Candidate record held in registers (loaded with warp-broadcast 128-bit
-// loads: every lane reads the same address, one request per load).
-template <int MAXK>
-struct RecRegs {
-  float4 h0, h1, h2;            // ax ay sigma o | r g b depth | 1-o dls nl -
-  float ln[3 * MAXK];           // A_j B_j C_j
-  __device__ __forceinline__ void load(const float *records, uint32_t id) {
-    const float4 *r = reinterpret_cast<const float4 *>(records + (size_t)id * Rec<MAXK>::kFloats);
-    h0 = __ldg(r);
-    h1 = __ldg(r + 1);
-    h2 = __ldg(r + 2);
+// Line coefficients of a candidate record in shared memory.  NL > 0: the
+// warp-uniform line count is a compile-time constant (the hot path, one
+// instantiation per count); NL == 0: runtime count nl <= MAXK (fallback).
+template <int NL, int MAXK>
+struct LineSet {
+  static constexpr int kN = NL > 0 ? NL : MAXK;
+  float c[3 * kN];
+  int nl;
+  __device__ __forceinline__ void load(const float4 *rec, int nl_rt) {
+    nl = NL > 0 ? NL : nl_rt;
 #pragma unroll
-    for (int q = 0; q < 3 * MAXK / 4; q++) {
-      const float4 v = __ldg(r + R_HEADER / 4 + q);
-      ln[4 * q] = v.x; ln[4 * q + 1] = v.y; ln[4 * q + 2] = v.z; ln[4 * q + 3] = v.w;
+    for (int q = 0; q < (3 * kN + 3) / 4; q++) {
+      const float4 v = rec[R_HEADER / 4 + q];
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+        if (4 * q + r < 3 * kN) c[4 * q + r] = e[r];
     }
   }
-  __device__ __forceinline__ void load_smem(const float4 *r) {
-    h0 = r[0];
-    h1 = r[1];
-    h2 = r[2];
-#pragma unroll
-    for (int q = 0; q < 3 * MAXK / 4; q++) {
-      const float4 v = r[R_HEADER / 4 + q];
-      ln[4 * q] = v.x; ln[4 * q + 1] = v.y; ln[4 * q + 2] = v.z; ln[4 * q + 3] = v.w;
-    }
-  }
-  __device__ __forceinline__ int nl() const { return __float_as_int(h2.z); }
+  __device__ __forceinline__ bool has(int l) const { return NL > 0 ? true : l < nl; }
 };
 
-// smooth field of a candidate at anchor-relative pixel (dx, dy):
-// z2_j = A_j dx + B_j dy + C_j, phi2 = max z2 + log2 sum 2^(z2 - max),
-// I = 1 / (1 + 2^(sigma_s phi2)), alpha = min(o I, ALPHA_MAX)
-// (field.py:51-72, rasterize.py:147-153 in log2 units).
-template <int MAXK>
-__device__ __forceinline__ Eval eval_field(const RecRegs<MAXK> &r, float dx, float dy, float *z) {
-  Eval e;
-  const int nl = r.nl();
-  float m = -INFINITY;
-#pragma unroll
-  for (int l = 0; l < MAXK; l++) {
-    if (l < nl) {
-      z[l] = fmaf(r.ln[3 * l], dx, fmaf(r.ln[3 * l + 1], dy, r.ln[3 * l + 2]));
-      m = fmaxf(m, z[l]);
-    }
-  }
+// Smooth field of a candidate at anchor-relative pixel (dx, dy), in log2
+// units (field.py:51-72, rasterize.py:147-153):
+//   z_l = A_l dx + B_l dy + C_l, phi2 = log2 sum 2^z_l,
+//   I = 1 / (1 + 2^(sigma_s phi2)), alpha = min(o I, ALPHA_MAX).
+// The sum is formed without the max shift (4 instructions per line); when it
+// leaves [2^-100, 2^100] (denormal flush / overflow would bias phi) it is
+// recomputed with the shift.  Softmax weights are w_l = 2^(z_l - phi2).
+#ifdef CS_BWD_ACCURATE
+__device__ __forceinline__ float acc_ex2(float x) { return exp2f(x); }
+__device__ __forceinline__ float acc_lg2(float x) { return log2f(x); }
+__device__ __forceinline__ float acc_rcp(float x) { return 1.f / x; }
+#else
+__device__ __forceinline__ float acc_ex2(float x) { return ex2(x); }
+__device__ __forceinline__ float acc_lg2(float x) { return lg2(x); }
+__device__ __forceinline__ float acc_rcp(float x) { return rcp(x); }
+#endif
+
+template <int NL, int MAXK, bool ACC = false>
+__device__ __forceinline__ Eval eval_field(const LineSet<NL, MAXK> &L, float sig, float o, float dx, float dy,
+                                           float (&z)[LineSet<NL, MAXK>::kN]) {
+  constexpr int N = LineSet<NL, MAXK>::kN;
   float s = 0.f;
 #pragma unroll
-  for (int l = 0; l < MAXK; l++)
-    if (l < nl) s += ex2(z[l] - m);
-  const float phi2 = m + lg2(s);
-  const float u = ex2(r.h0.z * phi2);
-  e.I = rcp(1.f + u);
+  for (int l = 0; l < N; l++) {
+    if (L.has(l)) {
+      z[l] = fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]));
+      s += ACC ? acc_ex2(z[l]) : ex2(z[l]);
+    }
+  }
+  float phi2;
+#ifdef CS_MAX_SHIFT
+  if (false) {
+#else
+  if (s >= 0x1p-100f && s <= 0x1p100f) {
+#endif
+    phi2 = ACC ? acc_lg2(s) : lg2(s);
+  } else {
+    float m = -INFINITY;
+#pragma unroll
+    for (int l = 0; l < N; l++)
+      if (L.has(l)) m = fmaxf(m, z[l]);
+    float s2 = 0.f;
+#pragma unroll
+    for (int l = 0; l < N; l++)
+      if (L.has(l)) s2 += ACC ? acc_ex2(z[l] - m) : ex2(z[l] - m);
+    phi2 = m + (ACC ? acc_lg2(s2) : lg2(s2));
+  }
+  Eval e;
+  const float u = ACC ? acc_ex2(sig * phi2) : ex2(sig * phi2);
+  e.I = ACC ? acc_rcp(1.f + u) : rcp(1.f + u);
   // 1 - I without cancellation: u*I while I >= 1/2, else 1 - I (also covers
   // u so large that I flushes to zero)
   e.J = u > 1.f ? 1.f - e.I : u * e.I;
-  e.alpha_raw = r.h0.w * e.I;
+  e.alpha_raw = o * e.I;
   e.alpha = fminf(e.alpha_raw, (float)kAlphaMaxD);
   e.phi2 = phi2;
-  e.m = m;
-  e.s = s;
   return e;
 }
 
@@ -133,6 +153,9 @@ __device__ __forceinline__ Eval eval_field(const RecRegs<MAXK> &r, float dx, flo
 // no block-wide barrier, a slow warp never stalls a fast one by more than the
 // ring depth.  When every consumer is done (all pixels terminated) the
 // producer stops streaming and releases the waiting consumers with `stop`.
+// Forward only: consumers OR the stage's candidates that blended somewhere
+// into `vis`; the producer writes visible[] for them when it recycles the
+// stage (rasterize.py:203 `visible[idx] = True`).
 constexpr int kConsumers = 8;
 constexpr int kPipeThreads = 32 * (kConsumers + 1);
 constexpr int kStages = 4;
@@ -142,6 +165,7 @@ template <int MAXK>
 struct PipeSmem {
   float4 rec[kStages][kStageCands][Rec<MAXK>::kFloats / 4];
   uint32_t id[kStages][kStageCands];
+  uint32_t vis[kStages];
   uint64_t full[kStages];
   uint64_t empty[kStages];
   int ndone;
@@ -152,21 +176,36 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+template <int MAXK>
+__device__ __forceinline__ void flush_visible(PipeSmem<MAXK> &sm, int s, uint8_t *visible) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t vm = *reinterpret_cast<volatile uint32_t *>(&sm.vis[s]);
+  if (visible && ((vm >> lane) & 1u)) visible[sm.id[s][lane]] = 1;
+  __syncwarp();
+  if (lane == 0) *reinterpret_cast<volatile uint32_t *>(&sm.vis[s]) = 0u;
+  __syncwarp();
+}
+
 // Producer warp: batch b covers pair indices first(b) .. first(b)+count(b)-1.
 template <int MAXK, typename Batch>
 __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK> &sm, const float *records, const uint32_t *pair_ids,
-                                             int nbatch, Batch batch, bool allow_stop) {
+                                             int nbatch, Batch batch, bool forward, uint8_t *visible) {
   constexpr int RB = Rec<MAXK>::kFloats * 4;
   const int lane = threadIdx.x & 31;
   int issued = 0;
   bool stopped = false;
   for (int b = 0; b < nbatch; b++) {
     const int s = b % kStages, u = b / kStages;
-    if (u > 0) mbar_wait(&sm.empty[s], (u - 1) & 1);
-    if (allow_stop && *reinterpret_cast<volatile int *>(&sm.ndone) == kConsumers) {
+    if (u > 0) {
+      mbar_wait(&sm.empty[s], (u - 1) & 1);  // batch b - kStages released by every consumer
+      if (forward) flush_visible(sm, s, visible);
+    }
+    if (forward && *reinterpret_cast<volatile int *>(&sm.ndone) == kConsumers) {
       if (lane == 0) {
-        *reinterpret_cast<volatile int *>(&sm.stop) = 1;
-        mbar_arrive(&sm.full[s]);          // wake consumers waiting on batch b; they see stop
+        // stop = b + 1: consumers leave at batch b.  Consumers still behind
+        // (done warps lag) keep releasing the issued batches < b normally.
+        *reinterpret_cast<volatile int *>(&sm.stop) = b + 1;
+        mbar_arrive(&sm.full[s]);          // wake consumers waiting on batch b
       }
       stopped = true;
       break;
@@ -184,13 +223,15 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK> &sm, const float *re
     if (lane < (int)count) tma_bulk_g2s(&sm.rec[s][lane][0], records + (size_t)id * Rec<MAXK>::kFloats, RB, &sm.full[s]);
     issued = b + 1;
   }
-  // drain: no bulk copy may still target this CTA's shared memory at exit.
-  // After a stop at batch `issued` the stop arrival completed the next phase
-  // of stage issued % kStages, whose previous batch was already consumed
-  // (the empty wait above), so that batch must not be waited on again (its
-  // parity would now name a phase that has not completed).
+  // drain: wait until the consumers released the last issued batches (their
+  // bulk copies have landed, so nothing targets this CTA's shared memory
+  // after exit) and publish their visibility.  After a stop, batch
+  // issued - kStages was already waited on and flushed above.
   const int lo = stopped ? issued - kStages + 1 : issued - kStages;
-  for (int b = max(0, lo); b < issued; b++) mbar_wait(&sm.full[b % kStages], (b / kStages) & 1);
+  for (int b = max(0, lo); b < issued; b++) {
+    mbar_wait(&sm.empty[b % kStages], (b / kStages) & 1);
+    if (forward) flush_visible(sm, b % kStages, visible);
+  }
 }
 
 template <int MAXK>
@@ -199,6 +240,7 @@ __device__ __forceinline__ void pipe_init(PipeSmem<MAXK> &sm) {
     for (int s = 0; s < kStages; s++) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kConsumers);
+      sm.vis[s] = 0u;
     }
     sm.ndone = 0;
     sm.stop = 0;
@@ -207,10 +249,42 @@ __device__ __forceinline__ void pipe_init(PipeSmem<MAXK> &sm) {
   __syncthreads();
 }
 
+// Per-pixel forward state (rasterize.py:178-204).
+struct FwdPixel {
+  float T, C0, C1, C2, W, D;
+  int last, nblend;
+  bool done;
+};
+
+// One candidate at one pixel: evaluate, and blend iff (T >= floor if floor >
+// 0) and alpha >= cutoff (rasterize.py:194-204).  Returns whether it blended.
+template <int NL, int MAXK>
+__device__ __forceinline__ bool fwd_candidate(const float4 *rec, float qx, float qy, float cutoff, float floor_,
+                                              bool use_floor, int pos, FwdPixel &P, unsigned &n_lines) {
+  const float4 h0 = rec[0], h2 = rec[2];
+  LineSet<NL, MAXK> L;
+  L.load(rec, __float_as_int(h2.z));
+  float z[LineSet<NL, MAXK>::kN];
+  const Eval e = eval_field<NL, MAXK>(L, h0.z, h0.w, qx - h0.x, qy - h0.y, z);
+  n_lines += L.nl;
+  if (!(e.alpha >= cutoff)) return false;
+  const float4 h1 = rec[1];
+  const float w = P.T * e.alpha;
+  P.C0 = fmaf(w, h1.x, P.C0);
+  P.C1 = fmaf(w, h1.y, P.C1);
+  P.C2 = fmaf(w, h1.z, P.C2);
+  P.W += w;
+  P.D = fmaf(w, h1.w, P.D);
+  P.T *= fmaxf(fmaf(h0.w, e.J, h2.x), 1e-6f);   // 1 - alpha = (1-o) + o (1-I)
+  P.nblend++;
+  P.last = pos;
+  if (use_floor && P.T < floor_) P.done = true;
+  return true;
+}
+
 // Forward blend (rasterize.py:178-209), one 16x16 tile per block.
 template <int MAXK>
-__global__ void __launch_bounds__(kPipeThreads) forward_kernel(BlendArgs a) {
-  constexpr int Q = Rec<MAXK>::kFloats / 4;
+__global__ void __launch_bounds__(kPipeThreads, 4) forward_kernel(BlendArgs a) {
   __shared__ PipeSmem<MAXK> sm;
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -224,7 +298,7 @@ __global__ void __launch_bounds__(kPipeThreads) forward_kernel(BlendArgs a) {
                        [&](int b, uint32_t &first, uint32_t &count) {
                          first = range.x + (uint32_t)b * kStageCands;
                          count = min((uint32_t)kStageCands, range.y - first);
-                       }, true);
+                       }, true, a.visible);
   } else {
     int lx, ly;
     tile_pixel(threadIdx.x, lx, ly);
@@ -232,76 +306,71 @@ __global__ void __launch_bounds__(kPipeThreads) forward_kernel(BlendArgs a) {
     const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2);
     const bool inside = px < a.width && py < a.height;
     const float qx = px + 0.5f, qy = py + 0.5f;
-    float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Wsum = 0.f, D = 0.f;
-    int last = -1;
-    bool done = !inside;
-    bool warp_done = __all_sync(0xffffffffu, done);
+    FwdPixel P;
+    P.T = 1.f; P.C0 = P.C1 = P.C2 = P.W = P.D = 0.f;
+    P.last = -1; P.nblend = 0;
+    P.done = !inside;
+    bool warp_done = __all_sync(0xffffffffu, P.done);
     if (warp_done && lane == 0) atomicAdd(&sm.ndone, 1);
     const bool use_floor = a.floor > 0.f;
-    float z[MAXK];
-    RecRegs<MAXK> r;
     for (int b = 0; b < nbatch; b++) {
       const int s = b % kStages;
       mbar_wait(&sm.full[s], (b / kStages) & 1);
-      if (*reinterpret_cast<volatile int *>(&sm.stop)) break;
+      if (*reinterpret_cast<volatile int *>(&sm.stop) == b + 1) break;
       if (!warp_done) {
         const uint32_t first = range.x + (uint32_t)b * kStageCands;
         const int count = (int)min((uint32_t)kStageCands, range.y - first);
         bool hit = false;
-        if (lane < count) {
-          const float4 bb = sm.rec[s][lane][R_BBX / 4];
-          hit = box_overlaps(make_uint2(__float_as_uint(bb.x), __float_as_uint(bb.y)), rx0, ry0);
-        }
+        if (lane < count) hit = box_overlaps(rec_bbox(sm.rec[s][lane]), rx0, ry0);
         uint32_t m = __ballot_sync(0xffffffffu, hit);
+        uint32_t vis = 0;
         while (m) {
           const int j = __ffs(m) - 1;
           m &= m - 1;
-          r.load_smem(sm.rec[s][j]);
-          const float4 bb = sm.rec[s][j][R_BBX / 4];
+          const float4 *rec = sm.rec[s][j];
           bool blended = false;
-          if (!done && in_box(__float_as_uint(bb.x), __float_as_uint(bb.y), px, py)) {
-            const Eval e = eval_field<MAXK>(r, qx - r.h0.x, qy - r.h0.y, z);
+          if (!P.done && in_box(rec_bbox(rec), px, py)) {
             n_eval++;
-            n_lines += r.nl();
-            if (e.alpha >= a.cutoff) {
-              const float w = T * e.alpha;
-              C0 = fmaf(w, r.h1.x, C0);
-              C1 = fmaf(w, r.h1.y, C1);
-              C2 = fmaf(w, r.h1.z, C2);
-              Wsum += w;
-              D = fmaf(w, r.h1.w, D);
-              T *= fmaxf(fmaf(r.h0.w, e.J, r.h2.x), 1e-6f);
-              n_blend++;
-              last = (int)(first + j);
-              blended = true;
-              if (use_floor && T < a.floor) done = true;
+            const int pos = (int)first + j;
+            if (MAXK == 8) {
+              switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
+                case 5: blended = fwd_candidate<5, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                case 6: blended = fwd_candidate<6, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                case 4: blended = fwd_candidate<4, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                case 3: blended = fwd_candidate<3, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                default: blended = fwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+              }
+            } else {
+              blended = fwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
             }
           }
           if (__any_sync(0xffffffffu, blended)) {
-            if (lane == 0 && a.visible) a.visible[sm.id[s][j]] = 1;
-            if (__all_sync(0xffffffffu, done)) {
+            vis |= 1u << j;
+            if (__all_sync(0xffffffffu, P.done)) {
               warp_done = true;
               if (lane == 0) atomicAdd(&sm.ndone, 1);
               break;
             }
           }
         }
+        if (lane == 0 && vis) atomicOr(&sm.vis[s], vis);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
+    n_blend = (unsigned)P.nblend;
     if (inside) {
       const size_t p = (size_t)py * a.width + px;
-      const float v0 = fmaf(T, a.bg[0], C0), v1 = fmaf(T, a.bg[1], C1), v2 = fmaf(T, a.bg[2], C2);
+      const float v0 = fmaf(P.T, a.bg[0], P.C0), v1 = fmaf(P.T, a.bg[1], P.C1), v2 = fmaf(P.T, a.bg[2], P.C2);
       a.image[3 * p] = fminf(fmaxf(v0, 0.f), 1.f);
       a.image[3 * p + 1] = fminf(fmaxf(v1, 0.f), 1.f);
       a.image[3 * p + 2] = fminf(fmaxf(v2, 0.f), 1.f);
-      a.final_T[p] = T;
-      a.pixel_T[p] = T;
-      a.weight_sum[p] = Wsum;
-      a.count[p] = (int)n_blend;
-      if (a.depth) a.depth[p] = D;
-      a.pixel_last[p] = last;
+      a.final_T[p] = P.T;
+      a.pixel_T[p] = P.T;
+      a.weight_sum[p] = P.W;
+      a.count[p] = P.nblend;
+      if (a.depth) a.depth[p] = P.D;
+      a.pixel_last[p] = P.last;
       a.pixel_clamp[p] = (uint8_t)((v0 >= 0.f && v0 <= 1.f) | ((v1 >= 0.f && v1 <= 1.f) << 1) |
                                    ((v2 >= 0.f && v2 <= 1.f) << 2));
     }
@@ -327,6 +396,70 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
   return v[0];
 }
 
+// Per-pixel backward state (backward.py:133-205).
+struct BwdPixel {
+  float T, g0, g1, g2, S0, S1, S2;
+  int last;
+};
+
+// One candidate at one pixel of the reverse walk: recompute the field,
+// reconstruct T_prev = T / (1 - alpha), and write the pixel's 32 screen-space
+// gradient terms into v (left zero when it did not blend).  Returns whether
+// it did.
+template <int NL, int MAXK, int VN>
+__device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float qy, float cutoff, BwdPixel &P,
+                                              float (&v)[VN], unsigned &n_lines) {
+  const float4 h0 = rec[0], h2 = rec[2];
+  LineSet<NL, MAXK> L;
+  L.load(rec, __float_as_int(h2.z));
+  constexpr int N = LineSet<NL, MAXK>::kN;
+  float z[N];
+  const float dx = qx - h0.x, dy = qy - h0.y;
+  const float o = h0.w, sig = h0.z, dls = h2.y, inv_dls = h2.w;
+  const Eval e = eval_field<NL, MAXK, true>(L, sig, o, dx, dy, z);
+  n_lines += L.nl;
+  if (!(e.alpha >= cutoff)) return false;
+  const float4 h1 = rec[1];
+  const float om = fmaxf(fmaf(o, e.J, h2.x), 1e-6f);  // 1 - alpha
+#ifdef CS_EXACT_RECIP
+  const float rom = 1.f / om;
+#else
+  const float rom = rcp(om);
+#endif
+  const float Tp = P.T * rom;
+  const float w = Tp * e.alpha;
+  const float c0 = h1.x, c1 = h1.y, c2 = h1.z;
+  v[A_DC] = P.g0 * w;
+  v[A_DC + 1] = P.g1 * w;
+  v[A_DC + 2] = P.g2 * w;
+  float dA = P.g0 * (Tp * c0 - P.S0 * rom) + P.g1 * (Tp * c1 - P.S1 * rom) + P.g2 * (Tp * c2 - P.S2 * rom);
+  if (!(e.alpha_raw < (float)kAlphaMaxD)) dA = 0.f;
+  v[A_DOEFF] = dA * e.I;
+  const float dI = dA * o;
+  const float slope = e.I * e.J;
+  const float dphi = -sig * slope * dI;          // d loss / d phi (natural units)
+  v[A_DSIG] = -(e.phi2 * kLn2) * slope * dI;
+  const float dscale = dphi * (dls * kLn2);      // dphi * delta_s
+  float wz = 0.f;
+#pragma unroll
+  for (int l = 0; l < N; l++) {
+    if (L.has(l)) {
+      const float wl = acc_ex2(z[l] - e.phi2);         // softmax_over_lines (field.py:62-67)
+      wz = fmaf(wl, z[l], wz);
+      const float dL = dscale * wl;
+      v[A_LINES + 3 * l] = dL * dx;
+      v[A_LINES + 3 * l + 1] = dL * dy;
+      v[A_LINES + 3 * l + 2] = dL;
+    }
+  }
+  v[A_DDEL] = dphi * wz * inv_dls;               // dphi * sum_l w_l L_l
+  P.S0 = fmaf(w, c0, P.S0);
+  P.S1 = fmaf(w, c1, P.S1);
+  P.S2 = fmaf(w, c2, P.S2);
+  P.T = Tp;
+  return true;
+}
+
 // Backward blend (backward.py:110-205): the producer streams the tile list
 // back to front from the block's largest `last`; each consumer warp culls a
 // stage by ballot, reconstructs T_prev = T / (1 - alpha) per pixel and
@@ -347,21 +480,22 @@ __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) 
   if (warp < kConsumers) tile_pixel(threadIdx.x, lx, ly);
   const int px = tx * kTile + lx, py = ty * kTile + ly;
   const bool inside = warp < kConsumers && px < a.width && py < a.height;
-  float T = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
-  int last = -1;
+  BwdPixel P;
+  P.T = 1.f; P.g0 = P.g1 = P.g2 = P.S0 = P.S1 = P.S2 = 0.f;
+  P.last = -1;
   if (inside) {
     const size_t p = (size_t)py * a.width + px;
-    T = a.pixel_T[p];
-    last = a.pixel_last[p];
+    P.T = a.pixel_T[p];
+    P.last = a.pixel_last[p];
     const uint32_t cm = a.pixel_clamp[p];
-    g0 = (cm & 1) ? a.d_image[3 * p] : 0.f;
-    g1 = (cm & 2) ? a.d_image[3 * p + 1] : 0.f;
-    g2 = (cm & 4) ? a.d_image[3 * p + 2] : 0.f;
-    S0 = T * a.bg[0];
-    S1 = T * a.bg[1];
-    S2 = T * a.bg[2];
+    P.g0 = (cm & 1) ? a.d_image[3 * p] : 0.f;
+    P.g1 = (cm & 2) ? a.d_image[3 * p + 1] : 0.f;
+    P.g2 = (cm & 4) ? a.d_image[3 * p + 2] : 0.f;
+    P.S0 = P.T * a.bg[0];
+    P.S1 = P.T * a.bg[1];
+    P.S2 = P.T * a.bg[2];
   }
-  const int warp_last = __reduce_max_sync(0xffffffffu, last);
+  const int warp_last = __reduce_max_sync(0xffffffffu, P.last);
   if (warp < kConsumers && lane == 0) s_last[warp] = warp_last;
   pipe_init(sm);  // (its __syncthreads also publishes s_last)
   int block_last = s_last[0];
@@ -378,12 +512,10 @@ __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) 
   };
   unsigned n_eval = 0, n_lines = 0;
   if (warp == kConsumers) {
-    pipe_produce<MAXK>(sm, a.records, a.pair_ids, nbatch, batch, false);
+    pipe_produce<MAXK>(sm, a.records, a.pair_ids, nbatch, batch, false, nullptr);
   } else {
     const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2);
     const float qx = px + 0.5f, qy = py + 0.5f;
-    float z[MAXK];
-    RecRegs<MAXK> r;
     for (int b = 0; b < nbatch; b++) {
       const int s = b % kStages;
       mbar_wait(&sm.full[s], (b / kStages) & 1);
@@ -391,63 +523,28 @@ __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) 
       batch(b, first, count);
       if ((int)first <= warp_last) {
         bool hit = false;
-        if (lane < (int)count && (int)(first + lane) <= warp_last) {
-          const float4 bb = sm.rec[s][lane][R_BBX / 4];
-          hit = box_overlaps(make_uint2(__float_as_uint(bb.x), __float_as_uint(bb.y)), rx0, ry0);
-        }
+        if (lane < (int)count && (int)(first + lane) <= warp_last)
+          hit = box_overlaps(rec_bbox(sm.rec[s][lane]), rx0, ry0);
         uint32_t m = __ballot_sync(0xffffffffu, hit);
         while (m) {
           const int j = 31 - __clz(m);   // back to front
           m &= ~(1u << j);
-          const int e_idx = (int)first + j;
-          r.load_smem(sm.rec[s][j]);
-          const float4 bb = sm.rec[s][j][R_BBX / 4];
-          bool contrib = e_idx <= last && in_box(__float_as_uint(bb.x), __float_as_uint(bb.y), px, py);
+          const float4 *rec = sm.rec[s][j];
           float v[NG * 32];
 #pragma unroll
           for (int f = 0; f < NG * 32; f++) v[f] = 0.f;
-          if (contrib) {
-            const float dx = qx - r.h0.x, dy = qy - r.h0.y;
-            const Eval e = eval_field<MAXK>(r, dx, dy, z);
+          bool contrib = false;
+          if ((int)first + j <= P.last && in_box(rec_bbox(rec), px, py)) {
             n_eval++;
-            n_lines += r.nl();
-            contrib = e.alpha >= a.cutoff;
-            if (contrib) {
-              const float o = r.h0.w, sig = r.h0.z, dls = r.h2.y;
-              const float om = fmaxf(fmaf(o, e.J, r.h2.x), 1e-6f);
-              const float rom = 1.f / om;
-              const float Tp = T * rom;
-              const float w = Tp * e.alpha;
-              const float c0 = r.h1.x, c1 = r.h1.y, c2 = r.h1.z;
-              v[A_DC] = g0 * w;
-              v[A_DC + 1] = g1 * w;
-              v[A_DC + 2] = g2 * w;
-              float dA = g0 * (Tp * c0 - S0 * rom) + g1 * (Tp * c1 - S1 * rom) + g2 * (Tp * c2 - S2 * rom);
-              if (!(e.alpha_raw < (float)kAlphaMaxD)) dA = 0.f;
-              v[A_DOEFF] = dA * e.I;
-              const float dI = dA * o;
-              const float slope = e.I * e.J;
-              const float dphi = -sig * slope * dI;         // d loss / d phi (natural units)
-              v[A_DSIG] = -(e.phi2 * kLn2) * slope * dI;
-              const float rs = 1.f / e.s;
-              const int nl = r.nl();
-              float wz = 0.f;
-#pragma unroll
-              for (int l = 0; l < MAXK; l++) {
-                if (l < nl) {
-                  const float wl = ex2(z[l] - e.m) * rs;    // softmax_over_lines (field.py:62-67)
-                  wz = fmaf(wl, z[l], wz);
-                  const float dL = dphi * (dls * kLn2) * wl;  // dphi * delta_s * w_l
-                  v[A_LINES + 3 * l] = dL * dx;
-                  v[A_LINES + 3 * l + 1] = dL * dy;
-                  v[A_LINES + 3 * l + 2] = dL;
-                }
+            if (MAXK == 8) {
+              switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
+                case 5: contrib = bwd_candidate<5, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines); break;
+                case 6: contrib = bwd_candidate<6, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines); break;
+                case 4: contrib = bwd_candidate<4, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines); break;
+                default: contrib = bwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines); break;
               }
-              v[A_DDEL] = dphi * wz / dls;                   // dphi * sum_l w_l L_l
-              S0 = fmaf(w, c0, S0);
-              S1 = fmaf(w, c1, S1);
-              S2 = fmaf(w, c2, S2);
-              T = Tp;
+            } else {
+              contrib = bwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines);
             }
           }
           if (__any_sync(0xffffffffu, contrib)) {

@@ -1,7 +1,8 @@
 // K4b: per-convex gradient chain (backward.py:215-282), one thread per convex.
 //
 // Turns the screen-space accumulators of the backward blend into gradients of
-// the raw parameters, in float64:
+// the raw parameters (reciprocals instead of divisions; float32 unless
+// built with -DCS_CHAIN_F64):
 //   hull lines -> hull vertices (normalisation Jacobian, backward.py:231-246)
 //   -> projection Jacobian -> 3-D points (backward.py:248-261)
 //   delta/sigma activations + the depth path (backward.py:263-269)
@@ -38,31 +39,31 @@ template <int MAXK> __host__ __device__ constexpr int chain_threads() { return M
 
 // d(Y_b)/d(dir) . v_b added into (gx, gy, gz): eval_sh_basis_grad
 // (harmonics.py:62-98) row b, written out (b is a compile-time constant).
-__device__ __forceinline__ void add_basis_grad(int b, double v, double x, double y, double z, double &gx, double &gy,
-                                               double &gz) {
-  const double xx = x * x, yy = y * y, zz = z * z;
+__device__ __forceinline__ void add_basis_grad(int b, float v, float x, float y, float z, float &gx, float &gy,
+                                               float &gz) {
+  const float xx = x * x, yy = y * y, zz = z * z;
   switch (b) {
     case 1: gy -= kC1 * v; break;
     case 2: gz += kC1 * v; break;
     case 3: gx -= kC1 * v; break;
     case 4: gx += kC20 * y * v; gy += kC20 * x * v; break;
     case 5: gy += kC21 * z * v; gz += kC21 * y * v; break;
-    case 6: gx += -2.0 * kC22 * x * v; gy += -2.0 * kC22 * y * v; gz += 4.0 * kC22 * z * v; break;
+    case 6: gx += -2.0f * kC22 * x * v; gy += -2.0f * kC22 * y * v; gz += 4.0f * kC22 * z * v; break;
     case 7: gx += kC23 * z * v; gz += kC23 * x * v; break;
-    case 8: gx += 2.0 * kC24 * x * v; gy += -2.0 * kC24 * y * v; break;
-    case 9: gx += kC30 * 6.0 * x * y * v; gy += kC30 * 3.0 * (xx - yy) * v; break;
+    case 8: gx += 2.0f * kC24 * x * v; gy += -2.0f * kC24 * y * v; break;
+    case 9: gx += kC30 * 6.0f * x * y * v; gy += kC30 * 3.0f * (xx - yy) * v; break;
     case 10: gx += kC31 * y * z * v; gy += kC31 * x * z * v; gz += kC31 * x * y * v; break;
     case 11:
-      gx += -2.0 * kC32 * x * y * v; gy += kC32 * (4.0 * zz - xx - 3.0 * yy) * v; gz += 8.0 * kC32 * y * z * v;
+      gx += -2.0f * kC32 * x * y * v; gy += kC32 * (4.0f * zz - xx - 3.0f * yy) * v; gz += 8.0f * kC32 * y * z * v;
       break;
     case 12:
-      gx += -6.0 * kC33 * x * z * v; gy += -6.0 * kC33 * y * z * v; gz += kC33 * (6.0 * zz - 3.0 * xx - 3.0 * yy) * v;
+      gx += -6.0f * kC33 * x * z * v; gy += -6.0f * kC33 * y * z * v; gz += kC33 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * v;
       break;
     case 13:
-      gx += kC34 * (4.0 * zz - 3.0 * xx - yy) * v; gy += -2.0 * kC34 * x * y * v; gz += 8.0 * kC34 * x * z * v;
+      gx += kC34 * (4.0f * zz - 3.0f * xx - yy) * v; gy += -2.0f * kC34 * x * y * v; gz += 8.0f * kC34 * x * z * v;
       break;
-    case 14: gx += 2.0 * kC35 * x * z * v; gy += -2.0 * kC35 * y * z * v; gz += kC35 * (xx - yy) * v; break;
-    case 15: gx += kC36 * 3.0 * (xx - yy) * v; gy += -6.0 * kC36 * x * y * v; break;
+    case 14: gx += 2.0f * kC35 * x * z * v; gy += -2.0f * kC35 * y * z * v; gz += kC35 * (xx - yy) * v; break;
+    case 15: gx += kC36 * 3.0f * (xx - yy) * v; gy += -6.0f * kC36 * x * y * v; break;
     default: break;
   }
 }
@@ -71,22 +72,22 @@ __device__ __forceinline__ void add_basis_grad(int b, double v, double x, double
 // direction gradient dY/ddir^T (sh . d_eff).  Streams the 16x3 rows as
 // float4 (two reads of sh, one read-modify-write of d_sh) so no per-thread
 // 48-float arrays stay live.
-__device__ __forceinline__ void sh_vjp(double x, double y, double z, int deg, const float *sh, const float *d_color,
-                                       float *d_sh, double *ddir) {
+__device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const float *sh, const float *d_color,
+                                       float *d_sh, float *ddir) {
   float Y[kShCoeffs];
   Y[0] = kC0;
-  const double xx = x * x, yy = y * y, zz = z * z;
+  const float xx = x * x, yy = y * y, zz = z * z;
 #pragma unroll
   for (int b = 1; b < kShCoeffs; b++) Y[b] = 0.f;
   if (deg >= 1) { Y[1] = -kC1 * y; Y[2] = kC1 * z; Y[3] = -kC1 * x; }
   if (deg >= 2) {
-    Y[4] = kC20 * x * y; Y[5] = kC21 * y * z; Y[6] = kC22 * (2.0 * zz - xx - yy);
+    Y[4] = kC20 * x * y; Y[5] = kC21 * y * z; Y[6] = kC22 * (2.0f * zz - xx - yy);
     Y[7] = kC23 * x * z; Y[8] = kC24 * (xx - yy);
   }
   if (deg >= 3) {
-    Y[9] = kC30 * y * (3.0 * xx - yy); Y[10] = kC31 * x * y * z; Y[11] = kC32 * y * (4.0 * zz - xx - yy);
-    Y[12] = kC33 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy); Y[13] = kC34 * x * (4.0 * zz - xx - yy);
-    Y[14] = kC35 * z * (xx - yy); Y[15] = kC36 * x * (xx - 3.0 * yy);
+    Y[9] = kC30 * y * (3.0f * xx - yy); Y[10] = kC31 * x * y * z; Y[11] = kC32 * y * (4.0f * zz - xx - yy);
+    Y[12] = kC33 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy); Y[13] = kC34 * x * (4.0f * zz - xx - yy);
+    Y[14] = kC35 * z * (xx - yy); Y[15] = kC36 * x * (xx - 3.0f * yy);
   }
   const int nb = (deg + 1) * (deg + 1);
   const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
@@ -107,7 +108,7 @@ __device__ __forceinline__ void sh_vjp(double x, double y, double z, int deg, co
   float deff[3];
 #pragma unroll
   for (int c = 0; c < 3; c++) deff[c] = raw[c] > 0.f ? d_color[c] : 0.f;
-  double gx = 0.0, gy = 0.0, gz = 0.0, vb = 0.0;
+  float gx = 0.0f, gy = 0.0f, gz = 0.0f, vb = 0.0f;
 #pragma unroll
   for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
     if (4 * q < 3 * nb) {
@@ -120,10 +121,10 @@ __device__ __forceinline__ void sh_vjp(double x, double y, double z, int deg, co
         const int f = 4 * q + r, b = f / 3, c = f % 3;
         if (b < nb) {
           de[r] += Y[b] * deff[c];
-          vb = fma((double)e[r], (double)deff[c], vb);
+          vb = fmaf(e[r], deff[c], vb);
           if (c == 2) {  // row b complete: its direction-gradient term
             add_basis_grad(b, vb, x, y, z, gx, gy, gz);
-            vb = 0.0;
+            vb = 0.0f;
           }
         }
       }
@@ -133,55 +134,78 @@ __device__ __forceinline__ void sh_vjp(double x, double y, double z, int deg, co
   ddir[0] = gx; ddir[1] = gy; ddir[2] = gz;
 }
 
+// Geometry precision of the chain.  float32 by default; -DCS_CHAIN_F64 for A/B.
+#ifdef CS_CHAIN_F64
+typedef double G;
+__device__ __forceinline__ G g_rcp(G x) { return __drcp_rn(x); }
+__device__ __forceinline__ G g_rsqrt(G x) { return rsqrt(x); }
+#else
+typedef float G;
+__device__ __forceinline__ G g_rcp(G x) { return __frcp_rn(x); }
+__device__ __forceinline__ G g_rsqrt(G x) { return rsqrtf(x); }
+#endif
+
 template <int MAXK>
-__global__ void __launch_bounds__(chain_threads<MAXK>(), 4) chain_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainArgs a) {
   constexpr int kChainThreads = chain_threads<MAXK>();
   // per-thread slots for the dynamically indexed per-point arrays
-  __shared__ double s_x[MAXK][kChainThreads], s_y[MAXK][kChainThreads];
-  __shared__ double s_dx[MAXK][kChainThreads], s_dy[MAXK][kChainThreads];
+  __shared__ G s_x[MAXK][kChainThreads], s_y[MAXK][kChainThreads];
+  __shared__ G s_dx[MAXK][kChainThreads], s_dy[MAXK][kChainThreads];
   const int t = threadIdx.x;
   const int64_t i = (int64_t)blockIdx.x * kChainThreads + t;
   if (i >= a.n || a.touched[i] == 0) return;  // not prepared for this view
   constexpr int RF = Rec<MAXK>::kFloats;
   constexpr int AF = Acc<MAXK>::kFloats;
   const int k = a.k;
-  float acc[AF];
-  const float4 *accv = reinterpret_cast<const float4 *>(a.accum + i * AF);
-#pragma unroll
-  for (int q = 0; q < AF / 4; q++) {
-    const float4 v = accv[q];
-    acc[4 * q] = v.x; acc[4 * q + 1] = v.y; acc[4 * q + 2] = v.z; acc[4 * q + 3] = v.w;
-  }
+  const G inv_k = G(1) / (G)k;
+  const float *acc = a.accum + i * AF;
   const float2 anchor = *reinterpret_cast<const float2 *>(a.records + i * RF);
-  const double ax = anchor.x, ay = anchor.y;
-  const double *R = a.cam.R;
-  // recompute the projection (projection.py:22-40)
-  double zsum = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
-  double xc[MAXK], yc[MAXK], zc[MAXK];
+  G R[9];
+#pragma unroll
+  for (int q = 0; q < 9; q++) R[q] = (G)a.cam.R[q];
+  const G fx = (G)a.cam.fx, fy = (G)a.cam.fy;
+  // recompute the projection (projection.py:22-40) in float64 and keep the
+  // projected points RELATIVE TO THE ANCHOR (ax, ay): the hull normals and
+  // the line -> vertex Jacobian then see small coordinates, so float32 keeps
+  // ~1e-6 px where absolute 1080p coordinates would only keep ~6e-5 px.
+  const double *Rd = a.cam.R;
+  const double ox = a.cam.cx - (double)anchor.x, oy = a.cam.cy - (double)anchor.y;
+  G zsum = 0, cx = 0, cy = 0, cz = 0;
+  G izc[MAXK];
 #pragma unroll
   for (int j = 0; j < MAXK; j++) {
     if (j < k) {
       const float *pp = a.points + (i * k + j) * 3;
-      const double p0 = pp[0], p1 = pp[1], p2 = pp[2];
-      cx += p0; cy += p1; cz += p2;
-      xc[j] = fma(p2, R[2], fma(p1, R[1], p0 * R[0])) + a.cam.t[0];
-      yc[j] = fma(p2, R[5], fma(p1, R[4], p0 * R[3])) + a.cam.t[1];
-      zc[j] = fma(p2, R[8], fma(p1, R[7], p0 * R[6])) + a.cam.t[2];
-      zsum += zc[j];
+      const float q0 = pp[0], q1 = pp[1], q2 = pp[2];
+      cx += q0; cy += q1; cz += q2;
+      const double p0 = q0, p1 = q1, p2 = q2;
+      const double xc = fma(p2, Rd[2], fma(p1, Rd[1], p0 * Rd[0])) + a.cam.t[0];
+      const double yc = fma(p2, Rd[5], fma(p1, Rd[4], p0 * Rd[3])) + a.cam.t[1];
+      const double zc = fma(p2, Rd[8], fma(p1, Rd[7], p0 * Rd[6])) + a.cam.t[2];
+      zsum += (G)zc;
       if (a.cam.ortho) {
-        s_x[j][t] = a.cam.fx * xc[j] + a.cam.cx;
-        s_y[j][t] = a.cam.fy * yc[j] + a.cam.cy;
+        s_x[j][t] = (G)fma(a.cam.fx, xc, ox);
+        s_y[j][t] = (G)fma(a.cam.fy, yc, oy);
+        izc[j] = 0;
       } else {
-        s_x[j][t] = (a.cam.fx * xc[j]) / zc[j] + a.cam.cx;
-        s_y[j][t] = (a.cam.fy * yc[j]) / zc[j] + a.cam.cy;
+        const double iz = __drcp_rn(zc);
+        izc[j] = (G)iz;
+        s_x[j][t] = (G)fma(a.cam.fx * xc, iz, ox);
+        s_y[j][t] = (G)fma(a.cam.fy * yc, iz, oy);
       }
-      s_dx[j][t] = 0.0;
-      s_dy[j][t] = 0.0;
+      s_dx[j][t] = 0;
+      s_dy[j][t] = 0;
     }
   }
   uint8_t hb[MAXK];
+  if (MAXK == 8) {
+    const uint2 hw = *reinterpret_cast<const uint2 *>(a.hull + i * MAXK);
 #pragma unroll
-  for (int j = 0; j < MAXK; j++) hb[j] = a.hull[i * MAXK + j];
+    for (int j = 0; j < 4; j++) { hb[j] = (hw.x >> (8 * j)) & 0xff; hb[j + 4] = (hw.y >> (8 * j)) & 0xff; }
+  } else {
+#pragma unroll
+    for (int j = 0; j < MAXK; j++) hb[j] = a.hull[i * MAXK + j];
+  }
   int h = 0;
 #pragma unroll
   for (int j = 0; j < MAXK; j++) h += hb[j] != 0xff;
@@ -194,78 +218,76 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 4) chain_kernel(ChainAr
       for (int q = 1; q < MAXK; q++)
         if (q == j + 1) v = q < h ? hb[q] : hb[0];
       const int u = hb[j];
-      const double ux = s_x[u][t], uy = s_y[u][t];
-      const double ex = s_x[v][t] - ux, ey = s_y[v][t] - uy;
-      const double len = hypot(ey, ex);
-      const double nx = ey / len, ny = -ex / len;
-      const double gs = acc[A_LINES + 3 * j + 2];
-      // reference gn = sum dL*q - gs*v = sum dL*(q-a) + gs*(a - v)
-      const double gx = acc[A_LINES + 3 * j] + gs * (ax - ux);
-      const double gy = acc[A_LINES + 3 * j + 1] + gs * (ay - uy);
-      const double nd = nx * gx + ny * gy;
-      const double rx = (gx - nx * nd) / len, ry = (gy - ny * nd) / len;
+      const G ux = s_x[u][t], uy = s_y[u][t];
+      const G ex = s_x[v][t] - ux, ey = s_y[v][t] - uy;
+      const G il = g_rsqrt(fma(ex, ex, ey * ey));
+      const G nx = ey * il, ny = -ex * il;
+      const G gs = (G)acc[A_LINES + 3 * j + 2];
+      // reference gn = sum dL*q - gs*v = sum dL*(q-a) - gs*(v-a); u is anchor-relative
+      const G gx = fma(-gs, ux, (G)acc[A_LINES + 3 * j]);
+      const G gy = fma(-gs, uy, (G)acc[A_LINES + 3 * j + 1]);
+      const G nd = fma(nx, gx, ny * gy);
+      const G rx = (gx - nx * nd) * il, ry = (gy - ny * nd) * il;
       s_dx[v][t] += -ry;
       s_dy[v][t] += rx;
       s_dx[u][t] += ry - nx * gs;
       s_dy[u][t] += -rx - ny * gs;
     }
   }
+  const float dcol[3] = {(float)acc[A_DC], (float)acc[A_DC + 1], (float)acc[A_DC + 2]};
   // depth, scale and activations (rasterize.py:99-103, field.py:26-48)
-  const double depth = zsum / k;
-  const double dsc = a.cam.ortho ? 1.0 : depth;
-  double s, sgrad;
+  const G depth = zsum * inv_k;
+  const G dsc = a.cam.ortho ? G(1) : depth;
+  G s, sgrad;
   switch (a.mode) {
-    case CS_SCALE_NONE: s = 1.0; sgrad = 0.0; break;
-    case CS_SCALE_SQRT: s = sqrt(dsc); sgrad = 0.5 / sqrt(depth); break;
-    case CS_SCALE_DEPTH: s = dsc; sgrad = 1.0; break;
-    default: s = dsc * dsc; sgrad = 2.0 * depth; break;
+    case CS_SCALE_NONE: s = 1; sgrad = 0; break;
+    case CS_SCALE_SQRT: s = sqrt(dsc); sgrad = G(0.5) * g_rsqrt(depth); break;
+    case CS_SCALE_DEPTH: s = dsc; sgrad = 1; break;
+    default: s = dsc * dsc; sgrad = G(2) * depth; break;
   }
-  const double delta = exp((double)a.raw_delta[i]), sigma = exp((double)a.raw_sigma[i]);
-  const double ddel = acc[A_DDEL], dsig = acc[A_DSIG];
-  const double d_depth = a.cam.ortho ? 0.0 : (ddel * delta + dsig * sigma) * sgrad;
+  const G delta = exp((G)a.raw_delta[i]), sigma = exp((G)a.raw_sigma[i]);
+  const G ddel = (G)acc[A_DDEL], dsig = (G)acc[A_DSIG];
+  const G d_depth = a.cam.ortho ? G(0) : (ddel * delta + dsig * sigma) * sgrad;
   // view direction (rasterize.py:110-113) and SH VJP (harmonics.py:112-128)
-  const double vx = cx / k - a.cam_center[0], vy = cy / k - a.cam_center[1], vz = cz / k - a.cam_center[2];
-  const double dist = sqrt(vx * vx + vy * vy + vz * vz);
-  double dir[3] = {0.0, 0.0, 1.0};
-  if (dist > 0.0) { dir[0] = vx / dist; dir[1] = vy / dist; dir[2] = vz / dist; }
-  double ddirf[3];
-  sh_vjp(dir[0], dir[1], dir[2], a.sh_degree, a.sh + i * kShCoeffs * 3, acc + A_DC,
-         a.g.d_sh + i * kShCoeffs * 3, ddirf);
-  const double dot = dir[0] * ddirf[0] + dir[1] * ddirf[1] + dir[2] * ddirf[2];
-  double dcen[3];
-#pragma unroll
-  for (int q = 0; q < 3; q++) dcen[q] = dist > 0.0 ? (ddirf[q] - dir[q] * dot) / dist : 0.0;
+  const float fk = 1.f / (float)k;
+  const float vx = (float)cx * fk - (float)a.cam_center[0], vy = (float)cy * fk - (float)a.cam_center[1],
+              vz = (float)cz * fk - (float)a.cam_center[2];
+  const float d2 = fmaf(vx, vx, fmaf(vy, vy, vz * vz));
+  const float idist = d2 > 0.f ? rsqrtf(d2) : 0.f;
+  float dir[3] = {0.f, 0.f, 1.f};
+  if (d2 > 0.f) { dir[0] = vx * idist; dir[1] = vy * idist; dir[2] = vz * idist; }
+  float ddirf[3];
+  sh_vjp(dir[0], dir[1], dir[2], a.sh_degree, a.sh + i * kShCoeffs * 3, dcol, a.g.d_sh + i * kShCoeffs * 3, ddirf);
+  const float dot = dir[0] * ddirf[0] + dir[1] * ddirf[1] + dir[2] * ddirf[2];
   // projection Jacobian + depth + centre paths into d_points (backward.py:248-269, 281-282)
+  G common[3];
+#pragma unroll
+  for (int c = 0; c < 3; c++) common[c] = (d_depth * R[6 + c] + (G)((ddirf[c] - dir[c] * dot) * idist)) * inv_k;
   float *dp = a.g.d_points + i * k * 3;
 #pragma unroll
   for (int j = 0; j < MAXK; j++) {
     if (j < k) {
-      const double gx = s_dx[j][t], gy = s_dy[j][t];
-      double d0, d1, d2;
+      const G gx = s_dx[j][t], gy = s_dy[j][t];
+      G d0, d1, dz;
       if (a.cam.ortho) {
-        d0 = a.cam.fx * gx; d1 = a.cam.fy * gy; d2 = 0.0;
+        d0 = fx * gx; d1 = fy * gy; dz = 0;
       } else {
-        const double z = zc[j];
-        d0 = a.cam.fx / z * gx;
-        d1 = a.cam.fy / z * gy;
-        d2 = -(a.cam.fx * xc[j] / (z * z)) * gx - (a.cam.fy * yc[j] / (z * z)) * gy;
+        d0 = fx * izc[j] * gx;
+        d1 = fy * izc[j] * gy;
+        // fx x / z^2 = (px - cx) / z, px - cx = (px - ax) - (cx - ax)
+        dz = -((s_x[j][t] - (G)ox) * gx + (s_y[j][t] - (G)oy) * gy) * izc[j];
       }
 #pragma unroll
-      for (int c = 0; c < 3; c++) {
-        double v = d0 * R[c] + d1 * R[3 + c] + d2 * R[6 + c];
-        v += d_depth * R[6 + c] / k;
-        v += dcen[c] / k;
-        dp[3 * j + c] += (float)v;
-      }
+      for (int c = 0; c < 3; c++) dp[3 * j + c] += (float)fma(d0, R[c], fma(d1, R[3 + c], fma(dz, R[6 + c], common[c])));
     }
   }
   a.g.d_raw_delta[i] += (float)(ddel * s * delta);
   a.g.d_raw_sigma[i] += (float)(dsig * s * sigma);
-  const double o = 1.0 / (1.0 + exp(-(double)a.raw_opacity[i]));
-  const double m = 1.0 / (1.0 + exp(-(double)a.raw_mask[i]));
-  const double doe = acc[A_DOEFF];
-  a.g.d_raw_opacity[i] += (float)(doe * o * (1.0 - o));
-  a.g.d_raw_mask[i] += (float)(doe * o * m * (1.0 - m));
+  const float o = 1.f / (1.f + __expf(-a.raw_opacity[i]));
+  const float m = 1.f / (1.f + __expf(-a.raw_mask[i]));
+  const float doe = (float)acc[A_DOEFF];
+  a.g.d_raw_opacity[i] += doe * o * (1.f - o);
+  a.g.d_raw_mask[i] += doe * o * m * (1.f - m);
 }
 
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,

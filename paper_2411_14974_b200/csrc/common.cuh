@@ -24,9 +24,11 @@ constexpr uint64_t kCulledKey = ~0ull;
 // where L_j = n_j.q + off_j is the reference's signed line distance
 // (projection.py:131-133) and (ax, ay) an integer anchor inside the bbox
 // (keeps fp32 cancellation out of 1080p coordinates).
+//   float4 0: ax ay sigma_s o | 1: r g b depth | 2: 1-o dls nl 1/dls
+//   float4 3: bbox x0 x1 y0 y1 (int32 bits, half-open) | 4..: lines (A,B,C)
 enum RecField {
   R_AX = 0, R_AY = 1, R_SIGMA = 2, R_OPACITY = 3, R_R = 4, R_G = 5, R_B = 6, R_DEPTH = 7,
-  R_ONE_MINUS_O = 8, R_DLS = 9, R_NLINES = 10, R_BBX = 12, R_BBY = 13, R_HEADER = 16
+  R_ONE_MINUS_O = 8, R_DLS = 9, R_NLINES = 10, R_INV_DLS = 11, R_BBOX = 12, R_HEADER = 16
 };
 template <int MAXK> struct Rec {
   static constexpr int kFloats = R_HEADER + 3 * MAXK;   // 40 for MAXK=8, multiple of 4
@@ -123,11 +125,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t phase) {
 // Wait for the phase of parity `phase` to complete.  A wait longer than 2 s
 // can only be a protocol bug: trap (the launch fails with an error the host
 // reports) instead of hanging the device.
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or the hint elapses) instead of spinning on issue slots.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t phase) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(1000000u)
+      : "memory");
+  return done != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   if (mbar_try_wait(bar, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_wait(bar, phase)) {
-    if (globaltimer_ns() - t0 > 2000000000ull) __trap();
+  for (uint32_t it = 1; !mbar_try_wait_sleep(bar, phase); it++) {
+    if ((it & 63u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
   }
 }
 

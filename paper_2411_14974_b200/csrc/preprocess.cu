@@ -463,8 +463,8 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   sh_colour(dx, dy, dz, a.sh_degree, sh_s, col);
   dst[0] = make_float4((float)ax, (float)ay, (float)sigma_s, (float)o);
   dst[1] = make_float4(col[0], col[1], col[2], (float)depth);
-  dst[2] = make_float4(1.f / (1.f + __expf(ro)), (float)dls, __int_as_float(h), 0.f);
-  dst[3] = make_float4(__int_as_float(x0 | (x1 << 16)), __int_as_float(y0 | (y1 << 16)), 0.f, 0.f);
+  dst[2] = make_float4(1.f / (1.f + __expf(ro)), (float)dls, __int_as_float(h), (float)(1.0 / dls));
+  dst[3] = make_float4(__int_as_float(x0), __int_as_float(x1), __int_as_float(y0), __int_as_float(y1));
   return true;
 }
 
