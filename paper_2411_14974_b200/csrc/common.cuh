@@ -44,7 +44,13 @@ template <int MAXK> struct Acc {
 };
 
 // Counters at the head of the workspace.
-enum Counter { C_NVISIBLE = 0, C_NPAIRS = 1, C_OVERFLOW = 2, C_NSORT = 3, C_CHUNK0 = 4, C_STATS = 16, C_COUNT = 32 };
+// C_KMINC / C_KMAX: uint64 complement of the smallest / the largest depth key
+// of the visible convexes (word offsets, 8-byte aligned), for the 32-bit
+// depth-sort keys.
+enum Counter {
+  C_NVISIBLE = 0, C_NPAIRS = 1, C_OVERFLOW = 2, C_NSORT = 3, C_CHUNK0 = 4, C_STATS = 16, C_KMINC = 32, C_KMAX = 34,
+  C_COUNT = 40
+};
 // uint64 work statistics at word C_STATS (roofline accounting, read by the benchmark)
 enum Stat { S_FWD_EVALS = 0, S_FWD_LINES = 1, S_FWD_BLENDS = 2, S_BWD_EVALS = 3, S_BWD_LINES = 4, S_COUNT = 8 };
 

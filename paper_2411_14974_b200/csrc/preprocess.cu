@@ -509,6 +509,25 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(PreArgs a) {
                                Xs + threadIdx.x, Ys + threadIdx.x);
   unsigned b = __ballot_sync(0xffffffffu, vis);
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(&a.counters[C_NVISIBLE], (unsigned)__popc(b));
+  // range of the visible depth keys (block reduce, one atomic pair per block)
+  {
+    __shared__ unsigned long long s_kminc, s_kmax;
+    if (threadIdx.x == 0) { s_kminc = 0ull; s_kmax = 0ull; }
+    __syncthreads();
+    unsigned long long kc = 0ull, kx = 0ull;
+    if (vis) { kx = a.depth_keys[i]; kc = ~kx; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      kc = max(kc, (unsigned long long)__shfl_xor_sync(0xffffffffu, kc, o));
+      kx = max(kx, (unsigned long long)__shfl_xor_sync(0xffffffffu, kx, o));
+    }
+    if ((threadIdx.x & 31) == 0 && b) { atomicMax(&s_kminc, kc); atomicMax(&s_kmax, kx); }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_kmax) {
+      atomicMax(reinterpret_cast<unsigned long long *>(a.counters + C_KMINC), s_kminc);
+      atomicMax(reinterpret_cast<unsigned long long *>(a.counters + C_KMAX), s_kmax);
+    }
+  }
   if (threadIdx.x == 0) mbar_wait(&bars[1], 0);  // never leave while a bulk copy still targets this smem
 }
 

@@ -1,6 +1,7 @@
 // K2: depth order + tile binning (rasterize.py:121 sort, rasterize.py:134-144).
 //
-//   depth sort   stable LSD radix sort of (orderable f64 depth bits, convex id)
+//   depth sort   stable LSD radix sort of 31-bit keys monotone in the
+//                orderable f64 depth bits + exact fix-up of equal-key runs
 //                == Python's sort by (depth, index) (rasterize.py:121)
 //   scan         exclusive scan of tiles_touched in depth order -> pair offsets
 //   duplicate    every convex, visited in depth order, emits (tile, id) pairs
@@ -457,6 +458,98 @@ __global__ void ranges_kernel(const uint32_t *pair_tiles, const uint32_t *counte
   ranges[t] = make_uint2(lower((uint32_t)t), lower((uint32_t)t + 1));
 }
 
+// ------------------------------------------------------------------ depth order
+// The depth order sorts (f64 depth, index) (rasterize.py:121).  Instead of a
+// 64-bit radix sort (8 passes) the keys are reduced to 31 bits,
+//   key32 = (key64 - kmin) >> shift,   shift = max(0, bits(kmax - kmin) - 31),
+// which is monotone in key64; a stable 4-pass sort by key32 then orders
+// (key32, index).  Only runs of EQUAL key32 can be out of (key64, index)
+// order, and only when shift > 0; depth_fixup_kernel re-sorts those runs by
+// the full key (they are a few items long on real scenes).  Culled convexes
+// get key32 = ~0 and stay at the end, in index order.
+__device__ __forceinline__ void depth_range(const uint32_t *counters, uint64_t &kmin, int &shift, bool &any) {
+  const uint64_t kminc = *reinterpret_cast<const unsigned long long *>(counters + C_KMINC);
+  const uint64_t kmax = *reinterpret_cast<const unsigned long long *>(counters + C_KMAX);
+  any = kmax != 0ull;
+  kmin = ~kminc;
+  const uint64_t range = any ? kmax - kmin : 0ull;
+  const int bits = range ? 64 - __clzll((long long)range) : 0;
+  shift = bits > 31 ? bits - 31 : 0;
+}
+
+__global__ void __launch_bounds__(kSortThreads) depth_key32_kernel(const uint64_t *keys64, const uint32_t *counters,
+                                                                   uint32_t n, uint32_t *keys32, uint32_t *order,
+                                                                   uint32_t *hist) {
+  __shared__ uint32_t h[4][kRadix];
+  for (int q = threadIdx.x; q < 4 * kRadix; q += kSortThreads) h[q / kRadix][q % kRadix] = 0;
+  __syncthreads();
+  uint64_t kmin;
+  int shift;
+  bool any;
+  depth_range(counters, kmin, shift, any);
+  for (uint32_t idx = blockIdx.x * kSortThreads + threadIdx.x; idx < n; idx += gridDim.x * kSortThreads) {
+    const uint64_t k = keys64[idx];
+    const uint32_t k32 = k == kCulledKey ? 0xffffffffu : (uint32_t)((k - kmin) >> shift);
+    keys32[idx] = k32;
+    order[idx] = idx;
+#pragma unroll
+    for (int p = 0; p < 4; p++) atomicAdd(&h[p][(k32 >> (p * kRadixBits)) & (kRadix - 1)], 1u);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 4 * kRadix; q += kSortThreads) {
+    const uint32_t v = h[q / kRadix][q % kRadix];
+    if (v) atomicAdd(&hist[q], v);
+  }
+}
+
+// Re-sort runs of equal key32 by (key64, index).  One thread per run start;
+// insertion sort for short runs, heap sort beyond (pathological clustering).
+__device__ __forceinline__ bool depth_less(const uint64_t *keys64, uint32_t a, uint32_t b) {
+  const uint64_t ka = keys64[a], kb = keys64[b];
+  return ka < kb || (ka == kb && a < b);
+}
+
+__global__ void depth_fixup_kernel(const uint64_t *keys64, const uint32_t *counters, const uint32_t *keys32,
+                                   uint32_t *order) {
+  uint64_t kmin;
+  int shift;
+  bool any;
+  depth_range(counters, kmin, shift, any);
+  if (!any || shift == 0) return;  // key32 exact: nothing to fix
+  const uint32_t V = counters[C_NVISIBLE];
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r + 1 >= V) return;
+  const uint32_t k = keys32[r];
+  if ((r > 0 && keys32[r - 1] == k) || keys32[r + 1] != k) return;  // not the start of a run of >= 2
+  uint32_t e = r + 2;
+  while (e < V && keys32[e] == k) e++;
+  uint32_t *o = order + r;
+  const uint32_t len = e - r;
+  if (len <= 32) {
+    for (uint32_t x = 1; x < len; x++) {
+      const uint32_t v = o[x];
+      uint32_t y = x;
+      while (y > 0 && depth_less(keys64, v, o[y - 1])) { o[y] = o[y - 1]; y--; }
+      o[y] = v;
+    }
+    return;
+  }
+  auto sift = [&](uint32_t root, uint32_t end) {
+    while (2 * root + 1 < end) {
+      uint32_t c = 2 * root + 1;
+      if (c + 1 < end && depth_less(keys64, o[c], o[c + 1])) c++;
+      if (!depth_less(keys64, o[root], o[c])) return;
+      const uint32_t t = o[root]; o[root] = o[c]; o[c] = t;
+      root = c;
+    }
+  };
+  for (uint32_t st = len / 2; st-- > 0;) sift(st, len);
+  for (uint32_t end = len - 1; end > 0; end--) {
+    const uint32_t t = o[0]; o[0] = o[end]; o[end] = t;
+    sift(0, end);
+  }
+}
+
 // ------------------------------------------------------------------ orchestration
 struct Scratch {
   uint64_t *dkeys_alt;
@@ -519,9 +612,14 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
   cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 16 * kRadix, s);
   cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * sc.lookback_words, s);
   if (n > 0) {
-    // depth order: 8 passes (even) -> result back in (dkeys, order)
-    radix_sort<uint64_t>(dkeys, order, sc.dkeys_alt, sc.dvals_alt, nullptr, n, n, 8, 0, sc.hist,
-                         sc.offsets, sc.lookback, counters + C_CHUNK0, false, s);
+    // depth order: 31-bit keys, 4 passes (even) -> (keys32, order), then
+    // the exact fix-up of equal-key runs
+    uint32_t *k32 = reinterpret_cast<uint32_t *>(sc.dkeys_alt), *k32b = k32 + n;
+    const int kb = min((int)((n + kSortThreads - 1) / kSortThreads), 148 * 8);
+    depth_key32_kernel<<<kb, kSortThreads, 0, s>>>(dkeys, counters, n, k32, order, sc.hist);
+    radix_sort<uint32_t>(k32, order, k32b, sc.dvals_alt, nullptr, n, n, 4, 0, sc.hist, sc.offsets, sc.lookback,
+                         counters + C_CHUNK0, true, s);
+    depth_fixup_kernel<<<(n + 255) / 256, 256, 0, s>>>(dkeys, counters, k32, order);
     const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
     scan_reduce_kernel<<<nb, kScanThreads, 0, s>>>(order, touched, n, sc.block_sums);
     scan_top_kernel<<<1, 1024, 0, s>>>(sc.block_sums, nb, counters, (uint64_t)cap);

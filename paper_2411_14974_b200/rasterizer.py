@@ -23,7 +23,7 @@ from .model import (EXACT_SETTINGS, SH_COEFFS, Camera, GradientBuffer, RenderOut
                     RenderSettings, ScalingMode)
 from .scene_tensors import SceneTensors, as_scene_tensors
 
-_COUNTERS = 32
+_COUNTERS = 40
 STAT_NAMES = ("fwd_evals", "fwd_line_evals", "fwd_blends", "bwd_evals", "bwd_line_evals")
 
 
@@ -349,7 +349,7 @@ def inspect_frame(fr: Frame) -> dict:
     hull = _np(ws.region("hull", torch.uint8, n * L.max_k)).reshape(n, L.max_k).astype(np.int64)
     hull[hull == 255] = -1
     bbox = _np(ws.region("bbox", torch.int32, 4 * n)).reshape(n, 4).astype(np.int64)
-    keys = _np(ws.region("depth_keys", torch.int64, n)).view(np.uint64)[:V]
+    keys = _np(ws.region("depth_keys", torch.int64, n)).view(np.uint64)[order]
     ranges = _np(ws.region("tile_ranges", torch.int32, 2 * tiles)).reshape(tiles, 2).astype(np.int64)
     pair_ids = _np(ws.region("pair_ids", torch.int32, P)).astype(np.int64)
     pair_tiles = _np(ws.region("pair_tiles", torch.int32, P)).astype(np.int64)
