@@ -57,6 +57,16 @@ __device__ __forceinline__ bool box_overlaps(int4 b, int rx0, int ry0) {
 __device__ __forceinline__ bool in_box(int4 b, int px, int py) {
   return px >= b.x && px < b.y && py >= b.z && py < b.w;
 }
+// Pixels of the warp's 8x4 block (bit = 8 * row + column, the lane order of
+// tile_pixel) inside a candidate's half-open bbox.
+__device__ __forceinline__ uint32_t block_mask(int4 b, int rx0, int ry0) {
+  const int c0 = max(b.x - rx0, 0), c1 = min(b.y - rx0, 8);
+  const int r0 = max(b.z - ry0, 0), r1 = min(b.w - ry0, 4);
+  if (c1 <= c0 || r1 <= r0) return 0u;
+  const uint32_t cols = (1u << c1) - (1u << c0);                                  // < 256
+  const uint32_t rows = (uint32_t)(((1ull << (8 * r1)) - (1ull << (8 * r0))) / 255ull);  // 0x01 per row byte
+  return cols * rows;
+}
 __device__ __forceinline__ int4 rec_bbox(const float4 *rec) {
   const float4 v = rec[R_BBOX / 4];
   return make_int4(__float_as_int(v.x), __float_as_int(v.y), __float_as_int(v.z), __float_as_int(v.w));
@@ -158,11 +168,21 @@ __device__ __forceinline__ Eval eval_field(const LineSet<NL, MAXK> &L, float sig
 // stage (rasterize.py:203 `visible[idx] = True`).
 constexpr int kConsumers = 8;
 constexpr int kPipeThreads = 32 * (kConsumers + 1);
-constexpr int kStages = 4;
+// Ring depth: the forward stops early (saturated pixels), so a deep ring
+// mostly prefetches records nobody evaluates; the backward walks the whole
+// list up to each warp's last candidate and profits from more lookahead
+// (measured: 4 / 6 stages best).
+#ifndef CS_FWD_STAGES
+#define CS_FWD_STAGES 4
+#endif
+#ifndef CS_BWD_STAGES
+#define CS_BWD_STAGES 6
+#endif
 constexpr int kStageCands = 32;
 
-template <int MAXK>
+template <int MAXK, int kStages>
 struct PipeSmem {
+  static constexpr int kRing = kStages;
   float4 rec[kStages][kStageCands][Rec<MAXK>::kFloats / 4];
   uint32_t id[kStages][kStageCands];
   uint32_t vis[kStages];
@@ -176,8 +196,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int MAXK>
-__device__ __forceinline__ void flush_visible(PipeSmem<MAXK> &sm, int s, uint8_t *visible) {
+template <int MAXK, int kStages>
+__device__ __forceinline__ void flush_visible(PipeSmem<MAXK, kStages> &sm, int s, uint8_t *visible) {
   const int lane = threadIdx.x & 31;
   const uint32_t vm = *reinterpret_cast<volatile uint32_t *>(&sm.vis[s]);
   if (visible && ((vm >> lane) & 1u)) visible[sm.id[s][lane]] = 1;
@@ -187,13 +207,21 @@ __device__ __forceinline__ void flush_visible(PipeSmem<MAXK> &sm, int s, uint8_t
 }
 
 // Producer warp: batch b covers pair indices first(b) .. first(b)+count(b)-1.
-template <int MAXK, typename Batch>
-__device__ __forceinline__ void pipe_produce(PipeSmem<MAXK> &sm, const float *records, const uint32_t *pair_ids,
+template <int MAXK, int kStages, typename Batch>
+__device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const float *records, const uint32_t *pair_ids,
                                              int nbatch, Batch batch, bool forward, uint8_t *visible) {
   constexpr int RB = Rec<MAXK>::kFloats * 4;
   const int lane = threadIdx.x & 31;
   int issued = 0;
   bool stopped = false;
+  // candidate ids are loaded one batch ahead (their latency hides behind the
+  // wait for the next free stage)
+  uint32_t next_id = 0;
+  if (nbatch > 0) {
+    uint32_t f0, c0;
+    batch(0, f0, c0);
+    if (lane < (int)c0) next_id = __ldg(pair_ids + f0 + lane);
+  }
   for (int b = 0; b < nbatch; b++) {
     const int s = b % kStages, u = b / kStages;
     if (u > 0) {
@@ -201,26 +229,51 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK> &sm, const float *re
       if (forward) flush_visible(sm, s, visible);
     }
     if (forward && *reinterpret_cast<volatile int *>(&sm.ndone) == kConsumers) {
-      if (lane == 0) {
-        // stop = b + 1: consumers leave at batch b.  Consumers still behind
-        // (done warps lag) keep releasing the issued batches < b normally.
-        *reinterpret_cast<volatile int *>(&sm.stop) = b + 1;
-        mbar_arrive(&sm.full[s]);          // wake consumers waiting on batch b
-      }
+      // stop = b + 1: consumers leave at batch b.  Consumers still behind
+      // (done warps lag) keep releasing the issued batches < b normally.
+      if (lane == 0) *reinterpret_cast<volatile int *>(&sm.stop) = b + 1;
+      __syncwarp();
+#ifdef CS_PRODUCER_TMA
+      if (lane == 0) mbar_arrive(&sm.full[s]);   // wake consumers waiting on batch b
+#else
+      mbar_arrive(&sm.full[s]);                  // all 32 lanes: the barrier counts 32
+#endif
       stopped = true;
       break;
     }
     uint32_t first, count;
     batch(b, first, count);
-    uint32_t id = 0;
-    if (lane < (int)count) {
-      id = __ldg(pair_ids + first + lane);
-      sm.id[s][lane] = id;
+    const uint32_t id = next_id;
+    if (b + 1 < nbatch) {
+      uint32_t f1, c1;
+      batch(b + 1, f1, c1);
+      next_id = lane < (int)c1 ? __ldg(pair_ids + f1 + lane) : 0u;
     }
+    if (lane < (int)count) sm.id[s][lane] = id;
     __syncwarp();
+#ifdef CS_PRODUCER_TMA
     if (lane == 0) mbar_expect_tx(&sm.full[s], count * RB);
     __syncwarp();
     if (lane < (int)count) tma_bulk_g2s(&sm.rec[s][lane][0], records + (size_t)id * Rec<MAXK>::kFloats, RB, &sm.full[s]);
+#else
+    {
+      // coalesced gather: each round copies RPR whole records, one 16-byte
+      // chunk per lane (cp.async.cg), so every record is read as contiguous
+      // sectors; the lanes then arrive on `full` when their copies land.
+      constexpr int CPR = Rec<MAXK>::kFloats / 4, RPR = 32 / CPR;
+      const int r_in = lane / CPR, c = lane % CPR;
+      for (int r0 = 0; r0 < (int)count; r0 += RPR) {
+        const int r = r0 + r_in;
+        const uint32_t rid = __shfl_sync(0xffffffffu, id, min(r, 31));
+        if (r_in < RPR && r < (int)count) {
+          const float4 *src = reinterpret_cast<const float4 *>(records + (size_t)rid * Rec<MAXK>::kFloats) + c;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sm.rec[s][r][c])), "l"(src)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
+    }
+#endif
     issued = b + 1;
   }
   // drain: wait until the consumers released the last issued batches (their
@@ -234,11 +287,15 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK> &sm, const float *re
   }
 }
 
-template <int MAXK>
-__device__ __forceinline__ void pipe_init(PipeSmem<MAXK> &sm) {
+template <int MAXK, int kStages>
+__device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages> &sm) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
+#ifdef CS_PRODUCER_TMA
       mbar_init(&sm.full[s], 1);
+#else
+      mbar_init(&sm.full[s], 32);   // one cp.async arrival per producer lane
+#endif
       mbar_init(&sm.empty[s], kConsumers);
       sm.vis[s] = 0u;
     }
@@ -285,16 +342,18 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float qx, float
 // Forward blend (rasterize.py:178-209), one 16x16 tile per block.
 template <int MAXK>
 __global__ void __launch_bounds__(kPipeThreads, 4) forward_kernel(BlendArgs a) {
-  __shared__ PipeSmem<MAXK> sm;
+  constexpr int kStages = CS_FWD_STAGES;
+  extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
+  PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint2 range = a.ranges[tile];
   const int nbatch = (int)((range.y - range.x + kStageCands - 1) / kStageCands);
   pipe_init(sm);
-  unsigned n_eval = 0, n_lines = 0, n_blend = 0;
+  unsigned n_eval = 0, n_lines = 0, n_blend = 0, n_warp_evals = 0;
   if (warp == kConsumers) {
-    pipe_produce<MAXK>(sm, a.records, a.pair_ids, nbatch,
+    pipe_produce<MAXK, kStages>(sm, a.records, a.pair_ids, nbatch,
                        [&](int b, uint32_t &first, uint32_t &count) {
                          first = range.x + (uint32_t)b * kStageCands;
                          count = min((uint32_t)kStageCands, range.y - first);
@@ -320,16 +379,24 @@ __global__ void __launch_bounds__(kPipeThreads, 4) forward_kernel(BlendArgs a) {
       if (!warp_done) {
         const uint32_t first = range.x + (uint32_t)b * kStageCands;
         const int count = (int)min((uint32_t)kStageCands, range.y - first);
-        bool hit = false;
-        if (lane < count) hit = box_overlaps(rec_bbox(sm.rec[s][lane]), rx0, ry0);
-        uint32_t m = __ballot_sync(0xffffffffu, hit);
+        // lane j: pixels of this warp's block inside candidate j's bbox and alive
+        const uint32_t alive = __ballot_sync(0xffffffffu, !P.done);
+        const uint32_t pm = lane < count ? block_mask(rec_bbox(sm.rec[s][lane]), rx0, ry0) & alive : 0u;
+        uint32_t m = __ballot_sync(0xffffffffu, pm != 0u);
         uint32_t vis = 0;
         while (m) {
           const int j = __ffs(m) - 1;
           m &= m - 1;
           const float4 *rec = sm.rec[s][j];
           bool blended = false;
-          if (!P.done && in_box(rec_bbox(rec), px, py)) {
+          const uint32_t pj = __shfl_sync(0xffffffffu, pm, j);
+          const bool act = !P.done && ((pj >> lane) & 1u);
+          n_warp_evals += __any_sync(0xffffffffu, act) ? 1u : 0u;
+#ifdef CS_NO_EVAL
+          if (false) {
+#else
+          if (act) {
+#endif
             n_eval++;
             const int pos = (int)first + j;
             if (MAXK == 8) {
@@ -378,6 +445,7 @@ __global__ void __launch_bounds__(kPipeThreads, 4) forward_kernel(BlendArgs a) {
   block_add_u64(a.stats + S_FWD_EVALS, n_eval);
   block_add_u64(a.stats + S_FWD_LINES, n_lines);
   block_add_u64(a.stats + S_FWD_BLENDS, n_blend);
+  block_add_u64(a.stats + S_FWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
 }
 
 // 32 per-lane values -> lane L holds the warp sum of value L.
@@ -469,7 +537,9 @@ template <int MAXK>
 __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) {
   constexpr int AF = Acc<MAXK>::kFloats;
   constexpr int NG = (AF + 31) / 32;  // 32-value groups
-  __shared__ PipeSmem<MAXK> sm;
+  constexpr int kStages = CS_BWD_STAGES;
+  extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
+  PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
   __shared__ int s_last[kConsumers];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -510,9 +580,9 @@ __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) 
     first = (uint32_t)lo;
     count = (uint32_t)(hi - lo);
   };
-  unsigned n_eval = 0, n_lines = 0;
+  unsigned n_eval = 0, n_lines = 0, n_warp_evals = 0;
   if (warp == kConsumers) {
-    pipe_produce<MAXK>(sm, a.records, a.pair_ids, nbatch, batch, false, nullptr);
+    pipe_produce<MAXK, kStages>(sm, a.records, a.pair_ids, nbatch, batch, false, nullptr);
   } else {
     const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2);
     const float qx = px + 0.5f, qy = py + 0.5f;
@@ -522,10 +592,13 @@ __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) 
       uint32_t first, count;
       batch(b, first, count);
       if ((int)first <= warp_last) {
-        bool hit = false;
-        if (lane < (int)count && (int)(first + lane) <= warp_last)
-          hit = box_overlaps(rec_bbox(sm.rec[s][lane]), rx0, ry0);
-        uint32_t m = __ballot_sync(0xffffffffu, hit);
+        // lane j: pixels of this warp's block inside candidate j's bbox that
+        // blended it or something behind it (list position <= their last)
+        const uint32_t pos = first + lane;
+        uint32_t pm = 0u;
+        if (lane < (int)count && (int)pos <= warp_last)
+          pm = block_mask(rec_bbox(sm.rec[s][lane]), rx0, ry0);
+        uint32_t m = __ballot_sync(0xffffffffu, pm != 0u);
         while (m) {
           const int j = 31 - __clz(m);   // back to front
           m &= ~(1u << j);
@@ -534,7 +607,8 @@ __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) 
 #pragma unroll
           for (int f = 0; f < NG * 32; f++) v[f] = 0.f;
           bool contrib = false;
-          if ((int)first + j <= P.last && in_box(rec_bbox(rec), px, py)) {
+          const uint32_t pj = __shfl_sync(0xffffffffu, pm, j);
+          if ((int)first + j <= P.last && ((pj >> lane) & 1u)) {
             n_eval++;
             if (MAXK == 8) {
               switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
@@ -547,6 +621,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) 
               contrib = bwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines);
             }
           }
+          n_warp_evals += __any_sync(0xffffffffu, (int)first + j <= P.last && ((pj >> lane) & 1u)) ? 1u : 0u;
           if (__any_sync(0xffffffffu, contrib)) {
             float *dst = a.accum + (size_t)sm.id[s][j] * AF;
 #pragma unroll
@@ -565,6 +640,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) 
   }
   block_add_u64(a.stats + S_BWD_EVALS, n_eval);
   block_add_u64(a.stats + S_BWD_LINES, n_lines);
+  block_add_u64(a.stats + S_BWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
 }
 
 static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const cs_layout &L, char *ws) {
@@ -601,10 +677,13 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
   a.visible = f.visible;
   if (f.visible && p.n > 0) cudaMemsetAsync(f.visible, 0, (size_t)p.n, s);
   const int tiles = L.tiles_x * L.tiles_y;
-  if (L.max_k == 8)
-    forward_kernel<8><<<tiles, kPipeThreads, 0, s>>>(a);
-  else
-    forward_kernel<16><<<tiles, kPipeThreads, 0, s>>>(a);
+  if (L.max_k == 8) {
+    cudaFuncSetAttribute(forward_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
+    forward_kernel<8><<<tiles, kPipeThreads, sizeof(PipeSmem<8, CS_FWD_STAGES>), s>>>(a);
+  } else {
+    cudaFuncSetAttribute(forward_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_FWD_STAGES>));
+    forward_kernel<16><<<tiles, kPipeThreads, sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
 
@@ -614,10 +693,13 @@ int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs
   a.d_image = d_image;
   if (p.n > 0) cudaMemsetAsync(a.accum, 0, (size_t)p.n * L.acc_floats * sizeof(float), s);
   const int tiles = L.tiles_x * L.tiles_y;
-  if (L.max_k == 8)
-    backward_kernel<8><<<tiles, kPipeThreads, 0, s>>>(a);
-  else
-    backward_kernel<16><<<tiles, kPipeThreads, 0, s>>>(a);
+  if (L.max_k == 8) {
+    cudaFuncSetAttribute(backward_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_BWD_STAGES>));
+    backward_kernel<8><<<tiles, kPipeThreads, sizeof(PipeSmem<8, CS_BWD_STAGES>), s>>>(a);
+  } else {
+    cudaFuncSetAttribute(backward_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_BWD_STAGES>));
+    backward_kernel<16><<<tiles, kPipeThreads, sizeof(PipeSmem<16, CS_BWD_STAGES>), s>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
 

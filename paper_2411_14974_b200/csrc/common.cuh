@@ -52,7 +52,10 @@ enum Counter {
   C_COUNT = 40
 };
 // uint64 work statistics at word C_STATS (roofline accounting, read by the benchmark)
-enum Stat { S_FWD_EVALS = 0, S_FWD_LINES = 1, S_FWD_BLENDS = 2, S_BWD_EVALS = 3, S_BWD_LINES = 4, S_COUNT = 8 };
+enum Stat {
+  S_FWD_EVALS = 0, S_FWD_LINES = 1, S_FWD_BLENDS = 2, S_BWD_EVALS = 3, S_BWD_LINES = 4, S_FWD_WARP_EVALS = 5,
+  S_BWD_WARP_EVALS = 6, S_COUNT = 8
+};
 
 // Block-wide sum of a per-thread count, added once per block to a global u64.
 __device__ __forceinline__ void block_add_u64(unsigned long long *dst, unsigned v) {
@@ -142,12 +145,24 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t phas
       : "memory");
   return done != 0;
 }
+// Waiting warps back off with __nanosleep so they do not steal issue slots
+// from the warps doing work (a suspend-time hint alone wakes on every
+// barrier event of the CTA).
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   if (mbar_try_wait(bar, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-  for (uint32_t it = 1; !mbar_try_wait_sleep(bar, phase); it++) {
-    if ((it & 63u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
+#ifdef CS_WAIT_SLEEP
+  uint32_t ns = 32;
+  for (uint32_t it = 1; !mbar_try_wait(bar, phase); it++) {
+    __nanosleep(ns);
+    ns = min(ns * 2u, 256u);
+    if ((it & 255u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
   }
+#else
+  for (uint32_t it = 1; !mbar_try_wait_sleep(bar, phase); it++) {
+    if ((it & 255u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
+  }
+#endif
 }
 
 // Pixel of a 16x16 tile handled by thread t: warps cover 8x4 sub-blocks so

@@ -24,7 +24,8 @@ from .model import (EXACT_SETTINGS, SH_COEFFS, Camera, GradientBuffer, RenderOut
 from .scene_tensors import SceneTensors, as_scene_tensors
 
 _COUNTERS = 40
-STAT_NAMES = ("fwd_evals", "fwd_line_evals", "fwd_blends", "bwd_evals", "bwd_line_evals")
+STAT_NAMES = ("fwd_evals", "fwd_line_evals", "fwd_blends", "bwd_evals", "bwd_line_evals", "fwd_warp_evals",
+              "bwd_warp_evals")
 
 
 def _device(device=None) -> torch.device:

@@ -59,3 +59,21 @@ for name, wx, wy, px, py in (("1px 8x4 warps", 8, 4, 1, 1), ("1px 16x2 warps", 1
     mufu = we * ((nl_w + 3) + 3 * (ppt - 1))
     print(f"{name:22s} warp-evals {we:9d}  SIMT eff {evals / (lanes * ppt):.3f}  thread-eff {te / lanes:.3f}"
           f"  MUFU warp-instr {mufu / 1e6:7.2f}M  (x{mufu / (evals / 32 * (nl_w + 3)):.2f} ideal)")
+
+# "own list" layout: every lane walks its own pixel's candidates of a stage
+# (kStageCands consecutive list entries) in order; a warp-stage costs
+# max-over-lanes rounds.  Efficiency = pixel evals / (32 * rounds).
+starts = np.concatenate([[0], np.cumsum([off[t + 1] - off[t] for t in tl])])
+for stage in (16, 32, 64):
+    rounds = 0
+    cand_iters = 0
+    for ti in range(tl.size):
+        g = grid[starts[ti]:starts[ti + 1]]                  # [cand, 16, 16]
+        blocks = g.reshape(-1, 4, 4, 2, 8).transpose(0, 1, 3, 2, 4).reshape(-1, 8, 32)  # [cand, warp, lane]
+        for s0 in range(0, blocks.shape[0], stage):
+            st_ = blocks[s0:s0 + stage]                      # [c, warp, lane]
+            per_lane = st_.sum(axis=0)                       # [warp, lane]
+            rounds += int(per_lane.max(axis=1).sum())
+            cand_iters += int(st_.any(axis=2).sum())         # current scheme: candidates per warp
+    print(f"own-list, stage {stage:3d}: SIMT eff {evals / (32 * rounds):.3f}  rounds {rounds}  "
+          f"(per-candidate scheme: {cand_iters} warp-evals, eff {evals / (32 * cand_iters):.3f})")
