@@ -281,7 +281,7 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
 }
 
 // SH colour in float32 (harmonics.py:33-59, 101-109): continuous output,
-// checked at 1e-4, so it needs no float64.  sh: 16x3 floats in smem.
+// checked at 1e-4, so it needs no float64.  sh: the convex's 16x3 floats.
 __device__ __forceinline__ void sh_colour(float x, float y, float z, int deg, const float *sh, float *col) {
   float b[kShCoeffs];
   b[0] = 0.28209479177387814f;
@@ -310,7 +310,7 @@ __device__ __forceinline__ void sh_colour(float x, float y, float z, int deg, co
 #pragma unroll
   for (int q = 0; q < kShCoeffs * 3 / 4; q++) {  // 4 coefficients of 3 channels = 3 float4
     if (4 * q < 3 * nb) {
-      const float4 v = sh4[q];
+      const float4 v = __ldg(sh4 + q);
       const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int r = 0; r < 4; r++) {
@@ -323,11 +323,20 @@ __device__ __forceinline__ void sh_colour(float x, float y, float z, int deg, co
   for (int c = 0; c < 3; c++) col[c] = fmaxf(0.5f + acc[c], 0.f);
 }
 
-// One convex.  pts_s / sh_s: this convex's rows staged in smem by TMA;
-// X, Y: this thread's projected-pixel slots in smem (stride kPreThreads).
+// One convex.  pts_s: this convex's points staged in smem by TMA; X, Y:
+// this thread's projected-pixel slots in smem (stride kPreThreads).
+//
+// Order of work: projection + cull, hull, then depth / activations / margin,
+// then ONE loop over the hull edges that computes each line (hull_lines),
+// writes its blend coefficients and inflates the vertex it starts at
+// (bbox_with_margin) -- the per-line arrays never exist, which keeps the
+// register footprint (and so the occupancy of this latency-bound float64
+// kernel) in check.  Every value is computed by the same expression as in the
+// reference, so the discrete results are unchanged.  The anchor of the
+// anchor-relative line offsets is the integer pixel at hull vertex 0.
 template <int MAXK>
-__device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, const float *sh_s,
-                                               uint64_t *sh_bar, double *X, double *Y) {
+__device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, double *X,
+                                               double *Y) {
   const int k = a.k;
   a.touched[i] = 0u;
   a.depth_keys[i] = kCulledKey;
@@ -361,21 +370,6 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   NibbleList hull;
   const int h = graham_scan_packed(k, X, Y, kPreThreads, hull);
   if (h == 0) return false;
-  // projection.py:116-128 (static register slots, j < h)
-  double nx[MAXK], ny[MAXK], off[MAXK];
-#pragma unroll
-  for (int j = 0; j < MAXK; j++) {
-    if (j < h) {
-      const int u = hull.get(j), v = hull.get(j + 1 < h ? j + 1 : 0);
-      const double ux = X[u * kPreThreads], uy = Y[u * kPreThreads];
-      const double ex = X[v * kPreThreads] - ux, ey = Y[v * kPreThreads] - uy;
-      const double rx = ey, ry = -ex;
-      const double len = sqrt(rx * rx + ry * ry);
-      nx[j] = rx / len;
-      ny[j] = ry / len;
-      off[j] = -(nx[j] * ux + ny[j] * uy);
-    }
-  }
   // rasterize.py:99-103
   const double depth = zsum / k;
   const double s = depth_scale(a.mode, a.cam.ortho ? 1.0 : depth);
@@ -383,34 +377,72 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   const double sigma_s = s * exp((double)a.raw_sigma[i]);
   const float ro = a.raw_opacity[i];
   const double o = 1.0 / (1.0 + exp(-(double)ro));
-  // projection.py:136-177
+  // projection.py:157-163
   if (o <= a.cutoff) return false;
-  int x0, x1, y0, y1;
-  if (a.cutoff <= 0.0) {
-    x0 = 0; x1 = a.cam.width; y0 = 0; y1 = a.cam.height;
-  } else {
+  const bool full_frame = a.cutoff <= 0.0;
+  double margin = 0.0;
+  if (!full_frame) {
     double eps = a.cutoff / o;
     if (0.5 < eps) eps = 0.5;
-    const double margin = log((1.0 - eps) / eps) / (sigma_s * delta_s);
-    double pnx = 0.0, pny = 0.0;  // normal of the line ending at vertex 0 (line h-1)
+    margin = log((1.0 - eps) / eps) / (sigma_s * delta_s);
+  }
+  const int v0 = hull.get(0);
+  const double axd = floor(X[v0 * kPreThreads]), ayd = floor(Y[v0 * kPreThreads]);
+  const double dls = delta_s * 1.4426950408889634;  // delta_s * log2(e)
+  constexpr int RF = Rec<MAXK>::kFloats;
+  float4 *dst = reinterpret_cast<float4 *>(a.records + i * RF);
+  // line of edge j (projection.py:116-128): from vertex hull[j] to hull[j+1]
+  auto line = [&](int j, double &nx, double &ny, double &off) {
+    const int u = hull.get(j), v = hull.get(j + 1 < h ? j + 1 : 0);
+    const double ux = X[u * kPreThreads], uy = Y[u * kPreThreads];
+    const double ex = X[v * kPreThreads] - ux, ey = Y[v * kPreThreads] - uy;
+    const double rx = ey, ry = -ex;
+    const double len = sqrt(rx * rx + ry * ry);
+    nx = rx / len;
+    ny = ry / len;
+    off = -(nx * ux + ny * uy);
+  };
+  double pnx, pny;  // normal of the line ending at the current vertex (projection.py:167)
+  {
+    double poff;
+    line(h - 1, pnx, pny, poff);
+  }
+  double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+  float buf[4];
 #pragma unroll
-    for (int j = 0; j < MAXK; j++)
-      if (j == h - 1) { pnx = nx[j]; pny = ny[j]; }
-    double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < MAXK; j++) {
-      if (j < h) {
+  for (int j = 0; j < MAXK; j++) {
+    float e3[3] = {0.f, 0.f, -INFINITY};   // padding line: 2^z = 0
+    if (j < h) {
+      double nx, ny, off;
+      line(j, nx, ny, off);
+      // blend coefficients, anchor-relative offset formed in float64
+      e3[0] = (float)(dls * nx);
+      e3[1] = (float)(dls * ny);
+      e3[2] = (float)(dls * (off + nx * axd + ny * ayd));
+      if (!full_frame) {  // projection.py:167-169, vertex j
         const int u = hull.get(j);
-        double den = 1.0 + (pnx * nx[j] + pny * ny[j]);
+        double den = 1.0 + (pnx * nx + pny * ny);
         if (!(den >= 1e-12)) den = 1e-12;
-        const double ix = X[u * kPreThreads] + (margin * (pnx + nx[j])) / den;
-        const double iy = Y[u * kPreThreads] + (margin * (pny + ny[j])) / den;
+        const double ix = X[u * kPreThreads] + (margin * (pnx + nx)) / den;
+        const double iy = Y[u * kPreThreads] + (margin * (pny + ny)) / den;
         xmin = fmin(xmin, ix); xmax = fmax(xmax, ix);
         ymin = fmin(ymin, iy); ymax = fmax(ymax, iy);
-        pnx = nx[j];
-        pny = ny[j];
       }
+      pnx = nx;
+      pny = ny;
     }
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      const int f = 3 * j + c;
+      buf[f & 3] = e3[c];
+      if ((f & 3) == 3) dst[R_HEADER / 4 + f / 4] = make_float4(buf[0], buf[1], buf[2], buf[3]);
+    }
+  }
+  // projection.py:170-177
+  int x0, x1, y0, y1;
+  if (full_frame) {
+    x0 = 0; x1 = a.cam.width; y0 = 0; y1 = a.cam.height;
+  } else {
     double fx0 = ceil(xmin - 0.5), fx1 = floor(xmax - 0.5) + 1.0;
     double fy0 = ceil(ymin - 0.5), fy1 = floor(ymax - 0.5) + 1.0;
     fx0 = fmax(fx0, 0.0); fy0 = fmax(fy0, 0.0);
@@ -418,7 +450,7 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
     if (!(fx0 < fx1) || !(fy0 < fy1)) return false;
     x0 = (int)fx0; x1 = (int)fx1; y0 = (int)fy0; y1 = (int)fy1;
   }
-  // ---- outputs: discrete state, then the float32 blend record ----
+  // ---- outputs: discrete state, then the float32 record header ----
   uint8_t hb[MAXK];
 #pragma unroll
   for (int j = 0; j < MAXK; j++) hb[j] = (uint8_t)(j < h ? hull.get(j) : 0xff);
@@ -433,35 +465,15 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   a.bbox[i] = make_int4(x0, x1, y0, y1);
   a.touched[i] = (uint32_t)(((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1));
   a.depth_keys[i] = orderable_bits(depth);
-
-  constexpr int RF = Rec<MAXK>::kFloats;
-  float4 *dst = reinterpret_cast<float4 *>(a.records + i * RF);
-  const int ax = (x0 + x1) >> 1, ay = (y0 + y1) >> 1;
-  const double dls = delta_s * 1.4426950408889634;  // delta_s * log2(e)
-#pragma unroll
-  for (int q = 0; q < 3 * MAXK / 4; q++) {  // line coefficients, anchor-relative offset in fp64
-    float e[4];
-#pragma unroll
-    for (int r = 0; r < 4; r++) {
-      const int f = 4 * q + r, j = f / 3, c = f % 3;
-      if (j < h) {
-        e[r] = c == 0 ? (float)(dls * nx[j]) : c == 1 ? (float)(dls * ny[j])
-                                                      : (float)(dls * (off[j] + nx[j] * ax + ny[j] * ay));
-      } else {
-        e[r] = c == 2 ? -INFINITY : 0.f;
-      }
-    }
-    dst[R_HEADER / 4 + q] = make_float4(e[0], e[1], e[2], e[3]);
-  }
-  // rasterize.py:110-114 view direction; harmonics.py:101-109 colour
+  // rasterize.py:110-114 view direction; harmonics.py:101-109 colour (float32,
+  // SH rows read straight from global: 12 x 16-byte loads per thread)
   const double dvx = cx / k - a.cam_center[0], dvy = cy / k - a.cam_center[1], dvz = cz / k - a.cam_center[2];
   const double dist = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
   float dx = 0.f, dy = 0.f, dz = 1.f;
   if (dist > 0.0) { dx = (float)(dvx / dist); dy = (float)(dvy / dist); dz = (float)(dvz / dist); }
-  mbar_wait(sh_bar, 0);  // SH rows landed (TMA issued at kernel start)
   float col[3];
-  sh_colour(dx, dy, dz, a.sh_degree, sh_s, col);
-  dst[0] = make_float4((float)ax, (float)ay, (float)sigma_s, (float)o);
+  sh_colour(dx, dy, dz, a.sh_degree, a.sh + i * kShCoeffs * 3, col);
+  dst[0] = make_float4((float)axd, (float)ayd, (float)sigma_s, (float)o);
   dst[1] = make_float4(col[0], col[1], col[2], (float)depth);
   dst[2] = make_float4(1.f / (1.f + __expf(ro)), (float)dls, __int_as_float(h), (float)(1.0 / dls));
   dst[3] = make_float4(__int_as_float(x0), __int_as_float(x1), __int_as_float(y0), __int_as_float(y1));
@@ -469,44 +481,35 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
 }
 
 template <int MAXK>
-__global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(PreArgs a) {
-  // dynamic smem: X[MAXK][threads], Y[MAXK][threads] (f64), SH[threads][48], points[threads][k*3] (f32)
+__global__ void __launch_bounds__(kPreThreads, 6) preprocess_kernel(PreArgs a) {
+  // dynamic smem: X[MAXK][threads], Y[MAXK][threads] (f64), points[threads][k*3] (f32)
   extern __shared__ __align__(16) double pre_smem[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[1];
   double *Xs = pre_smem, *Ys = pre_smem + MAXK * kPreThreads;
-  float *sh_smem = reinterpret_cast<float *>(pre_smem + 2 * MAXK * kPreThreads);
-  float *pts_smem = sh_smem + kPreThreads * kShCoeffs * 3;
+  float *pts_smem = reinterpret_cast<float *>(pre_smem + 2 * MAXK * kPreThreads);
   const int64_t base = (int64_t)blockIdx.x * kPreThreads;
   const int rowf = a.k * 3;
   const int64_t nblk = min((int64_t)kPreThreads, a.n - base);
   const bool full = nblk == kPreThreads;  // full blocks: 16B-aligned, in-bounds bulk copies
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (full) {
     if (threadIdx.x == 0) {
-      const uint32_t pbytes = kPreThreads * rowf * 4, sbytes = kPreThreads * kShCoeffs * 3 * 4;
+      const uint32_t pbytes = kPreThreads * rowf * 4;
       mbar_expect_tx(&bars[0], pbytes);
       tma_bulk_g2s(pts_smem, a.points + base * rowf, pbytes, &bars[0]);
-      mbar_expect_tx(&bars[1], sbytes);
-      tma_bulk_g2s(sh_smem, a.sh + base * kShCoeffs * 3, sbytes, &bars[1]);
     }
     mbar_wait(&bars[0], 0);
   } else {  // tail block: plain coalesced loads
     for (int q = threadIdx.x; q < nblk * rowf; q += kPreThreads) pts_smem[q] = a.points[base * rowf + q];
-    for (int q = threadIdx.x; q < nblk * kShCoeffs * 3; q += kPreThreads)
-      sh_smem[q] = a.sh[base * kShCoeffs * 3 + q];
     __syncthreads();
-    if (threadIdx.x == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[1])) : "memory");
   }
   const int64_t i = base + threadIdx.x;
   bool vis = false;
-  if (i < a.n)
-    vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, sh_smem + threadIdx.x * kShCoeffs * 3, &bars[1],
-                               Xs + threadIdx.x, Ys + threadIdx.x);
+  if (i < a.n) vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, Xs + threadIdx.x, Ys + threadIdx.x);
   unsigned b = __ballot_sync(0xffffffffu, vis);
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(&a.counters[C_NVISIBLE], (unsigned)__popc(b));
   // range of the visible depth keys (block reduce, one atomic pair per block)
@@ -528,7 +531,6 @@ __global__ void __launch_bounds__(kPreThreads, 4) preprocess_kernel(PreArgs a) {
       atomicMax(reinterpret_cast<unsigned long long *>(a.counters + C_KMAX), s_kmax);
     }
   }
-  if (threadIdx.x == 0) mbar_wait(&bars[1], 0);  // never leave while a bulk copy still targets this smem
 }
 
 // cs_graham_scan_batch: one thread per point set.
@@ -584,7 +586,7 @@ int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_par
   a.counters = reinterpret_cast<uint32_t *>(ws + L.counters);
   camera_center(cam, a.cam_center);
   const int blocks = (int)((p.n + kPreThreads - 1) / kPreThreads);
-  const size_t smem = (size_t)kPreThreads * (2 * L.max_k * sizeof(double) + (kShCoeffs * 3 + p.k * 3) * sizeof(float));
+  const size_t smem = (size_t)kPreThreads * (2 * L.max_k * sizeof(double) + p.k * 3 * sizeof(float));
   if (L.max_k == 8) {
     cudaFuncSetAttribute(preprocess_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     preprocess_kernel<8><<<blocks, kPreThreads, smem, s>>>(a);
