@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 1
+#define CS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define CS_API __attribute__((visibility("default")))
@@ -178,6 +178,60 @@ CS_API int cs_read_counters(const void *workspace, uint32_t *host_out4, void *st
  * hull_n [m] (0 == None). */
 CS_API int cs_graham_scan_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts,
                          int32_t *hull, int32_t *hull_n, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Training-step kernels (the callers on either side of the hot path; SURVEY
+ * section 8(f)): the image loss that produces d_image, the per-view
+ * sigma-signal of the density control, and the Adam update.
+ * ---------------------------------------------------------------------- */
+
+/* Per-view densification signal (trainer.py:192-193), accumulated by the
+ * backward's chain stage: sigma_signal += |this view's d_raw_sigma| * visible,
+ * sigma_views += visible.  visible = that view's RenderOutput.visible. */
+typedef struct cs_view_signal {
+    float *sigma_signal;      /* [n] */
+    float *sigma_views;       /* [n] */
+    const uint8_t *visible;   /* [n] */
+} cs_view_signal;
+
+/* cs_backward + the per-view signal (signal may be NULL). */
+CS_API int cs_backward_signal(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                              void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                              const float *d_image, const cs_grads *grads, const cs_view_signal *signal,
+                              void *stream);
+
+/* Scratch bytes cs_image_loss needs for an H x W image. Host-only. */
+CS_API int cs_image_loss_workspace(int32_t height, int32_t width, size_t *bytes);
+
+/* Training loss.  Replaces losses.image_loss (losses.py:129-155) with
+ * ssim_with_grad (losses.py:58-101): (1-lambda) L1 + lambda (1-SSIM)/2 +
+ * beta mean(sigmoid(raw_mask)), 11x11 sigma-1.5 Gaussian on the valid region.
+ * rendered/target [H,W,3]; d_image [H,W,3] is WRITTEN (d loss / d rendered);
+ * d_raw_mask [n] is ACCUMULATED (+=) like trainer.py:176.  stats[4] (device,
+ * written): sum |rendered - target|, sum over channels of sum of the SSIM map,
+ * sum sigmoid(raw_mask), number of valid SSIM positions per channel.
+ * total = (1-lambda) stats0/(3HW) + lambda (1 - stats1/(3 stats3))/2 + beta stats2/n. */
+CS_API int cs_image_loss(int32_t height, int32_t width, const float *rendered, const float *target,
+                         const float *raw_mask, int64_t n, double lambda_dssim, double beta_mask,
+                         float *d_image, float *d_raw_mask, double *stats, void *workspace,
+                         size_t workspace_bytes, void *stream);
+
+/* One parameter tensor of the Adam update. */
+typedef struct cs_adam_tensor {
+    float *param;
+    const float *grad;
+    float *m;
+    float *v;
+    int64_t numel;
+    double lr;
+} cs_adam_tensor;
+
+/* optim.Adam.step (optim.py:22-35) over `count` (<= 8) tensors, in place:
+ * g = grad_scale * grad; m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+ * p -= lr (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps).
+ * `tensors` is a HOST array; step is the 1-based step count. */
+CS_API int cs_adam_step(int32_t count, const cs_adam_tensor *tensors, double beta1, double beta2, double eps,
+                        int32_t step, double grad_scale, void *stream);
 
 #ifdef __cplusplus
 }

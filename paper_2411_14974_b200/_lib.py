@@ -12,8 +12,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libconvexsplat_sm100.so")
 
 EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forward", "cs_backward",
-           "cs_forward_stages", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch")
-ABI_VERSION = 1
+           "cs_forward_stages", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
+           "cs_backward_signal", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step")
+ABI_VERSION = 2
 
 _vp = ctypes.c_void_p
 
@@ -46,6 +47,15 @@ class CsFrame(ctypes.Structure):
 class CsGrads(ctypes.Structure):
     _fields_ = [("d_points", _vp), ("d_raw_delta", _vp), ("d_raw_sigma", _vp),
                 ("d_raw_opacity", _vp), ("d_raw_mask", _vp), ("d_sh", _vp)]
+
+
+class CsViewSignal(ctypes.Structure):
+    _fields_ = [("sigma_signal", _vp), ("sigma_views", _vp), ("visible", _vp)]
+
+
+class CsAdamTensor(ctypes.Structure):
+    _fields_ = [("param", _vp), ("grad", _vp), ("m", _vp), ("v", _vp), ("numel", ctypes.c_int64),
+                ("lr", ctypes.c_double)]
 
 
 class CsLayout(ctypes.Structure):
@@ -88,8 +98,15 @@ def load(path: str = None):
     L.cs_backward_stages.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.c_int32, ctypes.c_int32, _vp]
     L.cs_read_counters.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), _vp]
     L.cs_graham_scan_batch.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]
+    L.cs_backward_signal.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.POINTER(CsViewSignal), _vp]
+    L.cs_image_loss_workspace.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
+    L.cs_image_loss.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_double,
+                                ctypes.c_double, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+    L.cs_adam_step.argtypes = [ctypes.c_int32, ctypes.POINTER(CsAdamTensor), ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_int32, ctypes.c_double, _vp]
     for fn in ("cs_workspace_layout", "cs_forward", "cs_backward", "cs_forward_stages", "cs_backward_stages",
-               "cs_read_counters", "cs_graham_scan_batch"):
+               "cs_read_counters", "cs_graham_scan_batch", "cs_backward_signal", "cs_image_loss_workspace",
+               "cs_image_loss", "cs_adam_step"):
         getattr(L, fn).restype = ctypes.c_int
     if L.cs_abi_version() != ABI_VERSION:
         raise CsError(f"ABI mismatch: library {L.cs_abi_version()} != {ABI_VERSION}")

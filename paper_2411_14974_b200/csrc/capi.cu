@@ -110,9 +110,9 @@ int cs_forward(const cs_camera *cam, const cs_settings *set, const cs_params *pa
   return cs_forward_stages(cam, set, params, workspace, workspace_bytes, pair_capacity, frame, 0, 2, stream);
 }
 
-int cs_backward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
-                       size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
-                       int32_t first_stage, int32_t last_stage, void *stream) {
+static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                         size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
+                         const cs_view_signal *sig, int32_t first_stage, int32_t last_stage, void *stream) {
   if (!params || !grads || !workspace || !d_image) return CS_ERR_ARG;
   if (first_stage < 0 || last_stage > 1 || first_stage > last_stage) return CS_ERR_ARG;
   cs_layout L;
@@ -126,15 +126,58 @@ int cs_backward_stages(const cs_camera *cam, const cs_settings *set, const cs_pa
   char *ws = static_cast<char *>(workspace);
   if (first_stage == 0)
     if ((rc = cs::launch_backward_blend(*cam, *set, *params, L, ws, d_image, s))) return rc;
-  if (last_stage == 1) return cs::launch_chain(*cam, *set, *params, L, ws, *grads, s);
+  if (last_stage == 1) return cs::launch_chain(*cam, *set, *params, L, ws, *grads, sig, s);
   return CS_OK;
+}
+
+int cs_backward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                       size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
+                       int32_t first_stage, int32_t last_stage, void *stream) {
+  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, nullptr,
+                       first_stage, last_stage, stream);
 }
 
 int cs_backward(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
                 size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
                 void *stream) {
-  return cs_backward_stages(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, 0, 1,
-                            stream);
+  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, nullptr, 0, 1,
+                       stream);
+}
+
+int cs_backward_signal(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                       size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
+                       const cs_view_signal *signal, void *stream) {
+  if (signal && (!signal->sigma_signal || !signal->sigma_views || !signal->visible)) return CS_ERR_ARG;
+  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, signal, 0, 1,
+                       stream);
+}
+
+int cs_image_loss_workspace(int32_t height, int32_t width, size_t *bytes) {
+  if (!bytes || height < 11 || width < 11) return CS_ERR_ARG;   // losses.py:60-63
+  *bytes = sizeof(float) * 9 * (size_t)(height - 10) * (size_t)(width - 10);
+  return CS_OK;
+}
+
+int cs_image_loss(int32_t height, int32_t width, const float *rendered, const float *target, const float *raw_mask,
+                  int64_t n, double lambda_dssim, double beta_mask, float *d_image, float *d_raw_mask,
+                  double *stats, void *workspace, size_t workspace_bytes, void *stream) {
+  size_t need = 0;
+  int rc = cs_image_loss_workspace(height, width, &need);
+  if (rc) return rc;
+  if (!rendered || !target || !d_image || !stats || !workspace || n < 0 || (n > 0 && !raw_mask)) return CS_ERR_ARG;
+  if (workspace_bytes < need) return CS_ERR_WORKSPACE;
+  return cs::launch_image_loss(height, width, rendered, target, raw_mask, n, lambda_dssim, beta_mask, d_image,
+                               d_raw_mask, stats, workspace, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cs_adam_step(int32_t count, const cs_adam_tensor *tensors, double beta1, double beta2, double eps, int32_t step,
+                 double grad_scale, void *stream) {
+  if (count < 0 || count > 8 || (count > 0 && !tensors) || step < 1) return CS_ERR_ARG;
+  for (int k = 0; k < count; k++)
+    if (tensors[k].numel < 0 || (tensors[k].numel > 0 && (!tensors[k].param || !tensors[k].grad ||
+                                                          !tensors[k].m || !tensors[k].v)))
+      return CS_ERR_ARG;
+  return cs::launch_adam(count, tensors, beta1, beta2, eps, step, grad_scale, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int cs_read_counters(const void *workspace, uint32_t *host_out4, void *stream) {

@@ -33,6 +33,7 @@ struct ChainArgs {
   const uint8_t *hull;
   const uint32_t *touched;
   cs_grads g;
+  cs_view_signal sig;   // sigma_signal == nullptr: no densification signal
 };
 
 template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 128 : 64; }
@@ -282,7 +283,13 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
     }
   }
   a.g.d_raw_delta[i] += (float)(ddel * s * delta);
-  a.g.d_raw_sigma[i] += (float)(dsig * s * sigma);
+  const float d_rs = (float)(dsig * s * sigma);
+  a.g.d_raw_sigma[i] += d_rs;
+  if (a.sig.sigma_signal) {   // trainer.py:192-193, this view's contribution only
+    const float vis = a.sig.visible[i] ? 1.f : 0.f;
+    a.sig.sigma_signal[i] += fabsf(d_rs) * vis;
+    a.sig.sigma_views[i] += vis;
+  }
   const float o = 1.f / (1.f + __expf(-a.raw_opacity[i]));
   const float m = 1.f / (1.f + __expf(-a.raw_mask[i]));
   const float doe = (float)acc[A_DOEFF];
@@ -291,7 +298,7 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
 }
 
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                 const cs_layout &L, char *ws, const cs_grads &g, cudaStream_t s) {
+                 const cs_layout &L, char *ws, const cs_grads &g, const cs_view_signal *sig, cudaStream_t s) {
   if (p.n == 0) return CS_OK;
   ChainArgs a;
   a.cam = cam;
@@ -311,6 +318,7 @@ int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &
   a.hull = reinterpret_cast<const uint8_t *>(ws + L.hull);
   a.touched = reinterpret_cast<const uint32_t *>(ws + L.tiles_touched);
   a.g = g;
+  a.sig = sig ? *sig : cs_view_signal{nullptr, nullptr, nullptr};
   if (L.max_k == 8)
     chain_kernel<8><<<(int)((p.n + 127) / 128), chain_threads<8>(), 0, s>>>(a);
   else

@@ -186,7 +186,12 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
 int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                           const cs_layout &L, char *ws, const float *d_image, cudaStream_t s);
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                 const cs_layout &L, char *ws, const cs_grads &g, cudaStream_t s);
+                 const cs_layout &L, char *ws, const cs_grads &g, const cs_view_signal *sig, cudaStream_t s);
+int launch_image_loss(int H, int W, const float *img, const float *tgt, const float *raw_mask, int64_t n,
+                      double lam, double beta, float *d_image, float *d_raw_mask, double *stats, void *ws,
+                      cudaStream_t s);
+int launch_adam(int count, const cs_adam_tensor *tensors, double b1, double b2, double eps, int step,
+                double gscale, cudaStream_t s);
 int launch_hull_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts,
                       int32_t *hull, int32_t *hull_n, cudaStream_t s);
 size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, struct Scratch *sc, char *base);

@@ -167,6 +167,9 @@ __device__ __forceinline__ double depth_scale(int mode, double d) {  // field.py
 }
 
 constexpr int kPreThreads = 128;
+#ifndef CS_PRE_BLOCKS
+#define CS_PRE_BLOCKS 6   // resident blocks per SM (register budget 85)
+#endif
 
 // Index list of up to 16 entries packed as 4-bit nibbles in a register, so
 // the Graham scan's insert / erase / pop keep no per-thread local memory.
@@ -481,7 +484,7 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
 }
 
 template <int MAXK>
-__global__ void __launch_bounds__(kPreThreads, 6) preprocess_kernel(PreArgs a) {
+__global__ void __launch_bounds__(kPreThreads, CS_PRE_BLOCKS) preprocess_kernel(PreArgs a) {
   // dynamic smem: X[MAXK][threads], Y[MAXK][threads] (f64), points[threads][k*3] (f32)
   extern __shared__ __align__(16) double pre_smem[];
   __shared__ __align__(8) uint64_t bars[1];

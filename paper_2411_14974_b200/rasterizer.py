@@ -201,12 +201,23 @@ class Rasterizer:
                                                  stream), "cs_forward_stages")
 
     def launch_backward(self, fr: Frame, d_image: torch.Tensor, grads: dict, first_stage: int = 0,
-                        last_stage: int = 1):
-        """Backward stages (0 blend, 1 chain) into ``grads`` (+=), no sync."""
+                        last_stage: int = 1, signal=None):
+        """Backward stages (0 blend, 1 chain) into ``grads`` (+=), no sync.
+        ``signal`` = (sigma_signal, sigma_views, visible) tensors: also
+        accumulate the view's densification signal (trainer.py:192-193)."""
         g = _lib.CsGrads(grads["points"].data_ptr(), grads["raw_delta"].data_ptr(), grads["raw_sigma"].data_ptr(),
                          grads["raw_opacity"].data_ptr(), grads["raw_mask"].data_ptr(), grads["sh"].data_ptr())
         ws = fr.workspace
         stream = torch.cuda.current_stream(self.device).cuda_stream
+        if signal is not None:
+            if (first_stage, last_stage) != (0, 1):
+                raise ValueError("the sigma signal needs the full backward")
+            sig = _lib.CsViewSignal(signal[0].data_ptr(), signal[1].data_ptr(), signal[2].data_ptr())
+            _lib.check(_lib.load().cs_backward_signal(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
+                                                      ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
+                                                      d_image.data_ptr(), ctypes.byref(g), ctypes.byref(sig),
+                                                      stream), "cs_backward_signal")
+            return
         _lib.check(_lib.load().cs_backward_stages(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
                                                   ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
                                                   d_image.data_ptr(), ctypes.byref(g), first_stage, last_stage,

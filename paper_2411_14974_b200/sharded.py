@@ -10,9 +10,11 @@ because it cannot be formed from the summed gradient.  One all_reduce(SUM)
 over NCCL combines the buffer; every rank then applies the identical Adam step
 (optim.py:12-35, position schedule optim.py:56-61), so replicas stay equal.
 
-The loss mirrors losses.py:129-155 (L1 + D-SSIM with an 11x11 sigma-1.5
-Gaussian valid window + beta * mean sigmoid(mask)); its gradient w.r.t. the
-rendered image comes from torch autograd of the same expression.
+On the GPU the loss (losses.py:129-155: L1 + D-SSIM with an 11x11 sigma-1.5
+Gaussian valid window + beta * mean sigmoid(mask)) and its image gradient come
+from the fused CUDA kernels of ``train_ops`` and the update from one fused
+Adam launch; the torch formulation below (``image_loss``, ``Adam``) is the
+reference the tests compare against and the CPU (gloo) tests use.
 """
 from __future__ import annotations
 
@@ -110,12 +112,14 @@ class Adam:
         self.v = {k: torch.zeros_like(v) for k, v in params.items()}
 
     @torch.no_grad()
-    def step(self, params: dict, grads: dict, lrs: dict):
+    def step(self, params: dict, grads: dict, lrs: dict, grad_scale: float = 1.0):
         self.step_count += 1
         bc1 = 1.0 - self.beta1 ** self.step_count
         bc2 = 1.0 - self.beta2 ** self.step_count
         for name, p in params.items():
             g, m, v = grads[name], self.m[name], self.v[name]
+            if grad_scale != 1.0:
+                g = g * grad_scale
             m.mul_(self.beta1).add_(g, alpha=1.0 - self.beta1)
             v.mul_(self.beta2).addcmul_(g, g, value=1.0 - self.beta2)
             denom = (v / bc2).sqrt_().add_(self.eps)
@@ -171,7 +175,11 @@ class ViewShardedStep:
         n = params["points"].shape[0]
         self.flat = FlatGrads({k: tuple(v.shape) for k, v in params.items()}, n, params["points"].device,
                               params["points"].dtype)
-        self.adam = Adam(params)
+        if params["points"].device.type == "cuda":
+            from .train_ops import FusedAdam
+            self.adam = FusedAdam(params)      # one cs_adam_step launch for all six tensors
+        else:
+            self.adam = Adam(params)
         self.view_grad_fn = view_grad_fn
         self.iteration = 0
 
@@ -182,41 +190,71 @@ class ViewShardedStep:
                 "raw_mask": c.lr_mask}
 
     def accumulate(self, batch: list) -> dict:
-        """Local part: this rank's views, gradients summed into the flat buffer."""
+        """Local part: this rank's views, gradients summed into the flat buffer.
+        A view function with ``handles_signal`` accumulates the per-view sigma
+        signal itself (the CUDA path does it inside the backward's chain
+        kernel); otherwise it is formed here from the gradient difference."""
         self.flat.zero_()
         grads = self.flat.grads()
-        sigma_prev = torch.empty_like(grads["raw_sigma"])
+        signal = {"sigma_signal": self.flat.views["sigma_signal"], "sigma_views": self.flat.views["sigma_views"]}
+        own = getattr(self.view_grad_fn, "handles_signal", False)
+        sigma_prev = None if own else torch.empty_like(grads["raw_sigma"])
         losses = []
         for view in shard_views(batch, self.rank, self.world):
-            sigma_prev.copy_(grads["raw_sigma"])
-            loss, visible = self.view_grad_fn(view, grads)
-            # trainer.py:192-193: per-view |d_raw_sigma| on the visible primitives
-            vis = visible.to(self.flat.buffer.dtype)
-            self.flat.views["sigma_signal"].add_((grads["raw_sigma"] - sigma_prev).abs_() * vis)
-            self.flat.views["sigma_views"].add_(vis)
-            losses.append(loss.detach().reshape(()))
+            if own:
+                loss = self.view_grad_fn(view, grads, signal)
+            else:
+                sigma_prev.copy_(grads["raw_sigma"])
+                loss, visible = self.view_grad_fn(view, grads)
+                # trainer.py:192-193: per-view |d_raw_sigma| on the visible primitives
+                vis = visible.to(self.flat.buffer.dtype)
+                signal["sigma_signal"].add_((grads["raw_sigma"] - sigma_prev).abs_() * vis)
+                signal["sigma_views"].add_(vis)
+            losses.append(loss.detach().reshape(()).to(self.flat.buffer.dtype))
         total = torch.stack(losses).sum() if losses else torch.zeros((), device=self.flat.buffer.device)
         return {"local_views": len(losses), "local_loss_sum": total}
 
     def reduce(self, batch_size: int):
-        """The single collective: sum of everyone's gradients, then / B."""
+        """The single collective: sum of everyone's gradients (the 1/B of the
+        batch mean is applied inside the optimiser step)."""
         if self.world > 1:
             dist.all_reduce(self.flat.buffer, op=dist.ReduceOp.SUM, group=self.group)
-        for k in self.flat.names:
-            self.flat.views[k].div_(batch_size)
 
     def step(self, batch: list) -> dict:
         self.iteration += 1
         info = self.accumulate(batch)
         self.reduce(len(batch))
-        self.adam.step(self.params, self.flat.grads(), self.lrs(self.iteration))
+        self.adam.step(self.params, self.flat.grads(), self.lrs(self.iteration), grad_scale=1.0 / len(batch))
         return info
 
 
 def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConfig(), rasterizer=None):
-    """Default per-view function: render with the sm_100a path, device loss,
-    d_image by autograd of the loss, backward through the C ABI accumulating
-    into the given gradient buffers (+ the mask-loss gradient)."""
+    """Default per-view function on the GPU: sm_100a render, fused CUDA loss
+    (cs_image_loss; adds the mask-loss gradient, trainer.py:176), backward
+    through the C ABI accumulating into the flat buffers together with the
+    view's sigma signal (cs_backward_signal).  Returns the view's loss as a
+    device scalar (no host synchronisation besides the forward's pair count)."""
+    from .rasterizer import default_rasterizer
+    from .train_ops import LossWorkspace, image_loss as cuda_image_loss
+
+    r = rasterizer or default_rasterizer(scene.device)
+    lw = LossWorkspace()
+
+    def fn(view, grads: dict, signal: dict):
+        cam, target = view
+        fr = r.forward(scene, cam, mode, settings)
+        loss = cuda_image_loss(fr.image, target, scene.raw_mask, config.lambda_dssim, config.beta_mask,
+                               d_raw_mask=grads["raw_mask"], workspace=lw)
+        r.launch_backward(fr, loss["d_image"], grads,
+                          signal=(signal["sigma_signal"], signal["sigma_views"], fr.visible))
+        return loss["total"]
+    fn.handles_signal = True
+    return fn
+
+
+def torch_view_grad_fn(scene, mode, settings, config: StepConfig = StepConfig(), rasterizer=None):
+    """Per-view function with the loss formed by torch autograd of the
+    losses.py expression (reference formulation; used by the tests)."""
     from .rasterizer import default_rasterizer
 
     r = rasterizer or default_rasterizer(scene.device)
@@ -224,15 +262,17 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
     def fn(view, grads: dict):
         cam, target = view
         fr = r.forward(scene, cam, mode, settings)
-        img = fr.image.detach().requires_grad_(True)
-        raw_mask = scene.raw_mask.detach().requires_grad_(True)
-        loss = image_loss(img, target, raw_mask, config.lambda_dssim, config.beta_mask)
+        # the loss in float64, like the reference (float32 SSIM loses bits in
+        # sxx = vxx - mu^2 on flat regions)
+        img = fr.image.detach().double().requires_grad_(True)
+        raw_mask = scene.raw_mask.detach().double().requires_grad_(True)
+        loss = image_loss(img, target.double(), raw_mask, config.lambda_dssim, config.beta_mask)
         d_img, d_mask = torch.autograd.grad(loss["total"], (img, raw_mask))
-        r.launch_backward(fr, d_img.contiguous(), grads)
-        grads["raw_mask"].add_(d_mask)          # trainer.py:176 (straight-through mask-loss term)
-        return loss["total"].detach(), fr.visible
+        r.launch_backward(fr, d_img.float().contiguous(), grads)
+        grads["raw_mask"].add_(d_mask.float())  # trainer.py:176 (straight-through mask-loss term)
+        return loss["total"].detach().float(), fr.visible
     return fn
 
 
 __all__ = ["StepConfig", "image_loss", "ssim", "gaussian_window", "Adam", "position_lr", "shard_views",
-           "FlatGrads", "ViewShardedStep", "rasterizer_view_grad_fn"]
+           "FlatGrads", "ViewShardedStep", "rasterizer_view_grad_fn", "torch_view_grad_fn"]

@@ -143,7 +143,7 @@ def test_sharded_step_gradients_equal_sum_of_view_backwards():
         scene = cs.SceneTensors(**{k: leaves[k] for k in ("points", "raw_delta", "raw_sigma", "raw_opacity",
                                                           "raw_mask", "sh")}, background=st.background)
         img = cs.rasterize(scene, cam, mode, settings)[0]
-        loss = sharded.image_loss(img, target, leaves["raw_mask"])["total"]
+        loss = sharded.image_loss(img.double(), target.double(), leaves["raw_mask"].double())["total"]
         loss.backward()
         for k in ref:
             ref[k] += leaves[k].grad
