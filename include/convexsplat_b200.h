@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 2
+#define CS_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define CS_API __attribute__((visibility("default")))
@@ -232,6 +232,56 @@ typedef struct cs_adam_tensor {
  * `tensors` is a HOST array; step is the 1-based step count. */
 CS_API int cs_adam_step(int32_t count, const cs_adam_tensor *tensors, double beta1, double beta2, double eps,
                         int32_t step, double grad_scale, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Scene-level operations on the SoA parameters.
+ * ---------------------------------------------------------------------- */
+
+/* Writable SoA scene arrays (same shapes as cs_params). */
+typedef struct cs_scene_out {
+    float *points;            /* [n,k,3] */
+    float *raw_delta;         /* [n] */
+    float *raw_sigma;         /* [n] */
+    float *raw_opacity;       /* [n] */
+    float *raw_mask;          /* [n] */
+    float *sh;                /* [n,16,3] */
+} cs_scene_out;
+
+/* .3dcs checkpoint payload (sceneio.py:251-320): n rows of
+ * points(3k) | raw_delta raw_sigma raw_opacity | sh(48) | raw_mask as
+ * little-endian float32 (precision 32) or float16 (precision 16, round to
+ * nearest even).  unpack: device rows -> SoA arrays; pack: SoA -> rows. */
+CS_API int cs_checkpoint_unpack(int32_t precision, int64_t n, int32_t k, const void *rows,
+                                const cs_scene_out *out, void *stream);
+CS_API int cs_checkpoint_pack(int32_t precision, int64_t n, int32_t k, const cs_scene_out *scene, void *rows,
+                              void *stream);
+
+/* density.densify_and_prune settings (density.py:54-105, trainer.py:31-39). */
+typedef struct cs_density_config {
+    double sigma_threshold;       /* split when signal > threshold (sigma_loss_threshold) */
+    double split_scale;           /* split_convex scale */
+    double split_sigma_boost;
+    double split_opacity_factor;
+    double prune_opacity;         /* drop when opacity < prune_opacity */
+    double size_limit;            /* drop when diameter > prune_size_fraction * scene_extent */
+    int32_t allow_split;          /* iteration <= densify_stop */
+    int32_t reserved;
+} cs_density_config;
+
+/* Pass 1: per convex, flags bit0 = survivor kept, bit1 = split; child_keep =
+ * bitmask of the kept children (split_convex order); surv_count / child_count
+ * = the numbers of rows each convex contributes (int64, for the scans). */
+CS_API int cs_density_flags(const cs_params *params, const float *signal, const cs_density_config *cfg,
+                            uint8_t *flags, uint32_t *child_keep, int64_t *surv_count, int64_t *child_count,
+                            void *stream);
+
+/* Pass 2 (after exclusive scans surv_pos / child_pos of the counts and the
+ * kept-survivor total n_surv, a device scalar): writes the new scene rows in
+ * the reference order -- kept survivors in index order, then the kept
+ * children of each split parent -- and index_map (old index, -1 for a child). */
+CS_API int cs_density_scatter(const cs_params *params, const cs_density_config *cfg, const uint8_t *flags,
+                              const uint32_t *child_keep, const int64_t *surv_pos, const int64_t *child_pos,
+                              const int64_t *n_surv, const cs_scene_out *out, int64_t *index_map, void *stream);
 
 #ifdef __cplusplus
 }

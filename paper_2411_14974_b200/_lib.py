@@ -13,8 +13,9 @@ LIB_PATH = os.path.join(_HERE, "libconvexsplat_sm100.so")
 
 EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forward", "cs_backward",
            "cs_forward_stages", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
-           "cs_backward_signal", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step")
-ABI_VERSION = 2
+           "cs_backward_signal", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step",
+           "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags", "cs_density_scatter")
+ABI_VERSION = 3
 
 _vp = ctypes.c_void_p
 
@@ -56,6 +57,18 @@ class CsViewSignal(ctypes.Structure):
 class CsAdamTensor(ctypes.Structure):
     _fields_ = [("param", _vp), ("grad", _vp), ("m", _vp), ("v", _vp), ("numel", ctypes.c_int64),
                 ("lr", ctypes.c_double)]
+
+
+class CsSceneOut(ctypes.Structure):
+    _fields_ = [("points", _vp), ("raw_delta", _vp), ("raw_sigma", _vp), ("raw_opacity", _vp),
+                ("raw_mask", _vp), ("sh", _vp)]
+
+
+class CsDensityConfig(ctypes.Structure):
+    _fields_ = [("sigma_threshold", ctypes.c_double), ("split_scale", ctypes.c_double),
+                ("split_sigma_boost", ctypes.c_double), ("split_opacity_factor", ctypes.c_double),
+                ("prune_opacity", ctypes.c_double), ("size_limit", ctypes.c_double),
+                ("allow_split", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class CsLayout(ctypes.Structure):
@@ -104,9 +117,18 @@ def load(path: str = None):
                                 ctypes.c_double, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
     L.cs_adam_step.argtypes = [ctypes.c_int32, ctypes.POINTER(CsAdamTensor), ctypes.c_double, ctypes.c_double,
                                ctypes.c_double, ctypes.c_int32, ctypes.c_double, _vp]
+    L.cs_checkpoint_unpack.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, _vp,
+                                       ctypes.POINTER(CsSceneOut), _vp]
+    L.cs_checkpoint_pack.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(CsSceneOut),
+                                     _vp, _vp]
+    L.cs_density_flags.argtypes = [ctypes.POINTER(CsParams), _vp, ctypes.POINTER(CsDensityConfig), _vp, _vp, _vp,
+                                   _vp, _vp]
+    L.cs_density_scatter.argtypes = [ctypes.POINTER(CsParams), ctypes.POINTER(CsDensityConfig), _vp, _vp, _vp,
+                                     _vp, _vp, ctypes.POINTER(CsSceneOut), _vp, _vp]
     for fn in ("cs_workspace_layout", "cs_forward", "cs_backward", "cs_forward_stages", "cs_backward_stages",
                "cs_read_counters", "cs_graham_scan_batch", "cs_backward_signal", "cs_image_loss_workspace",
-               "cs_image_loss", "cs_adam_step"):
+               "cs_image_loss", "cs_adam_step", "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags",
+               "cs_density_scatter"):
         getattr(L, fn).restype = ctypes.c_int
     if L.cs_abi_version() != ABI_VERSION:
         raise CsError(f"ABI mismatch: library {L.cs_abi_version()} != {ABI_VERSION}")

@@ -19,7 +19,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build", "csrc")
 LIB = os.path.join(HERE, "libconvexsplat_sm100.so")
-SOURCES = ["preprocess.cu", "sort.cu", "blend.cu", "chain.cu", "train.cu", "capi.cu"]
+SOURCES = ["preprocess.cu", "sort.cu", "blend.cu", "chain.cu", "train.cu", "scene_ops.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]

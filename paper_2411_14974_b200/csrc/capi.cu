@@ -194,4 +194,47 @@ int cs_graham_scan_batch(int32_t m, int32_t npts, const int32_t *counts, const d
   return cs::launch_hull_batch(m, npts, counts, pts, hull, hull_n, reinterpret_cast<cudaStream_t>(stream));
 }
 
+static bool scene_out_ok(const cs_scene_out *o) {
+  return o && o->points && o->raw_delta && o->raw_sigma && o->raw_opacity && o->raw_mask && o->sh;
+}
+
+int cs_checkpoint_unpack(int32_t precision, int64_t n, int32_t k, const void *rows, const cs_scene_out *out,
+                         void *stream) {
+  if ((precision != 16 && precision != 32) || n < 0 || k < 3 || k > 16) return CS_ERR_ARG;
+  if (n > 0 && (!rows || !scene_out_ok(out))) return CS_ERR_ARG;
+  return cs::launch_checkpoint_rows(false, precision, n, k, const_cast<void *>(rows), *out,
+                                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cs_checkpoint_pack(int32_t precision, int64_t n, int32_t k, const cs_scene_out *scene, void *rows,
+                       void *stream) {
+  if ((precision != 16 && precision != 32) || n < 0 || k < 3 || k > 16) return CS_ERR_ARG;
+  if (n > 0 && (!rows || !scene_out_ok(scene))) return CS_ERR_ARG;
+  return cs::launch_checkpoint_rows(true, precision, n, k, rows, *scene, reinterpret_cast<cudaStream_t>(stream));
+}
+
+static bool params_ok(const cs_params *p) {
+  return p && p->n >= 0 && p->k >= 3 && p->k <= 16 &&
+         (p->n == 0 || (p->points && p->raw_delta && p->raw_sigma && p->raw_opacity && p->raw_mask && p->sh));
+}
+
+int cs_density_flags(const cs_params *params, const float *signal, const cs_density_config *cfg, uint8_t *flags,
+                     uint32_t *child_keep, int64_t *surv_count, int64_t *child_count, void *stream) {
+  if (!params_ok(params) || !cfg) return CS_ERR_ARG;
+  if (params->n > 0 && (!signal || !flags || !child_keep || !surv_count || !child_count)) return CS_ERR_ARG;
+  return cs::launch_density_flags(*params, signal, *cfg, flags, child_keep, surv_count, child_count,
+                                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cs_density_scatter(const cs_params *params, const cs_density_config *cfg, const uint8_t *flags,
+                       const uint32_t *child_keep, const int64_t *surv_pos, const int64_t *child_pos,
+                       const int64_t *n_surv, const cs_scene_out *out, int64_t *index_map, void *stream) {
+  if (!params_ok(params) || !cfg) return CS_ERR_ARG;
+  if (params->n > 0 && (!flags || !child_keep || !surv_pos || !child_pos || !n_surv || !index_map ||
+                        !scene_out_ok(out)))
+    return CS_ERR_ARG;
+  return cs::launch_density_scatter(*params, *cfg, flags, child_keep, surv_pos, child_pos, n_surv, *out, index_map,
+                                    reinterpret_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

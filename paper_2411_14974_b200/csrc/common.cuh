@@ -192,6 +192,13 @@ int launch_image_loss(int H, int W, const float *img, const float *tgt, const fl
                       cudaStream_t s);
 int launch_adam(int count, const cs_adam_tensor *tensors, double b1, double b2, double eps, int step,
                 double gscale, cudaStream_t s);
+int launch_checkpoint_rows(bool pack, int precision, int64_t n, int k, void *rows, const cs_scene_out &o,
+                           cudaStream_t s);
+int launch_density_flags(const cs_params &P, const float *signal, const cs_density_config &c, uint8_t *flags,
+                         uint32_t *child_keep, int64_t *surv_count, int64_t *child_count, cudaStream_t s);
+int launch_density_scatter(const cs_params &P, const cs_density_config &c, const uint8_t *flags,
+                           const uint32_t *child_keep, const int64_t *surv_pos, const int64_t *child_pos,
+                           const int64_t *n_surv, const cs_scene_out &o, int64_t *index_map, cudaStream_t s);
 int launch_hull_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts,
                       int32_t *hull, int32_t *hull_n, cudaStream_t s);
 size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, struct Scratch *sc, char *base);

@@ -225,7 +225,33 @@ class ViewShardedStep:
         info = self.accumulate(batch)
         self.reduce(len(batch))
         self.adam.step(self.params, self.flat.grads(), self.lrs(self.iteration), grad_scale=1.0 / len(batch))
+        # densification signal since the last densify round (trainer.py:192-193)
+        if not hasattr(self, "sigma_sum"):
+            self.sigma_sum = torch.zeros_like(self.flat.views["sigma_signal"])
+            self.sigma_views = torch.zeros_like(self.flat.views["sigma_views"])
+        self.sigma_sum.add_(self.flat.views["sigma_signal"])
+        self.sigma_views.add_(self.flat.views["sigma_views"])
         return info
+
+    def densify(self, scene, density_config=None):
+        """density.densify_and_prune on the device (trainer.py:195-203) with the
+        accumulated signal sum / max(views, 1); identical on every rank (the
+        signal was all-reduced).  Returns the new SceneTensors; ``params``, the
+        Adam moments (remapped, optim.py:37-53), the flat buffers and the
+        signal are rebuilt for it.  The caller re-creates its view function."""
+        from .density import DensityConfig, densify_and_prune
+        cfg = density_config or DensityConfig()
+        signal = self.sigma_sum / torch.clamp(self.sigma_views, min=1.0)
+        new, index_map, stats = densify_and_prune(scene, signal, cfg, self.iteration)
+        self.params = {k: getattr(new, k) for k in PARAM_ORDER}
+        self.adam.remap(index_map)
+        n = new.n
+        self.flat = FlatGrads({k: tuple(v.shape) for k, v in self.params.items()}, n, new.points.device,
+                              new.points.dtype)
+        self.sigma_sum = torch.zeros(n, dtype=self.flat.buffer.dtype, device=self.flat.buffer.device)
+        self.sigma_views = torch.zeros_like(self.sigma_sum)
+        self.last_densify = stats
+        return new
 
 
 def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConfig(), rasterizer=None):

@@ -208,8 +208,50 @@ def gen_loss():
     print("loss: ok")
 
 
+def gen_scene_ops():
+    """.3dcs checkpoints (sceneio.py:251-320) and densify_and_prune
+    (density.py:54-105) known answers on float32-quantised scenes."""
+    from convexsplat.density import densify_and_prune
+    from convexsplat.sceneio import save_checkpoint
+    from convexsplat.trainer import TrainConfig
+    scene = quantize32(make_scene(9, seed=11, background=(0.1, 0.2, 0.3)))
+    scene.scene_extent = 2.5
+    for prec in (32, 16):
+        save_checkpoint(os.path.join(OUT, f"ckpt_f{prec}.3dcs"), scene, precision=prec)
+    arr = scene_arrays(scene)
+    np.savez_compressed(os.path.join(OUT, "ckpt.npz"), **arr, scene_extent=scene.scene_extent)
+    # densification: a scene with splits, low-opacity / low-mask / oversized convexes
+    rng = np.random.default_rng(21)
+    dscene = quantize32(make_scene(40, seed=12))
+    dscene.scene_extent = 2.0
+    prims = dscene.primitives
+    prims[3].raw_opacity = float(np.float32(inverse_opacity_activation(0.02)))       # pruned: opacity
+    prims[7].raw_mask = float(np.float32(inverse_mask_activation(0.005)))            # pruned: mask gate
+    prims[11].points = (prims[11].points * 8.0).astype(np.float32).astype(np.float64)  # pruned: diameter
+    prims[5].raw_opacity = float(np.float32(inverse_opacity_activation(0.035)))      # children pruned (0.8 o)
+    signal = rng.uniform(0.0, 8e-6, size=len(prims)).astype(np.float32).astype(np.float64)
+    signal[[3, 5, 11]] = 9e-6
+    cfg = TrainConfig()
+    before = scene_arrays(dscene)
+    out = {}
+    for tag, it in (("split", 600), ("nosplit", cfg.densify_stop + 1)):
+        work = dscene.copy()
+        work.scene_extent = dscene.scene_extent
+        index_map, stats = densify_and_prune(work, signal, cfg, it)
+        after = scene_arrays(work)
+        for kk in ("points", "raw_delta", "raw_sigma", "raw_opacity", "raw_mask", "sh"):
+            out[f"{tag}_{kk}"] = after[kk]
+        out[f"{tag}_index_map"] = index_map
+        out[f"{tag}_stats"] = np.array([stats.split, stats.pruned, stats.before, stats.after])
+        out[f"{tag}_iteration"] = np.array(it)
+    np.savez_compressed(os.path.join(OUT, "density.npz"), **{f"in_{k}": v for k, v in before.items()},
+                        signal=signal, scene_extent=dscene.scene_extent, **out)
+    print("scene ops: ok")
+
+
 def main():
     DEPTH, NONE = ScalingMode.DEPTH, ScalingMode.NONE
+    gen_scene_ops()
     gen_hulls()
     gen_loss()
 
@@ -289,5 +331,7 @@ def main():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "loss":
         gen_loss()
+    elif len(sys.argv) > 1 and sys.argv[1] == "scene_ops":
+        gen_scene_ops()
     else:
         main()

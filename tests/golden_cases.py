@@ -11,7 +11,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def scene_cases():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not p.endswith(("hulls.npz", "loss.npz")))
+                  if not p.endswith(("hulls.npz", "loss.npz", "ckpt.npz", "density.npz")))
 
 
 def load(name: str) -> dict:
