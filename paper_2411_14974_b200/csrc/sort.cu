@@ -15,6 +15,8 @@
 // pass, then one kernel per 8-bit digit that ranks keys with warp
 // __match_any_sync, publishes per-chunk digit counts and resolves its prefix
 // by decoupled look-back.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cs {
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t 
 // The 8-bit digit histograms of the tile keys for the pair sort are
 // accumulated on the way (shared-memory atomics, one global add per bin).
 constexpr int kDupThreads = 256;
+constexpr int kDupRounds = 4;   // ranks per block = kDupRounds * kDupThreads (fewer histogram flushes)
 
 __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *order, const uint32_t *touched,
                                                                 const int4 *bbox, const uint32_t *offsets,
@@ -370,69 +373,75 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *
   for (int q = threadIdx.x; q < passes * kRadix; q += kDupThreads) s_h[q / kRadix][q % kRadix] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint32_t r = blockIdx.x * kDupThreads + threadIdx.x;
-  uint32_t id = 0, cnt = 0, off = 0;
-  int tx0 = 0, ty0 = 0, wdt = 1;
-  if (r < n) {
-    id = order[r];
-    cnt = touched[id];
-    off = offsets[r];
-    if (cnt) {
-      const int4 b = bbox[id];
+  // gather every round's convex first (independent loads in flight)
+  uint32_t id[kDupRounds], cnt[kDupRounds], off[kDupRounds];
+#pragma unroll
+  for (int k = 0; k < kDupRounds; k++) {
+    const uint32_t r = (blockIdx.x * kDupRounds + k) * kDupThreads + threadIdx.x;
+    id[k] = r < n ? order[r] : 0u;
+    off[k] = r < n ? offsets[r] : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < kDupRounds; k++) {
+    const uint32_t r = (blockIdx.x * kDupRounds + k) * kDupThreads + threadIdx.x;
+    cnt[k] = r < n ? touched[id[k]] : 0u;
+  }
+#pragma unroll 1
+  for (int k = 0; k < kDupRounds; k++) {
+    int tx0 = 0, ty0 = 0, wdt = 1;
+    if (cnt[k]) {
+      const int4 b = bbox[id[k]];
       tx0 = b.x / kTile;
       ty0 = b.z / kTile;
       wdt = (b.y - 1) / kTile - tx0 + 1;
-    }
-  }
-  // digit histograms of this convex's tile keys: digit 0 per tile, higher
-  // digits per row segment (a row of tiles rarely crosses a 256 boundary)
-  if (cnt && (uint64_t)off + cnt <= cap) {
-    const int4 b = bbox[id];
-    const int ty1 = (b.w - 1) / kTile;
-    for (int ty = ty0; ty <= ty1; ty++) {
-      const uint32_t t0 = (uint32_t)(ty * tiles_x + tx0), t1 = t0 + (uint32_t)wdt - 1;
-      for (uint32_t t = t0; t <= t1; t++) atomicAdd(&s_h[0][t & (kRadix - 1)], 1u);
-      for (int ps = 1; ps < passes; ps++) {
-        const int sh = ps * kRadixBits;
-        uint32_t seg = t0;
-        while (seg <= t1) {
-          const uint32_t blk_end = min(t1, ((seg >> sh) + 1) * (1u << sh) - 1);
-          atomicAdd(&s_h[ps][(seg >> sh) & (kRadix - 1)], blk_end - seg + 1);
-          seg = blk_end + 1;
+      // digit histograms of this convex's tile keys: digit 0 per tile, higher
+      // digits per row segment (a row of tiles rarely crosses a 256 boundary)
+      if ((uint64_t)off[k] + cnt[k] <= cap) {
+        const int ty1 = (b.w - 1) / kTile;
+        for (int ty = ty0; ty <= ty1; ty++) {
+          const uint32_t t0 = (uint32_t)(ty * tiles_x + tx0), t1 = t0 + (uint32_t)wdt - 1;
+          for (uint32_t t = t0; t <= t1; t++) atomicAdd(&s_h[0][t & (kRadix - 1)], 1u);
+          for (int ps = 1; ps < passes; ps++) {
+            const int sh = ps * kRadixBits;
+            uint32_t seg = t0;
+            while (seg <= t1) {
+              const uint32_t blk_end = min(t1, ((seg >> sh) + 1) * (1u << sh) - 1);
+              atomicAdd(&s_h[ps][(seg >> sh) & (kRadix - 1)], blk_end - seg + 1);
+              seg = blk_end + 1;
+            }
+          }
         }
       }
     }
-  }
-  // inclusive prefix of the counts inside the warp (ranks are contiguous)
-  uint32_t inc = cnt;
+    // inclusive prefix of the counts inside the warp (its 32 ranks are contiguous)
+    uint32_t inc = cnt[k];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += u;
-  }
-  const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-  const uint32_t base = __shfl_sync(0xffffffffu, off - (inc - cnt), 0);  // offset of the warp's first pair
-  const uint32_t excl = inc - cnt;
-  for (uint32_t p0 = 0; p0 < total; p0 += 32) {  // warp-uniform trip count
-    const uint32_t p = p0 + lane;
-    // owner = last lane whose exclusive prefix is <= p
-    int lo = 0;
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-      const uint32_t e = __shfl_sync(0xffffffffu, excl, (lo + step) & 31);
-      if (lo + step < 32 && e <= p) lo += step;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
     }
-    const uint32_t q = p - __shfl_sync(0xffffffffu, excl, lo);
-    const int w_o = __shfl_sync(0xffffffffu, wdt, lo);
-    const int tx = __shfl_sync(0xffffffffu, tx0, lo) + (int)(q % (uint32_t)w_o);
-    const int ty = __shfl_sync(0xffffffffu, ty0, lo) + (int)(q / (uint32_t)w_o);
-    const uint32_t owner_id = __shfl_sync(0xffffffffu, id, lo);
-    const uint32_t pos = base + p;
-    const bool ok = p < total && pos < cap;
-    const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
-    if (ok) {
-      pair_tiles[pos] = tile;
-      pair_ids[pos] = owner_id;
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    const uint32_t base = __shfl_sync(0xffffffffu, off[k] - (inc - cnt[k]), 0);  // offset of the warp's first pair
+    const uint32_t excl = inc - cnt[k];
+    for (uint32_t p0 = 0; p0 < total; p0 += 32) {  // warp-uniform trip count
+      const uint32_t p = p0 + lane;
+      // owner = last lane whose exclusive prefix is <= p
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t e = __shfl_sync(0xffffffffu, excl, (lo + step) & 31);
+        if (lo + step < 32 && e <= p) lo += step;
+      }
+      const uint32_t q = p - __shfl_sync(0xffffffffu, excl, lo);
+      const int w_o = __shfl_sync(0xffffffffu, wdt, lo);
+      const int tx = __shfl_sync(0xffffffffu, tx0, lo) + (int)(q % (uint32_t)w_o);
+      const int ty = __shfl_sync(0xffffffffu, ty0, lo) + (int)(q / (uint32_t)w_o);
+      const uint32_t owner_id = __shfl_sync(0xffffffffu, id[k], lo);
+      const uint32_t pos = base + p;
+      if (p < total && pos < cap) {
+        pair_tiles[pos] = (uint32_t)(ty * tiles_x + tx);
+        pair_ids[pos] = owner_id;
+      }
     }
   }
   __syncthreads();
@@ -442,20 +451,31 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *
   }
 }
 
-// [start, end) of every tile in the sorted pair keys, by binary search.
-__global__ void ranges_kernel(const uint32_t *pair_tiles, const uint32_t *counters, int tiles, uint2 *ranges) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= tiles) return;
+// [start, end) of every tile in the sorted pair keys: each pair position
+// that starts or ends a run of equal tiles writes that bound (one coalesced
+// pass over the keys; empty tiles keep the zeroed (0, 0)).
+__global__ void __launch_bounds__(256) ranges_kernel(const uint32_t *pair_tiles, const uint32_t *counters,
+                                                     uint2 *ranges) {
   const uint32_t P = counters[C_NSORT];
-  auto lower = [&](uint32_t key) {
-    uint32_t lo = 0, hi = P;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (pair_tiles[mid] < key) lo = mid + 1; else hi = mid;
+  // four positions per thread: one 16-byte load plus the two neighbours
+  for (uint32_t p0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x); p0 < P; p0 += 4 * gridDim.x * blockDim.x) {
+    uint32_t t[6];
+    t[0] = p0 > 0 ? __ldg(pair_tiles + p0 - 1) : ~0u;
+    if (p0 + 4 <= P) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(pair_tiles + p0));
+      t[1] = v.x; t[2] = v.y; t[3] = v.z; t[4] = v.w;
+    } else {
+      for (int q = 0; q < 4; q++) t[1 + q] = p0 + q < P ? pair_tiles[p0 + q] : ~0u;
     }
-    return lo;
-  };
-  ranges[t] = make_uint2(lower((uint32_t)t), lower((uint32_t)t + 1));
+    t[5] = p0 + 4 < P ? __ldg(pair_tiles + p0 + 4) : ~0u;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const uint32_t p = p0 + q;
+      if (p >= P) break;
+      if (t[q] != t[q + 1]) ranges[t[q + 1]].x = p;
+      if (t[q + 2] != t[q + 1]) ranges[t[q + 1]].y = p + 1;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ depth order
@@ -493,7 +513,16 @@ __global__ void __launch_bounds__(kSortThreads) depth_key32_kernel(const uint64_
     keys32[idx] = k32;
     order[idx] = idx;
 #pragma unroll
-    for (int p = 0; p < 4; p++) atomicAdd(&h[p][(k32 >> (p * kRadixBits)) & (kRadix - 1)], 1u);
+    for (int p = 0; p < 4; p++) {   // one shared atomic when the whole warp shares the digit (depths cluster)
+      const uint32_t d = (k32 >> (p * kRadixBits)) & (kRadix - 1);
+      const uint32_t act = __activemask();
+      const uint32_t d0 = __shfl_sync(act, d, __ffs(act) - 1);
+      if (__all_sync(act, d == d0)) {
+        if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(&h[p][d], (uint32_t)__popc(act));
+      } else {
+        atomicAdd(&h[p][d], 1u);
+      }
+    }
   }
   __syncthreads();
   for (int q = threadIdx.x; q < 4 * kRadix; q += kSortThreads) {
@@ -611,6 +640,7 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
 
   cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 16 * kRadix, s);
   cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * sc.lookback_words, s);
+  cudaMemsetAsync(ranges, 0, sizeof(uint2) * tiles, s);   // empty tiles (and n == 0) read (0, 0)
   if (n > 0) {
     // depth order: 31-bit keys, 4 passes (even) -> (keys32, order), then
     // the exact fix-up of equal-key runs
@@ -627,7 +657,7 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
     // pairs land in the buffer that makes the sorted result end in (ptiles, pids)
     uint32_t *dt = (pp & 1) ? sc.ptiles_alt : ptiles;
     uint32_t *di = (pp & 1) ? sc.pids_alt : pids;
-    duplicate_kernel<<<(n + kDupThreads - 1) / kDupThreads, kDupThreads, 0, s>>>(
+    duplicate_kernel<<<(n + kDupThreads * kDupRounds - 1) / (kDupThreads * kDupRounds), kDupThreads, 0, s>>>(
         order, touched, reinterpret_cast<const int4 *>(ws + L.bbox), offs, n, (uint32_t)cap, L.tiles_x, pp, dt, di,
         sc.hist + 8 * kRadix);
     if (cap > 0) {
@@ -637,7 +667,8 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
                            sc.offsets + 8 * kRadix, sc.lookback + 8 * ((n + kSortChunk - 1) / kSortChunk) * kRadix,
                            counters + C_CHUNK0 + 8, true, s);
     }
-    ranges_kernel<<<(tiles + 255) / 256, 256, 0, s>>>(ptiles, counters, tiles, ranges);
+    const int rb = (int)std::min<int64_t>((cap + 1023) / 1024, 148 * 16);
+    if (rb > 0) ranges_kernel<<<rb, 256, 0, s>>>(ptiles, counters, ranges);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
