@@ -38,6 +38,18 @@ struct ChainArgs {
 
 template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 128 : 64; }
 
+// Accumulation into the caller's gradient buffers (+=, GradientBuffer.add).
+// Every convex has one owning thread, so these need no atomicity; they are
+// issued as fire-and-forget L2 reductions (RED) so the SM never waits for the
+// read half of a read-modify-write of ~0.7 KB per convex.
+__device__ __forceinline__ void red_add(float *p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add4(float4 *p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 // d(Y_b)/d(dir) . v_b added into (gx, gy, gz): eval_sh_basis_grad
 // (harmonics.py:62-98) row b, written out (b is a compile-time constant).
 __device__ __forceinline__ void add_basis_grad(int b, float v, float x, float y, float z, float &gx, float &gy,
@@ -71,7 +83,7 @@ __device__ __forceinline__ void add_basis_grad(int b, float v, float x, float y,
 
 // SH colour VJP (harmonics.py:112-128): d_sh += Y (x) d_eff and the
 // direction gradient dY/ddir^T (sh . d_eff).  Streams the 16x3 rows as
-// float4 (two reads of sh, one read-modify-write of d_sh) so no per-thread
+// float4 (two reads of sh, one vector reduction into d_sh) so no per-thread
 // 48-float arrays stay live.
 __device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const float *sh, const float *d_color,
                                        float *d_sh, float *ddir) {
@@ -115,13 +127,12 @@ __device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const
     if (4 * q < 3 * nb) {
       const float4 v = __ldg(sh4 + q);
       const float e[4] = {v.x, v.y, v.z, v.w};
-      float4 d = dsh4[q];
-      float de[4] = {d.x, d.y, d.z, d.w};
+      float de[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int r = 0; r < 4; r++) {
         const int f = 4 * q + r, b = f / 3, c = f % 3;
         if (b < nb) {
-          de[r] += Y[b] * deff[c];
+          de[r] = Y[b] * deff[c];
           vb = fmaf(e[r], deff[c], vb);
           if (c == 2) {  // row b complete: its direction-gradient term
             add_basis_grad(b, vb, x, y, z, gx, gy, gz);
@@ -129,7 +140,7 @@ __device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const
           }
         }
       }
-      dsh4[q] = make_float4(de[0], de[1], de[2], de[3]);
+      red_add4(dsh4 + q, make_float4(de[0], de[1], de[2], de[3]));
     }
   }
   ddir[0] = gx; ddir[1] = gy; ddir[2] = gz;
@@ -279,22 +290,22 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
         dz = -((s_x[j][t] - (G)ox) * gx + (s_y[j][t] - (G)oy) * gy) * izc[j];
       }
 #pragma unroll
-      for (int c = 0; c < 3; c++) dp[3 * j + c] += (float)fma(d0, R[c], fma(d1, R[3 + c], fma(dz, R[6 + c], common[c])));
+      for (int c = 0; c < 3; c++) red_add(dp + 3 * j + c, (float)fma(d0, R[c], fma(d1, R[3 + c], fma(dz, R[6 + c], common[c]))));
     }
   }
-  a.g.d_raw_delta[i] += (float)(ddel * s * delta);
+  red_add(a.g.d_raw_delta + i, (float)(ddel * s * delta));
   const float d_rs = (float)(dsig * s * sigma);
-  a.g.d_raw_sigma[i] += d_rs;
+  red_add(a.g.d_raw_sigma + i, d_rs);
   if (a.sig.sigma_signal) {   // trainer.py:192-193, this view's contribution only
     const float vis = a.sig.visible[i] ? 1.f : 0.f;
-    a.sig.sigma_signal[i] += fabsf(d_rs) * vis;
-    a.sig.sigma_views[i] += vis;
+    red_add(a.sig.sigma_signal + i, fabsf(d_rs) * vis);
+    red_add(a.sig.sigma_views + i, vis);
   }
   const float o = 1.f / (1.f + __expf(-a.raw_opacity[i]));
   const float m = 1.f / (1.f + __expf(-a.raw_mask[i]));
   const float doe = (float)acc[A_DOEFF];
-  a.g.d_raw_opacity[i] += doe * o * (1.f - o);
-  a.g.d_raw_mask[i] += doe * o * m * (1.f - m);
+  red_add(a.g.d_raw_opacity + i, doe * o * (1.f - o));
+  red_add(a.g.d_raw_mask + i, doe * o * m * (1.f - m));
 }
 
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
