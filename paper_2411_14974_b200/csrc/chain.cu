@@ -170,7 +170,16 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
   constexpr int AF = Acc<MAXK>::kFloats;
   const int k = a.k;
   const G inv_k = G(1) / (G)k;
-  const float *acc = a.accum + i * AF;
+  // the convex's screen-space accumulators, loaded as float4 up front
+  float acc[AF];
+  {
+    const float4 *acc4 = reinterpret_cast<const float4 *>(a.accum + i * AF);
+#pragma unroll
+    for (int q = 0; q < AF / 4; q++) {
+      const float4 v = __ldg(acc4 + q);
+      acc[4 * q] = v.x; acc[4 * q + 1] = v.y; acc[4 * q + 2] = v.z; acc[4 * q + 3] = v.w;
+    }
+  }
   const float2 anchor = *reinterpret_cast<const float2 *>(a.records + i * RF);
   G R[9];
 #pragma unroll
