@@ -504,6 +504,10 @@ __global__ void __launch_bounds__(kPreThreads, CS_PRE_BLOCKS) preprocess_kernel(
       const uint32_t pbytes = kPreThreads * rowf * 4;
       mbar_expect_tx(&bars[0], pbytes);
       tma_bulk_g2s(pts_smem, a.points + base * rowf, pbytes, &bars[0]);
+      // the block's SH rows are read at the very end of each thread (colour):
+      // start pulling them into L2 now so that read does not wait on DRAM
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.sh + base * kShCoeffs * 3),
+                   "r"((uint32_t)(kPreThreads * kShCoeffs * 3 * 4)) : "memory");
     }
     mbar_wait(&bars[0], 0);
   } else {  // tail block: plain coalesced loads
