@@ -11,6 +11,8 @@
 // translation unit is compiled with --fmad=false so that only the explicit
 // fma() of the projection (OpenBLAS dgemm order of `points @ R.T`) fuses.
 // Outputs are a float32 blend record per convex plus the discrete results.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace cs {
@@ -173,16 +175,18 @@ constexpr int kPreThreads = 128;
 
 // Index list of up to 16 entries packed as 4-bit nibbles in a register, so
 // the Graham scan's insert / erase / pop keep no per-thread local memory.
-struct NibbleList {
-  uint64_t w = 0;
+template <typename W>
+struct NibbleListT {
+  static constexpr int kCap = (int)sizeof(W) * 2;   // 4-bit entries per word
+  W w = 0;
   int n = 0;
-  __device__ __forceinline__ static uint64_t low(int i) { return i >= 16 ? ~0ull : ((1ull << (4 * i)) - 1ull); }
-  __device__ __forceinline__ int get(int i) const { return (int)((w >> (4 * i)) & 15ull); }
-  __device__ __forceinline__ void set(int i, int v) { w = (w & ~(15ull << (4 * i))) | ((uint64_t)v << (4 * i)); }
-  __device__ __forceinline__ void push(int v) { w |= (uint64_t)v << (4 * n); n++; }
+  __device__ __forceinline__ static W low(int i) { return i >= kCap ? ~W(0) : ((W(1) << (4 * i)) - W(1)); }
+  __device__ __forceinline__ int get(int i) const { return (int)((w >> (4 * i)) & W(15)); }
+  __device__ __forceinline__ void set(int i, int v) { w = (w & ~(W(15) << (4 * i))) | ((W)v << (4 * i)); }
+  __device__ __forceinline__ void push(int v) { w |= (W)v << (4 * n); n++; }
   __device__ __forceinline__ void pop() { n--; w &= low(n); }
   __device__ __forceinline__ void insert(int i, int v) {
-    w = (w & low(i)) | ((uint64_t)v << (4 * i)) | ((w & ~low(i)) << 4);
+    w = (w & low(i)) | ((W)v << (4 * i)) | ((w & ~low(i)) << 4);
     n++;
   }
   __device__ __forceinline__ void erase(int i) {
@@ -190,16 +194,19 @@ struct NibbleList {
     n--;
   }
 };
+// 8 entries fit a 32-bit word (the K <= 8 kernels: cheaper shifts than 64-bit)
+using NibbleList = NibbleListT<uint64_t>;
 
 // projection.py:47-113 on points X[j*stride], Y[j*stride] (shared memory),
 // n <= 16.  Same algorithm as graham_scan_dev (CPython list.sort
 // count_run + binary insertion for the tolerance comparator), with the
 // index lists held in registers.
-__device__ int graham_scan_packed(int n, const double *X, const double *Y, int stride, NibbleList &out) {
+template <typename NL>
+__device__ int graham_scan_packed(int n, const double *X, const double *Y, int stride, NL &out) {
 #define GX(i) X[(i) * stride]
 #define GY(i) Y[(i) * stride]
   if (n < 3) return 0;
-  NibbleList uq;
+  NL uq;
   for (int i = 0; i < n; i++) {
     const double xi = GX(i), yi = GY(i);
     bool dup = false;
@@ -223,7 +230,7 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
     if (c < -kCrossTol) return false;
     return (ax * ax + ay * ay) < (bx * bx + by * by);
   };
-  NibbleList rest;
+  NL rest;
   for (int j = 0; j < uq.n; j++)
     if (uq.get(j) != ref) rest.push(uq.get(j));
   const int m = rest.n;
@@ -253,7 +260,7 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
   auto cross = [&](int o, int a, int b) -> double {  // projection.py:43-44
     return (GX(a) - GX(o)) * (GY(b) - GY(o)) - (GY(a) - GY(o)) * (GX(b) - GX(o));
   };
-  NibbleList st;
+  NL st;
   st.push(ref);
   for (int j = 0; j < m; j++) {
     const int c = rest.get(j);
@@ -276,7 +283,7 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
   int start = 0;
   for (int q = 0; q < st.n; q++)
     if (st.get(q) == ref) { start = q; break; }
-  out = NibbleList();
+  out = NL();
   for (int q = 0; q < st.n; q++) out.push(st.get((start + q) % st.n));
   return out.n;
 #undef GX
@@ -370,7 +377,7 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
     }
   }
   if (culled) return false;
-  NibbleList hull;
+  NibbleListT<typename std::conditional<(MAXK <= 8), uint32_t, uint64_t>::type> hull;
   const int h = graham_scan_packed(k, X, Y, kPreThreads, hull);
   if (h == 0) return false;
   // rasterize.py:99-103
