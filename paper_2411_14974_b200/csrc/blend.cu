@@ -115,14 +115,22 @@ template <int NL, int MAXK, bool ACC = false>
 __device__ __forceinline__ Eval eval_field(const LineSet<NL, MAXK> &L, float sig, float o, float dx, float dy,
                                            float (&z)[LineSet<NL, MAXK>::kN]) {
   constexpr int N = LineSet<NL, MAXK>::kN;
-  float s = 0.f;
+  float ex[N];
 #pragma unroll
   for (int l = 0; l < N; l++) {
     if (L.has(l)) {
       z[l] = fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]));
-      s += ACC ? acc_ex2(z[l]) : ex2(z[l]);
+      ex[l] = ACC ? acc_ex2(z[l]) : ex2(z[l]);
+    } else {
+      ex[l] = 0.f;
     }
   }
+  // pairwise sum (log-depth dependency chain instead of N-1 serial adds)
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int l = 0; l + w < N; l += 2 * w) ex[l] += ex[l + w];
+  const float s = ex[0];
   float phi2;
 #ifdef CS_MAX_SHIFT
   if (false) {
@@ -391,7 +399,8 @@ __global__ void __launch_bounds__(kPipeThreads, 4) forward_kernel(BlendArgs a) {
           bool blended = false;
           const uint32_t pj = __shfl_sync(0xffffffffu, pm, j);
           const bool act = !P.done && ((pj >> lane) & 1u);
-          n_warp_evals += __any_sync(0xffffffffu, act) ? 1u : 0u;
+          if (!__any_sync(0xffffffffu, act)) continue;   // its pixels died earlier in this stage
+          n_warp_evals++;
 #ifdef CS_NO_EVAL
           if (false) {
 #else
