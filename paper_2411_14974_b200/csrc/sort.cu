@@ -80,6 +80,7 @@ struct PassArgs {
   const uint32_t *count;  // device item count (or null -> n_fixed)
   uint32_t n_fixed;
   int shift;
+  int bits;                 // significant bits of this pass's digit (<= 8): fewer ballots
   const uint32_t *offsets;  // [256] global exclusive digit offsets of this pass
   uint32_t *lookback;       // [chunks][256]
   uint32_t *chunk_counter;
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) onesweep_kernel(PassArgs<KeyT
     uint32_t peers = __ballot_sync(0xffffffffu, d < kRadix);
 #pragma unroll
     for (int b = 0; b < kRadixBits; b++) {
+      if (b >= a.bits) break;            // higher digit bits are zero for every key
       const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
       peers &= ((d >> b) & 1u) ? bal : ~bal;
     }
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) onesweep_kernel(PassArgs<KeyT
 // (k0,v0) <-> (k1,v1); returns true when the result ends in (k1,v1).  With
 // hist_ready the caller has already accumulated the digit histograms.
 template <typename KeyT>
-static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uint32_t *count,
+static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uint32_t *count, int key_bits,
                        uint32_t n_fixed, uint32_t n_cap, int passes, int shift0, uint32_t *hist,
                        uint32_t *offsets, uint32_t *lookback, uint32_t *chunk_counters, bool hist_ready,
                        cudaStream_t s) {
@@ -263,6 +265,7 @@ static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uin
     a.count = count;
     a.n_fixed = n_fixed;
     a.shift = shift0 + p * kRadixBits;
+    a.bits = min(kRadixBits, key_bits - a.shift);
     a.offsets = offsets + p * kRadix;
     a.lookback = lookback + (size_t)p * chunks * kRadix;
     a.chunk_counter = chunk_counters + p;
@@ -647,7 +650,7 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
     uint32_t *k32 = reinterpret_cast<uint32_t *>(sc.dkeys_alt), *k32b = k32 + n;
     const int kb = min((int)((n + kSortThreads - 1) / kSortThreads), 148 * 8);
     depth_key32_kernel<<<kb, kSortThreads, 0, s>>>(dkeys, counters, n, k32, order, sc.hist);
-    radix_sort<uint32_t>(k32, order, k32b, sc.dvals_alt, nullptr, n, n, 4, 0, sc.hist, sc.offsets, sc.lookback,
+    radix_sort<uint32_t>(k32, order, k32b, sc.dvals_alt, nullptr, 32, n, n, 4, 0, sc.hist, sc.offsets, sc.lookback,
                          counters + C_CHUNK0, true, s);
     depth_fixup_kernel<<<(n + 255) / 256, 256, 0, s>>>(dkeys, counters, k32, order);
     const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
@@ -663,7 +666,9 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
     if (cap > 0) {
       uint32_t *ka = (pp & 1) ? sc.ptiles_alt : ptiles, *va = (pp & 1) ? sc.pids_alt : pids;
       uint32_t *kb = (pp & 1) ? ptiles : sc.ptiles_alt, *vb = (pp & 1) ? pids : sc.pids_alt;
-      radix_sort<uint32_t>(ka, va, kb, vb, counters + C_NSORT, 0, (uint32_t)cap, pp, 0, sc.hist + 8 * kRadix,
+      int tile_bits = 0;
+      while ((1 << tile_bits) < tiles) tile_bits++;
+      radix_sort<uint32_t>(ka, va, kb, vb, counters + C_NSORT, tile_bits, 0, (uint32_t)cap, pp, 0, sc.hist + 8 * kRadix,
                            sc.offsets + 8 * kRadix, sc.lookback + 8 * ((n + kSortChunk - 1) / kSortChunk) * kRadix,
                            counters + C_CHUNK0 + 8, true, s);
     }
