@@ -3,18 +3,20 @@
 //   depth sort   stable LSD radix sort of 31-bit keys monotone in the
 //                orderable f64 depth bits + exact fix-up of equal-key runs
 //                == Python's sort by (depth, index) (rasterize.py:121)
-//   scan         exclusive scan of tiles_touched in depth order -> pair offsets
-//   duplicate    every convex, visited in depth order, emits (tile, id) pairs
-//                for each tile of its bbox (the append loop of bin_tiles)
+//   duplicate    one fused kernel: exclusive scan of tiles_touched in depth
+//                order (decoupled look-back between 1024-rank chunks) and
+//                the (tile, id) pairs of every convex's bbox tiles, written
+//                in depth order (the append loop of bin_tiles), plus the
+//                digit histograms of the pair sort
 //   pair sort    stable radix sort by tile id only: since pairs are emitted in
 //                depth order, a stable sort by tile gives exactly the reference
 //                per-tile lists in (depth, index) order
 //   ranges       [start, end) of every tile in the sorted pairs
 //
-// Both radix sorts are onesweep (Adinets & Merrill): one global histogram
-// pass, then one kernel per 8-bit digit that ranks keys with warp
-// __match_any_sync, publishes per-chunk digit counts and resolves its prefix
-// by decoupled look-back.
+// Both radix sorts are onesweep (Adinets & Merrill): the digit histograms
+// come from the producing kernel, then one kernel per 8-bit digit ranks keys
+// with warp ballots, publishes per-chunk digit counts and resolves its
+// prefix by decoupled look-back.
 #include <algorithm>
 
 #include "common.cuh"
@@ -31,9 +33,6 @@ constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
 
-constexpr int kScanThreads = 512;
-constexpr int kScanItems = 4;
-constexpr int kScanChunk = kScanThreads * kScanItems;
 
 // ------------------------------------------------------------------ hist
 template <typename KeyT>
@@ -274,91 +273,6 @@ static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uin
   return passes & 1;
 }
 
-// ------------------------------------------------------------------ scan of tiles_touched in depth order
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t *order, const uint32_t *touched,
-                                                                   uint32_t n, uint32_t *block_sums) {
-  __shared__ uint32_t s[kScanThreads / 32];
-  uint32_t base = blockIdx.x * kScanChunk, acc = 0;
-  for (int i = 0; i < kScanItems; i++) {
-    uint32_t r = base + i * kScanThreads + threadIdx.x;
-    if (r < n) acc += touched[order[r]];
-  }
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint32_t v = threadIdx.x < kScanThreads / 32 ? s[threadIdx.x] : 0;
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) block_sums[blockIdx.x] = v;
-  }
-}
-
-// single block: exclusive scan of the block sums (uint64 to detect overflow)
-__global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t *block_sums, int nb, uint32_t *counters,
-                                                        uint64_t cap) {
-  __shared__ unsigned long long s[1024];
-  __shared__ unsigned long long carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < nb; base += 1024) {
-    int i = base + threadIdx.x;
-    unsigned long long v = i < nb ? block_sums[i] : 0;
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int d = 1; d < 1024; d <<= 1) {
-      unsigned long long u = threadIdx.x >= d ? s[threadIdx.x - d] : 0;
-      __syncthreads();
-      s[threadIdx.x] += u;
-      __syncthreads();
-    }
-    if (i < nb) block_sums[i] = (uint32_t)(carry + s[threadIdx.x] - v);
-    __syncthreads();
-    if (threadIdx.x == 1023) carry += s[1023];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    counters[C_NPAIRS] = carry > 0xffffffffull ? 0xffffffffu : (uint32_t)carry;
-    counters[C_OVERFLOW] = carry > cap ? 1u : 0u;
-    counters[C_NSORT] = carry > cap ? 0u : (uint32_t)carry;  // pairs the sort may touch
-  }
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t *order, const uint32_t *touched,
-                                                                 uint32_t n, const uint32_t *block_sums,
-                                                                 uint32_t *offsets) {
-  __shared__ uint32_t s[kScanThreads / 32];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  uint32_t base = blockIdx.x * kScanChunk + t * kScanItems;
-  uint32_t v[kScanItems], acc = 0;
-  for (int i = 0; i < kScanItems; i++) {
-    uint32_t r = base + i;
-    v[i] = r < n ? touched[order[r]] : 0;
-    acc += v[i];
-  }
-  uint32_t inc = acc;
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += u;
-  }
-  if (lane == 31) s[w] = inc;
-  __syncthreads();
-  if (w == 0) {
-    uint32_t x = lane < kScanThreads / 32 ? s[lane] : 0, y = x;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t u = __shfl_up_sync(0xffffffffu, y, o);
-      if (lane >= o) y += u;
-    }
-    if (lane < kScanThreads / 32) s[lane] = y - x;
-  }
-  __syncthreads();
-  uint32_t run = block_sums[blockIdx.x] + s[w] + inc - acc;
-  for (int i = 0; i < kScanItems; i++) {
-    uint32_t r = base + i;
-    if (r < n) offsets[r] = run;
-    run += v[i];
-  }
-}
-
 // ------------------------------------------------------------------ duplicate
 // A warp takes 32 consecutive depth ranks; their pairs occupy one contiguous
 // range of the pair arrays, which the warp writes cooperatively (coalesced).
@@ -367,43 +281,114 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t 
 constexpr int kDupThreads = 256;
 constexpr int kDupRounds = 4;   // ranks per block = kDupRounds * kDupThreads (fewer histogram flushes)
 
-__global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *order, const uint32_t *touched,
-                                                                const int4 *bbox, const uint32_t *offsets,
-                                                                uint32_t n, uint32_t cap, int tiles_x, int passes,
-                                                                uint32_t *pair_tiles, uint32_t *pair_ids,
-                                                                uint32_t *hist) {
+// Fused scan + duplicate: every block takes the next 1024 depth ranks (a
+// dynamic chunk id, so predecessors are always resident), sums their tile
+// counts, resolves its offset by decoupled look-back over the preceding
+// chunks (one warp, 32 predecessors per round) and emits its pairs.  This
+// replaces the three-kernel scan of tiles_touched (rasterize.py:134-144
+// append order == exclusive scan in depth order).
+constexpr uint64_t kDupFlagAgg = 1ull << 62, kDupFlagPrefix = 2ull << 62, kDupValue = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kDupThreads) duplicate_scan_kernel(
+    const uint32_t *order, const uint32_t *touched, const int4 *bbox, uint32_t n, uint32_t cap, int tiles_x,
+    int passes, uint32_t *pair_tiles, uint32_t *pair_ids, uint32_t *hist, uint32_t *offsets_out,
+    unsigned long long *lookback, uint32_t *chunk_counter, uint32_t *counters) {
+  constexpr int kRanks = kDupThreads * kDupRounds;
   __shared__ uint32_t s_h[3][kRadix];
-  for (int q = threadIdx.x; q < passes * kRadix; q += kDupThreads) s_h[q / kRadix][q % kRadix] = 0;
+  __shared__ uint32_t s_wtot[kDupRounds][kDupThreads / 32];
+  __shared__ uint32_t s_chunk;
+  __shared__ unsigned long long s_base;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) s_chunk = atomicAdd(chunk_counter, 1u);
+  for (int q = t; q < passes * kRadix; q += kDupThreads) s_h[q / kRadix][q % kRadix] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  // gather every round's convex first (independent loads in flight)
-  uint32_t id[kDupRounds], cnt[kDupRounds], off[kDupRounds];
+  const uint32_t chunk = s_chunk;
+  const uint32_t nchunks = (n + kRanks - 1) / kRanks;
+  uint32_t id[kDupRounds], cnt[kDupRounds], inc[kDupRounds];
 #pragma unroll
   for (int k = 0; k < kDupRounds; k++) {
-    const uint32_t r = (blockIdx.x * kDupRounds + k) * kDupThreads + threadIdx.x;
+    const uint32_t r = chunk * kRanks + k * kDupThreads + t;
     id[k] = r < n ? order[r] : 0u;
-    off[k] = r < n ? offsets[r] : 0u;
   }
 #pragma unroll
   for (int k = 0; k < kDupRounds; k++) {
-    const uint32_t r = (blockIdx.x * kDupRounds + k) * kDupThreads + threadIdx.x;
+    const uint32_t r = chunk * kRanks + k * kDupThreads + t;
     cnt[k] = r < n ? touched[id[k]] : 0u;
+    uint32_t v = cnt[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    inc[k] = v;
+    if (lane == 31) s_wtot[k][w] = v;
   }
+  __syncthreads();
+  // exclusive offset of each warp-round inside the chunk (rounds in order)
+  uint32_t before[kDupRounds];
+  uint32_t run = 0;
+#pragma unroll
+  for (int k = 0; k < kDupRounds; k++) {
+    uint32_t wb = run;
+    for (int ww = 0; ww < kDupThreads / 32; ww++) {
+      if (ww == w) wb = run;
+      run += s_wtot[k][ww];
+    }
+    before[k] = wb;
+  }
+  const uint32_t total = run;   // chunk total (<= 1024 * tiles, fits 32 bits)
+  if (w == 0) {
+    volatile unsigned long long *lb = lookback;
+    if (lane == 0) lb[chunk] = (chunk == 0 ? kDupFlagPrefix : kDupFlagAgg) | (unsigned long long)total;
+    unsigned long long excl = 0;
+    if (chunk > 0) {
+      int c = (int)chunk - 1;
+      while (true) {
+        const unsigned long long v = c - lane >= 0 ? lb[c - lane] : kDupFlagPrefix;
+        const uint64_t flag = v & ~kDupValue;
+        const uint32_t notready = __ballot_sync(0xffffffffu, flag == 0);
+        const uint32_t prefix = __ballot_sync(0xffffffffu, flag == kDupFlagPrefix);
+        const int fp = prefix ? __ffs(prefix) - 1 : 32;
+        const int nr = notready ? __ffs(notready) - 1 : 32;
+        if (nr <= fp && nr < 32) continue;   // a nearer predecessor has not published yet
+        unsigned long long part = lane <= fp ? (v & kDupValue) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (fp < 32) break;
+        c -= 32;
+      }
+      if (lane == 0) lb[chunk] = kDupFlagPrefix | (excl + total);
+    }
+    if (lane == 0) {
+      s_base = excl;
+      if (chunk + 1 == nchunks) {   // the grand total: pair count and capacity check
+        const unsigned long long all = excl + total;
+        counters[C_NPAIRS] = all > 0xffffffffull ? 0xffffffffu : (uint32_t)all;
+        counters[C_OVERFLOW] = all > cap ? 1u : 0u;
+        counters[C_NSORT] = all > cap ? 0u : (uint32_t)all;
+      }
+    }
+  }
+  __syncthreads();
+  const unsigned long long cbase = s_base;
 #pragma unroll 1
   for (int k = 0; k < kDupRounds; k++) {
+    const uint32_t r = chunk * kRanks + k * kDupThreads + t;
+    const unsigned long long off64 = cbase + before[k] + (inc[k] - cnt[k]);
+    const uint32_t off = off64 > 0xffffffffull ? 0xffffffffu : (uint32_t)off64;
+    if (r < n) offsets_out[r] = off;
     int tx0 = 0, ty0 = 0, wdt = 1;
     if (cnt[k]) {
       const int4 b = bbox[id[k]];
       tx0 = b.x / kTile;
       ty0 = b.z / kTile;
       wdt = (b.y - 1) / kTile - tx0 + 1;
-      // digit histograms of this convex's tile keys: digit 0 per tile, higher
-      // digits per row segment (a row of tiles rarely crosses a 256 boundary)
-      if ((uint64_t)off[k] + cnt[k] <= cap) {
+      if (off64 + cnt[k] <= cap) {   // digit histograms of the pairs that will be sorted
         const int ty1 = (b.w - 1) / kTile;
         for (int ty = ty0; ty <= ty1; ty++) {
           const uint32_t t0 = (uint32_t)(ty * tiles_x + tx0), t1 = t0 + (uint32_t)wdt - 1;
-          for (uint32_t t = t0; t <= t1; t++) atomicAdd(&s_h[0][t & (kRadix - 1)], 1u);
+          for (uint32_t tt = t0; tt <= t1; tt++) atomicAdd(&s_h[0][tt & (kRadix - 1)], 1u);
           for (int ps = 1; ps < passes; ps++) {
             const int sh = ps * kRadixBits;
             uint32_t seg = t0;
@@ -416,19 +401,12 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *
         }
       }
     }
-    // inclusive prefix of the counts inside the warp (its 32 ranks are contiguous)
-    uint32_t inc = cnt[k];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    const uint32_t base = __shfl_sync(0xffffffffu, off[k] - (inc - cnt[k]), 0);  // offset of the warp's first pair
-    const uint32_t excl = inc - cnt[k];
-    for (uint32_t p0 = 0; p0 < total; p0 += 32) {  // warp-uniform trip count
+    // the warp's 32 ranks are contiguous: write its pairs cooperatively
+    const uint32_t wtotal = __shfl_sync(0xffffffffu, inc[k], 31);
+    const uint64_t wbase = cbase + before[k];
+    const uint32_t excl = inc[k] - cnt[k];
+    for (uint32_t p0 = 0; p0 < wtotal; p0 += 32) {
       const uint32_t p = p0 + lane;
-      // owner = last lane whose exclusive prefix is <= p
       int lo = 0;
 #pragma unroll
       for (int step = 16; step >= 1; step >>= 1) {
@@ -440,15 +418,15 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const uint32_t *
       const int tx = __shfl_sync(0xffffffffu, tx0, lo) + (int)(q % (uint32_t)w_o);
       const int ty = __shfl_sync(0xffffffffu, ty0, lo) + (int)(q / (uint32_t)w_o);
       const uint32_t owner_id = __shfl_sync(0xffffffffu, id[k], lo);
-      const uint32_t pos = base + p;
-      if (p < total && pos < cap) {
+      const uint64_t pos = wbase + p;
+      if (p < wtotal && pos < cap) {
         pair_tiles[pos] = (uint32_t)(ty * tiles_x + tx);
         pair_ids[pos] = owner_id;
       }
     }
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < passes * kRadix; q += kDupThreads) {
+  for (int q = t; q < passes * kRadix; q += kDupThreads) {
     const uint32_t v = s_h[q / kRadix][q % kRadix];
     if (v) atomicAdd(&hist[q], v);
   }
@@ -608,7 +586,7 @@ size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, Scratch *sc, char 
   char *p4 = take(sizeof(uint32_t) * 16 * kRadix);
   char *p5 = take(sizeof(uint32_t) * 16 * kRadix);
   char *p6 = take(sizeof(uint32_t) * lb_words);
-  char *p7 = take(sizeof(uint32_t) * ((n + kScanChunk - 1) / kScanChunk + 1));
+  char *p7 = take(sizeof(uint64_t) * ((n + 1023) / 1024 + 2));   // duplicate-scan look-back
   if (sc) {
     sc->dkeys_alt = (uint64_t *)p0; sc->dvals_alt = (uint32_t *)p1;
     sc->ptiles_alt = (uint32_t *)p2; sc->pids_alt = (uint32_t *)p3;
@@ -653,16 +631,15 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
     radix_sort<uint32_t>(k32, order, k32b, sc.dvals_alt, nullptr, 32, n, n, 4, 0, sc.hist, sc.offsets, sc.lookback,
                          counters + C_CHUNK0, true, s);
     depth_fixup_kernel<<<(n + 255) / 256, 256, 0, s>>>(dkeys, counters, k32, order);
-    const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
-    scan_reduce_kernel<<<nb, kScanThreads, 0, s>>>(order, touched, n, sc.block_sums);
-    scan_top_kernel<<<1, 1024, 0, s>>>(sc.block_sums, nb, counters, (uint64_t)cap);
-    scan_down_kernel<<<nb, kScanThreads, 0, s>>>(order, touched, n, sc.block_sums, offs);
     // pairs land in the buffer that makes the sorted result end in (ptiles, pids)
     uint32_t *dt = (pp & 1) ? sc.ptiles_alt : ptiles;
     uint32_t *di = (pp & 1) ? sc.pids_alt : pids;
-    duplicate_kernel<<<(n + kDupThreads * kDupRounds - 1) / (kDupThreads * kDupRounds), kDupThreads, 0, s>>>(
-        order, touched, reinterpret_cast<const int4 *>(ws + L.bbox), offs, n, (uint32_t)cap, L.tiles_x, pp, dt, di,
-        sc.hist + 8 * kRadix);
+    const uint32_t dchunks = (n + kDupThreads * kDupRounds - 1) / (kDupThreads * kDupRounds);
+    cudaMemsetAsync(sc.block_sums, 0, sizeof(uint64_t) * dchunks, s);
+    duplicate_scan_kernel<<<dchunks, kDupThreads, 0, s>>>(
+        order, touched, reinterpret_cast<const int4 *>(ws + L.bbox), n, (uint32_t)cap, L.tiles_x, pp, dt, di,
+        sc.hist + 8 * kRadix, offs, reinterpret_cast<unsigned long long *>(sc.block_sums), counters + C_CHUNK0 + 6,
+        counters);
     if (cap > 0) {
       uint32_t *ka = (pp & 1) ? sc.ptiles_alt : ptiles, *va = (pp & 1) ? sc.pids_alt : pids;
       uint32_t *kb = (pp & 1) ? ptiles : sc.ptiles_alt, *vb = (pp & 1) ? pids : sc.pids_alt;
