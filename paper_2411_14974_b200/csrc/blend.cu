@@ -543,7 +543,10 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
 // reduces the 32 screen-space gradient values of each candidate across the
 // warp (transpose-reduce) into one vector of float atomics.
 template <int MAXK>
-__global__ void __launch_bounds__(kPipeThreads, 3) backward_kernel(BlendArgs a) {
+#ifndef CS_BWD_MINB
+#define CS_BWD_MINB 4   // 4 blocks/SM with a small spill beat 3 without (926 vs 934 us)
+#endif
+__global__ void __launch_bounds__(kPipeThreads, CS_BWD_MINB) backward_kernel(BlendArgs a) {
   constexpr int AF = Acc<MAXK>::kFloats;
   constexpr int NG = (AF + 31) / 32;  // 32-value groups
   constexpr int kStages = CS_BWD_STAGES;
