@@ -95,3 +95,38 @@ def test_error_strings(lib):
     for code in range(5):
         assert lib.cs_error_string(code)
     assert b"unknown" in lib.cs_error_string(99)
+
+
+def test_training_and_scene_structs_match_the_header(lib):
+    assert ctypes.sizeof(_lib.CsViewSignal) == 3 * 8
+    assert ctypes.sizeof(_lib.CsAdamTensor) == 4 * 8 + 8 + 8
+    assert ctypes.sizeof(_lib.CsSceneOut) == 6 * 8
+    assert ctypes.sizeof(_lib.CsDensityConfig) == 6 * 8 + 2 * 4
+
+
+def test_training_entry_points_validate_before_launching(lib):
+    """Argument checks of cs_image_loss / cs_adam_step / cs_checkpoint_* /
+    cs_density_* run on the host (no device needed): losses.py:60-63 size
+    check, precision 16|32, K range, null pointers."""
+    size = ctypes.c_size_t()
+    assert lib.cs_image_loss_workspace(10, 40, ctypes.byref(size)) == 1
+    assert lib.cs_image_loss_workspace(70, 100, ctypes.byref(size)) == 0
+    assert size.value == 4 * 9 * 60 * 90
+    one = ctypes.c_void_p(1)
+    assert lib.cs_image_loss(70, 100, None, one, one, 3, 0.2, 5e-4, one, one, one, one, size.value, None) == 1
+    assert lib.cs_image_loss(70, 100, one, one, one, 3, 0.2, 5e-4, one, one, one, one, size.value - 4, None) == 3
+    assert lib.cs_adam_step(9, None, 0.9, 0.999, 1e-15, 1, 1.0, None) == 1
+    t = (_lib.CsAdamTensor * 1)()
+    assert lib.cs_adam_step(1, t, 0.9, 0.999, 1e-15, 0, 1.0, None) == 1        # step counts from 1
+    assert lib.cs_adam_step(0, t, 0.9, 0.999, 1e-15, 1, 1.0, None) == 0        # nothing to do
+    out = _lib.CsSceneOut()
+    assert lib.cs_checkpoint_unpack(8, 1, 6, one, ctypes.byref(out), None) == 1
+    assert lib.cs_checkpoint_unpack(32, 1, 2, one, ctypes.byref(out), None) == 1
+    assert lib.cs_checkpoint_pack(16, 1, 6, ctypes.byref(out), one, None) == 1   # null arrays
+    assert lib.cs_checkpoint_unpack(16, 0, 6, None, None, None) == 0              # empty scene
+    p = _lib.CsParams()
+    p.n, p.k = 0, 6
+    cfg = _lib.CsDensityConfig()
+    assert lib.cs_density_flags(ctypes.byref(p), None, None, None, None, None, None, None) == 1
+    assert lib.cs_density_flags(ctypes.byref(p), None, ctypes.byref(cfg), None, None, None, None, None) == 0
+    assert lib.cs_abi_version() == _lib.ABI_VERSION == 3
