@@ -223,6 +223,9 @@ class ViewShardedStep:
     def step(self, batch: list) -> dict:
         self.iteration += 1
         info = self.accumulate(batch)
+        check = getattr(self.view_grad_fn, "check_overflow", None)
+        while check is not None and check():   # a view overflowed its pair capacity: redo with more room
+            info = self.accumulate(batch)
         self.reduce(len(batch))
         self.adam.step(self.params, self.flat.grads(), self.lrs(self.iteration), grad_scale=1.0 / len(batch))
         # densification signal since the last densify round (trainer.py:192-193)
@@ -259,22 +262,49 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
     (cs_image_loss; adds the mask-loss gradient, trainer.py:176), backward
     through the C ABI accumulating into the flat buffers together with the
     view's sigma signal (cs_backward_signal).  Returns the view's loss as a
-    device scalar (no host synchronisation besides the forward's pair count)."""
-    from .rasterizer import default_rasterizer
+    device scalar.
+
+    No host synchronisation per view: one workspace is reused by every view
+    (stream order serialises them) and the forwards run with the cached pair
+    capacity; each view's pair count and overflow flag are folded into a
+    device maximum that ``check_overflow`` reads once per step -- if any view
+    overflowed, the step is redone with a larger capacity (ViewShardedStep)."""
+    from .rasterizer import Workspace, default_rasterizer
     from .train_ops import LossWorkspace, image_loss as cuda_image_loss
 
     r = rasterizer or default_rasterizer(scene.device)
     lw = LossWorkspace()
+    ws = Workspace(scene.device)
+    state = {"cap": None, "max": torch.zeros(2, dtype=torch.int32, device=scene.device)}
 
     def fn(view, grads: dict, signal: dict):
         cam, target = view
-        fr = r.forward(scene, cam, mode, settings)
+        if state["cap"] is None:      # first view ever: size the capacity with a checked forward
+            fr = r.forward(scene, cam, mode, settings, workspace=ws)
+            state["cap"] = fr.capacity
+        else:
+            fr = r.forward(scene, cam, mode, settings, workspace=ws, capacity=state["cap"], check=False)
+        torch.maximum(state["max"], ws.counters()[1:3], out=state["max"])   # (pairs, overflow)
         loss = cuda_image_loss(fr.image, target, scene.raw_mask, config.lambda_dssim, config.beta_mask,
                                d_raw_mask=grads["raw_mask"], workspace=lw)
         r.launch_backward(fr, loss["d_image"], grads,
                           signal=(signal["sigma_signal"], signal["sigma_views"], fr.visible))
         return loss["total"]
+
+    def check_overflow() -> bool:
+        """One host read per step: True (and a larger capacity) if any view
+        overflowed its pair capacity since the last check."""
+        pairs, ovf = (int(v) for v in state["max"].cpu())
+        state["max"].zero_()
+        if ovf:
+            state["cap"] = int(pairs * 1.25) + 1024
+            if state["cap"] >= (1 << 30):
+                raise RuntimeError(f"{pairs} tile pairs exceed the supported 2^30")
+            return True
+        return False
+
     fn.handles_signal = True
+    fn.check_overflow = check_overflow
     return fn
 
 
