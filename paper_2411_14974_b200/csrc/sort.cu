@@ -379,11 +379,13 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_scan_kernel(
     const uint32_t off = off64 > 0xffffffffull ? 0xffffffffu : (uint32_t)off64;
     if (r < n) offsets_out[r] = off;
     int tx0 = 0, ty0 = 0, wdt = 1;
+    float inv_wdt = 1.f;
     if (cnt[k]) {
       const int4 b = bbox[id[k]];
       tx0 = b.x / kTile;
       ty0 = b.z / kTile;
       wdt = (b.y - 1) / kTile - tx0 + 1;
+      inv_wdt = 1.f / (float)wdt;
       if (off64 + cnt[k] <= cap) {   // digit histograms of the pairs that will be sorted
         const int ty1 = (b.w - 1) / kTile;
         for (int ty = ty0; ty <= ty1; ty++) {
@@ -415,8 +417,13 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_scan_kernel(
       }
       const uint32_t q = p - __shfl_sync(0xffffffffu, excl, lo);
       const int w_o = __shfl_sync(0xffffffffu, wdt, lo);
-      const int tx = __shfl_sync(0xffffffffu, tx0, lo) + (int)(q % (uint32_t)w_o);
-      const int ty = __shfl_sync(0xffffffffu, ty0, lo) + (int)(q / (uint32_t)w_o);
+      // q / w_o by a float reciprocal plus a one-step correction (exact for
+      // any q < 2^24), instead of an integer division
+      int qy = (int)(((float)q + 0.5f) * __shfl_sync(0xffffffffu, inv_wdt, lo));
+      if (qy * w_o > (int)q) qy--;
+      else if ((qy + 1) * w_o <= (int)q) qy++;
+      const int tx = __shfl_sync(0xffffffffu, tx0, lo) + ((int)q - qy * w_o);
+      const int ty = __shfl_sync(0xffffffffu, ty0, lo) + qy;
       const uint32_t owner_id = __shfl_sync(0xffffffffu, id[k], lo);
       const uint64_t pos = wbase + p;
       if (p < wtotal && pos < cap) {
