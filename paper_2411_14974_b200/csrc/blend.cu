@@ -30,6 +30,7 @@ struct BlendArgs {
   const float *records;
   const uint32_t *pair_ids;
   const uint2 *ranges;
+  const uint32_t *tile_order;   // heaviest tiles first (null: index order)
   int width, height, tiles_x;
   float cutoff, floor;
   float bg[3];
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kPipeThreads, 4) forward_kernel(BlendArgs a) {
   constexpr int kStages = CS_FWD_STAGES;
   extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
   PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
-  const int tile = blockIdx.x;
+  const int tile = a.tile_order ? (int)a.tile_order[blockIdx.x] : (int)blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint2 range = a.ranges[tile];
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(kPipeThreads, CS_BWD_MINB) backward_kernel(Ble
   extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
   PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
   __shared__ int s_last[kConsumers];
-  const int tile = blockIdx.x;
+  const int tile = a.tile_order ? (int)a.tile_order[blockIdx.x] : (int)blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint2 range = a.ranges[tile];
@@ -660,6 +661,7 @@ static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const c
   a.records = reinterpret_cast<const float *>(ws + L.records);
   a.pair_ids = reinterpret_cast<const uint32_t *>(ws + L.pair_ids);
   a.ranges = reinterpret_cast<const uint2 *>(ws + L.tile_ranges);
+  a.tile_order = L.tiles_x * L.tiles_y <= kMaxTileOrder ? reinterpret_cast<const uint32_t *>(ws + L.scratch) : nullptr;
   a.width = cam.width;
   a.height = cam.height;
   a.tiles_x = L.tiles_x;

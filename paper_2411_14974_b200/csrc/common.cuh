@@ -16,6 +16,8 @@ constexpr double kAlphaMaxD = 1.0 - 1e-6; // rasterize.py:30
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr uint64_t kCulledKey = ~0ull;
+// tiles ordered heaviest first for the blends (scratch + 0); larger frames use index order
+constexpr int kMaxTileOrder = 1 << 17;
 
 // ---------------------------------------------------------------------------
 // Per-convex blend record (float32), written by the preprocess kernel and

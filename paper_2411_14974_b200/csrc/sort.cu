@@ -567,6 +567,40 @@ __global__ void depth_fixup_kernel(const uint64_t *keys64, const uint32_t *count
   }
 }
 
+// ------------------------------------------------------------------ tile order
+// The blend kernels take tiles heaviest first (candidate-list length, log
+// buckets): the long tiles start in the first wave instead of forming the
+// grid's tail.  One block: bucket histogram, scan, scatter.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2 *ranges, int tiles, uint32_t *order) {
+  __shared__ uint32_t h[256], base[256];
+  const int t = threadIdx.x;
+  if (t < 256) h[t] = 0;
+  __syncthreads();
+  auto bucket = [&](int tile) {   // 255 - ~20 log2(len + 1): heavy tiles get small buckets
+    const uint2 r = ranges[tile];
+    const uint32_t len = r.y > r.x ? r.y - r.x : 0u;
+    return 255 - min(255, (int)(20.f * __log2f((float)len + 1.f)));
+  };
+  for (int q = t; q < tiles; q += 1024) atomicAdd(&h[bucket(q)], 1u);
+  __syncthreads();
+  if (t < 32) {   // exclusive scan of the 256 buckets, 8 per lane
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) { v[i] = h[t * 8 + i]; sum += v[i]; }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (t >= o) inc += u;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int i = 0; i < 8; i++) { base[t * 8 + i] = run; run += v[i]; }
+  }
+  __syncthreads();
+  for (int q = t; q < tiles; q += 1024) order[atomicAdd(&base[bucket(q)], 1u)] = (uint32_t)q;
+}
+
 // ------------------------------------------------------------------ orchestration
 struct Scratch {
   uint64_t *dkeys_alt;
@@ -586,6 +620,7 @@ size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, Scratch *sc, char 
   const size_t dchunks = (size_t)((n + kSortChunk - 1) / kSortChunk);
   const size_t pchunks = (size_t)((cap + kSortChunk - 1) / kSortChunk);
   const size_t lb_words = (8 * dchunks + pair_passes * pchunks) * kRadix;
+  take(sizeof(uint32_t) * kMaxTileOrder);   // tile_order first: the blends find it at scratch + 0
   char *p0 = take(sizeof(uint64_t) * n);
   char *p1 = take(sizeof(uint32_t) * n);
   char *p2 = take(sizeof(uint32_t) * cap);
@@ -659,6 +694,8 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
     const int rb = (int)std::min<int64_t>((cap + 1023) / 1024, 148 * 16);
     if (rb > 0) ranges_kernel<<<rb, 256, 0, s>>>(ptiles, counters, ranges);
   }
+  if (tiles <= kMaxTileOrder)
+    tile_order_kernel<<<1, 1024, 0, s>>>(ranges, tiles, reinterpret_cast<uint32_t *>(ws + L.scratch));
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
 
