@@ -163,7 +163,7 @@ __device__ __forceinline__ Eval eval_field(const LineSet<NL, MAXK> &L, float sig
 }
 
 // ---------------------------------------------------------------------------
-// Producer/consumer pipeline shared by both blend kernels.  Warp kConsumers
+// Producer/consumer pipeline shared by both blend kernels.  Warp NC
 // (the producer) streams the tile's candidate records into a ring of kStages
 // shared-memory stages of kStageCands records, one TMA bulk copy
 // (cp.async.bulk) per 16-byte-aligned record row, completion counted on the
@@ -175,8 +175,16 @@ __device__ __forceinline__ Eval eval_field(const LineSet<NL, MAXK> &L, float sig
 // Forward only: consumers OR the stage's candidates that blended somewhere
 // into `vis`; the producer writes visible[] for them when it recycles the
 // stage (rasterize.py:203 `visible[idx] = True`).
-constexpr int kConsumers = 8;
-constexpr int kPipeThreads = 32 * (kConsumers + 1);
+// Consumer warps per block: 8 cover a whole 16x16 tile; 4 cover half of it
+// (two blocks per tile, each streaming the tile's list) -- smaller blocks
+// finish sooner and leave fewer idle warps behind (measured per kernel).
+#ifndef CS_FWD_NC
+#define CS_FWD_NC 8
+#endif
+#ifndef CS_BWD_NC
+#define CS_BWD_NC 8
+#endif
+template <int NC> __host__ __device__ constexpr int pipe_threads() { return 32 * (NC + 1); }
 // Ring depth: the forward stops early (saturated pixels), so a deep ring
 // mostly prefetches records nobody evaluates; the backward walks the whole
 // list up to each warp's last candidate and profits from more lookahead
@@ -216,7 +224,7 @@ __device__ __forceinline__ void flush_visible(PipeSmem<MAXK, kStages> &sm, int s
 }
 
 // Producer warp: batch b covers pair indices first(b) .. first(b)+count(b)-1.
-template <int MAXK, int kStages, typename Batch>
+template <int MAXK, int kStages, int NC, typename Batch>
 __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const float *records, const uint32_t *pair_ids,
                                              int nbatch, Batch batch, bool forward, uint8_t *visible) {
   constexpr int RB = Rec<MAXK>::kFloats * 4;
@@ -237,7 +245,7 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
       mbar_wait(&sm.empty[s], (u - 1) & 1);  // batch b - kStages released by every consumer
       if (forward) flush_visible(sm, s, visible);
     }
-    if (forward && *reinterpret_cast<volatile int *>(&sm.ndone) == kConsumers) {
+    if (forward && *reinterpret_cast<volatile int *>(&sm.ndone) == NC) {
       // stop = b + 1: consumers leave at batch b.  Consumers still behind
       // (done warps lag) keep releasing the issued batches < b normally.
       if (lane == 0) *reinterpret_cast<volatile int *>(&sm.stop) = b + 1;
@@ -296,7 +304,7 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
   }
 }
 
-template <int MAXK, int kStages>
+template <int MAXK, int kStages, int NC>
 __device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages> &sm) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
@@ -305,7 +313,7 @@ __device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages> &sm) {
 #else
       mbar_init(&sm.full[s], 32);   // one cp.async arrival per producer lane
 #endif
-      mbar_init(&sm.empty[s], kConsumers);
+      mbar_init(&sm.empty[s], NC);
       sm.vis[s] = 0u;
     }
     sm.ndone = 0;
@@ -350,19 +358,25 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float qx, float
 
 // Forward blend (rasterize.py:178-209), one 16x16 tile per block.
 template <int MAXK>
-__global__ void __launch_bounds__(kPipeThreads, 4) forward_kernel(BlendArgs a) {
+#ifndef CS_FWD_MINB
+#define CS_FWD_MINB (CS_FWD_NC == 8 ? 4 : 7)
+#endif
+__global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forward_kernel(BlendArgs a) {
   constexpr int kStages = CS_FWD_STAGES;
+  constexpr int NC = CS_FWD_NC;
+  const int half = NC == 8 ? 0 : (int)(blockIdx.x & 1);   // which half of the tile (NC == 4)
+  const int unit = NC == 8 ? (int)blockIdx.x : (int)(blockIdx.x >> 1);
   extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
   PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
-  const int tile = a.tile_order ? (int)a.tile_order[blockIdx.x] : (int)blockIdx.x;
+  const int tile = a.tile_order ? (int)a.tile_order[unit] : unit;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint2 range = a.ranges[tile];
   const int nbatch = (int)((range.y - range.x + kStageCands - 1) / kStageCands);
-  pipe_init(sm);
+  pipe_init<MAXK, kStages, NC>(sm);
   unsigned n_eval = 0, n_lines = 0, n_blend = 0, n_warp_evals = 0;
-  if (warp == kConsumers) {
-    pipe_produce<MAXK, kStages>(sm, a.records, a.pair_ids, nbatch,
+  if (warp == NC) {
+    pipe_produce<MAXK, kStages, NC>(sm, a.records, a.pair_ids, nbatch,
                        [&](int b, uint32_t &first, uint32_t &count) {
                          first = range.x + (uint32_t)b * kStageCands;
                          count = min((uint32_t)kStageCands, range.y - first);
@@ -370,8 +384,9 @@ __global__ void __launch_bounds__(kPipeThreads, 4) forward_kernel(BlendArgs a) {
   } else {
     int lx, ly;
     tile_pixel(threadIdx.x, lx, ly);
+    ly += half * 8;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
-    const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2);
+    const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2) + half * 8;
     const bool inside = px < a.width && py < a.height;
     const float qx = px + 0.5f, qy = py + 0.5f;
     FwdPixel P;
@@ -545,24 +560,28 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
 // warp (transpose-reduce) into one vector of float atomics.
 template <int MAXK>
 #ifndef CS_BWD_MINB
-#define CS_BWD_MINB 4   // 4 blocks/SM with a small spill beat 3 without (926 vs 934 us)
+#define CS_BWD_MINB (CS_BWD_NC == 8 ? 4 : 7)   // 8 warps: 4 blocks/SM with a small spill beat 3 without (926 vs 934 us)
 #endif
-__global__ void __launch_bounds__(kPipeThreads, CS_BWD_MINB) backward_kernel(BlendArgs a) {
+__global__ void __launch_bounds__(pipe_threads<CS_BWD_NC>(), CS_BWD_MINB) backward_kernel(BlendArgs a) {
+  constexpr int NC = CS_BWD_NC;
+  const int half = NC == 8 ? 0 : (int)(blockIdx.x & 1);
+  const int unit = NC == 8 ? (int)blockIdx.x : (int)(blockIdx.x >> 1);
   constexpr int AF = Acc<MAXK>::kFloats;
   constexpr int NG = (AF + 31) / 32;  // 32-value groups
   constexpr int kStages = CS_BWD_STAGES;
   extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
   PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
-  __shared__ int s_last[kConsumers];
-  const int tile = a.tile_order ? (int)a.tile_order[blockIdx.x] : (int)blockIdx.x;
+  __shared__ int s_last[NC];
+  const int tile = a.tile_order ? (int)a.tile_order[unit] : unit;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint2 range = a.ranges[tile];
   // consumer pixel state
   int lx = 0, ly = 0;
-  if (warp < kConsumers) tile_pixel(threadIdx.x, lx, ly);
+  if (warp < NC) tile_pixel(threadIdx.x, lx, ly);
+  ly += half * 8;
   const int px = tx * kTile + lx, py = ty * kTile + ly;
-  const bool inside = warp < kConsumers && px < a.width && py < a.height;
+  const bool inside = warp < NC && px < a.width && py < a.height;
   BwdPixel P;
   P.T = 1.f; P.g0 = P.g1 = P.g2 = P.S0 = P.S1 = P.S2 = 0.f;
   P.last = -1;
@@ -579,11 +598,11 @@ __global__ void __launch_bounds__(kPipeThreads, CS_BWD_MINB) backward_kernel(Ble
     P.S2 = P.T * a.bg[2];
   }
   const int warp_last = __reduce_max_sync(0xffffffffu, P.last);
-  if (warp < kConsumers && lane == 0) s_last[warp] = warp_last;
-  pipe_init(sm);  // (its __syncthreads also publishes s_last)
+  if (warp < NC && lane == 0) s_last[warp] = warp_last;
+  pipe_init<MAXK, kStages, NC>(sm);  // (its __syncthreads also publishes s_last)
   int block_last = s_last[0];
 #pragma unroll
-  for (int w = 1; w < kConsumers; w++) block_last = max(block_last, s_last[w]);
+  for (int w = 1; w < NC; w++) block_last = max(block_last, s_last[w]);
   // batches back to front over [range.x, block_last]
   const int64_t end = (int64_t)block_last + 1;
   const int nbatch = end > (int64_t)range.x ? (int)((end - range.x + kStageCands - 1) / kStageCands) : 0;
@@ -594,10 +613,10 @@ __global__ void __launch_bounds__(kPipeThreads, CS_BWD_MINB) backward_kernel(Ble
     count = (uint32_t)(hi - lo);
   };
   unsigned n_eval = 0, n_lines = 0, n_warp_evals = 0;
-  if (warp == kConsumers) {
-    pipe_produce<MAXK, kStages>(sm, a.records, a.pair_ids, nbatch, batch, false, nullptr);
+  if (warp == NC) {
+    pipe_produce<MAXK, kStages, NC>(sm, a.records, a.pair_ids, nbatch, batch, false, nullptr);
   } else {
-    const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2);
+    const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2) + half * 8;
     const float qx = px + 0.5f, qy = py + 0.5f;
     for (int b = 0; b < nbatch; b++) {
       const int s = b % kStages;
@@ -693,10 +712,10 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
   const int tiles = L.tiles_x * L.tiles_y;
   if (L.max_k == 8) {
     cudaFuncSetAttribute(forward_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
-    forward_kernel<8><<<tiles, kPipeThreads, sizeof(PipeSmem<8, CS_FWD_STAGES>), s>>>(a);
+    forward_kernel<8><<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<8, CS_FWD_STAGES>), s>>>(a);
   } else {
     cudaFuncSetAttribute(forward_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_FWD_STAGES>));
-    forward_kernel<16><<<tiles, kPipeThreads, sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
+    forward_kernel<16><<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
@@ -709,10 +728,10 @@ int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs
   const int tiles = L.tiles_x * L.tiles_y;
   if (L.max_k == 8) {
     cudaFuncSetAttribute(backward_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_BWD_STAGES>));
-    backward_kernel<8><<<tiles, kPipeThreads, sizeof(PipeSmem<8, CS_BWD_STAGES>), s>>>(a);
+    backward_kernel<8><<<tiles * (8 / CS_BWD_NC), pipe_threads<CS_BWD_NC>(), sizeof(PipeSmem<8, CS_BWD_STAGES>), s>>>(a);
   } else {
     cudaFuncSetAttribute(backward_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_BWD_STAGES>));
-    backward_kernel<16><<<tiles, kPipeThreads, sizeof(PipeSmem<16, CS_BWD_STAGES>), s>>>(a);
+    backward_kernel<16><<<tiles * (8 / CS_BWD_NC), pipe_threads<CS_BWD_NC>(), sizeof(PipeSmem<16, CS_BWD_STAGES>), s>>>(a);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
