@@ -1,6 +1,6 @@
 // K2: depth order + tile binning (rasterize.py:121 sort, rasterize.py:134-144).
 //
-//   depth sort   stable LSD radix sort of 31-bit keys monotone in the
+//   depth sort   stable LSD radix sort of 24-bit keys monotone in the
 //                orderable f64 depth bits + exact fix-up of equal-key runs
 //                == Python's sort by (depth, index) (rasterize.py:121)
 //   duplicate    one fused kernel: exclusive scan of tiles_touched in depth
@@ -468,13 +468,16 @@ __global__ void __launch_bounds__(256) ranges_kernel(const uint32_t *pair_tiles,
 
 // ------------------------------------------------------------------ depth order
 // The depth order sorts (f64 depth, index) (rasterize.py:121).  Instead of a
-// 64-bit radix sort (8 passes) the keys are reduced to 31 bits,
-//   key32 = (key64 - kmin) >> shift,   shift = max(0, bits(kmax - kmin) - 31),
-// which is monotone in key64; a stable 4-pass sort by key32 then orders
+// 64-bit radix sort (8 passes) the keys are reduced to 23 bits,
+//   key32 = (key64 - kmin) >> shift,   shift = max(0, bits(kmax - kmin) - 23),
+// which is monotone in key64; a stable 3-pass sort by key32 then orders
 // (key32, index).  Only runs of EQUAL key32 can be out of (key64, index)
 // order, and only when shift > 0; depth_fixup_kernel re-sorts those runs by
 // the full key (they are a few items long on real scenes).  Culled convexes
-// get key32 = ~0 and stay at the end, in index order.
+// get key32 = 0xffffff and stay at the end, in index order.
+constexpr int kDepthBits = 23, kDepthPasses = 3;
+constexpr uint32_t kDepthCulled = (1u << (kDepthBits + 1)) - 1;
+
 __device__ __forceinline__ void depth_range(const uint32_t *counters, uint64_t &kmin, int &shift, bool &any) {
   const uint64_t kminc = *reinterpret_cast<const unsigned long long *>(counters + C_KMINC);
   const uint64_t kmax = *reinterpret_cast<const unsigned long long *>(counters + C_KMAX);
@@ -482,14 +485,14 @@ __device__ __forceinline__ void depth_range(const uint32_t *counters, uint64_t &
   kmin = ~kminc;
   const uint64_t range = any ? kmax - kmin : 0ull;
   const int bits = range ? 64 - __clzll((long long)range) : 0;
-  shift = bits > 31 ? bits - 31 : 0;
+  shift = bits > kDepthBits ? bits - kDepthBits : 0;
 }
 
 __global__ void __launch_bounds__(kSortThreads) depth_key32_kernel(const uint64_t *keys64, const uint32_t *counters,
                                                                    uint32_t n, uint32_t *keys32, uint32_t *order,
                                                                    uint32_t *hist) {
-  __shared__ uint32_t h[4][kRadix];
-  for (int q = threadIdx.x; q < 4 * kRadix; q += kSortThreads) h[q / kRadix][q % kRadix] = 0;
+  __shared__ uint32_t h[kDepthPasses][kRadix];
+  for (int q = threadIdx.x; q < kDepthPasses * kRadix; q += kSortThreads) h[q / kRadix][q % kRadix] = 0;
   __syncthreads();
   uint64_t kmin;
   int shift;
@@ -497,11 +500,11 @@ __global__ void __launch_bounds__(kSortThreads) depth_key32_kernel(const uint64_
   depth_range(counters, kmin, shift, any);
   for (uint32_t idx = blockIdx.x * kSortThreads + threadIdx.x; idx < n; idx += gridDim.x * kSortThreads) {
     const uint64_t k = keys64[idx];
-    const uint32_t k32 = k == kCulledKey ? 0xffffffffu : (uint32_t)((k - kmin) >> shift);
+    const uint32_t k32 = k == kCulledKey ? kDepthCulled : (uint32_t)((k - kmin) >> shift);
     keys32[idx] = k32;
     order[idx] = idx;
 #pragma unroll
-    for (int p = 0; p < 4; p++) {   // one shared atomic when the whole warp shares the digit (depths cluster)
+    for (int p = 0; p < kDepthPasses; p++) {   // one shared atomic when the whole warp shares the digit (depths cluster)
       const uint32_t d = (k32 >> (p * kRadixBits)) & (kRadix - 1);
       const uint32_t act = __activemask();
       const uint32_t d0 = __shfl_sync(act, d, __ffs(act) - 1);
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(kSortThreads) depth_key32_kernel(const uint64_
     }
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < 4 * kRadix; q += kSortThreads) {
+  for (int q = threadIdx.x; q < kDepthPasses * kRadix; q += kSortThreads) {
     const uint32_t v = h[q / kRadix][q % kRadix];
     if (v) atomicAdd(&hist[q], v);
   }
@@ -665,13 +668,15 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
   cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * sc.lookback_words, s);
   cudaMemsetAsync(ranges, 0, sizeof(uint2) * tiles, s);   // empty tiles (and n == 0) read (0, 0)
   if (n > 0) {
-    // depth order: 31-bit keys, 4 passes (even) -> (keys32, order), then
-    // the exact fix-up of equal-key runs
+    // depth order: 24-bit keys, 3 passes (odd: start in the alternate
+    // buffers so the result ends in (keys32, order)), then the exact fix-up
+    // of equal-key runs
+    static_assert(kDepthPasses == 3, "odd pass count assumed below");
     uint32_t *k32 = reinterpret_cast<uint32_t *>(sc.dkeys_alt), *k32b = k32 + n;
     const int kb = min((int)((n + kSortThreads - 1) / kSortThreads), 148 * 8);
-    depth_key32_kernel<<<kb, kSortThreads, 0, s>>>(dkeys, counters, n, k32, order, sc.hist);
-    radix_sort<uint32_t>(k32, order, k32b, sc.dvals_alt, nullptr, 32, n, n, 4, 0, sc.hist, sc.offsets, sc.lookback,
-                         counters + C_CHUNK0, true, s);
+    depth_key32_kernel<<<kb, kSortThreads, 0, s>>>(dkeys, counters, n, k32b, sc.dvals_alt, sc.hist);
+    radix_sort<uint32_t>(k32b, sc.dvals_alt, k32, order, nullptr, kDepthBits + 1, n, n, kDepthPasses, 0, sc.hist,
+                         sc.offsets, sc.lookback, counters + C_CHUNK0, true, s);
     depth_fixup_kernel<<<(n + 255) / 256, 256, 0, s>>>(dkeys, counters, k32, order);
     // pairs land in the buffer that makes the sorted result end in (ptiles, pids)
     uint32_t *dt = (pp & 1) ? sc.ptiles_alt : ptiles;
