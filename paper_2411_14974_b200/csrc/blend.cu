@@ -181,9 +181,6 @@ __device__ __forceinline__ Eval eval_field(const LineSet<NL, MAXK> &L, float sig
 #ifndef CS_FWD_NC
 #define CS_FWD_NC 8
 #endif
-#ifndef CS_BWD_NC
-#define CS_BWD_NC 8
-#endif
 template <int NC> __host__ __device__ constexpr int pipe_threads() { return 32 * (NC + 1); }
 // Ring depth: the forward stops early (saturated pixels), so a deep ring
 // mostly prefetches records nobody evaluates; the backward walks the whole
@@ -496,8 +493,8 @@ struct BwdPixel {
 };
 
 // One candidate at one pixel of the reverse walk: recompute the field,
-// reconstruct T_prev = T / (1 - alpha), and write the pixel's 32 screen-space
-// gradient terms into v (left zero when it did not blend).  Returns whether
+// reconstruct T_prev = T / (1 - alpha), and add the pixel's 32 screen-space
+// gradient terms to v (unchanged when it did not blend).  Returns whether
 // it did.
 template <int NL, int MAXK, int VN>
 __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float qy, float cutoff, BwdPixel &P,
@@ -522,16 +519,16 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
   const float Tp = P.T * rom;
   const float w = Tp * e.alpha;
   const float c0 = h1.x, c1 = h1.y, c2 = h1.z;
-  v[A_DC] = P.g0 * w;
-  v[A_DC + 1] = P.g1 * w;
-  v[A_DC + 2] = P.g2 * w;
+  v[A_DC] += P.g0 * w;
+  v[A_DC + 1] += P.g1 * w;
+  v[A_DC + 2] += P.g2 * w;
   float dA = P.g0 * (Tp * c0 - P.S0 * rom) + P.g1 * (Tp * c1 - P.S1 * rom) + P.g2 * (Tp * c2 - P.S2 * rom);
   if (!(e.alpha_raw < (float)kAlphaMaxD)) dA = 0.f;
-  v[A_DOEFF] = dA * e.I;
+  v[A_DOEFF] += dA * e.I;
   const float dI = dA * o;
   const float slope = e.I * e.J;
   const float dphi = -sig * slope * dI;          // d loss / d phi (natural units)
-  v[A_DSIG] = -(e.phi2 * kLn2) * slope * dI;
+  v[A_DSIG] += -(e.phi2 * kLn2) * slope * dI;
   const float dscale = dphi * (dls * kLn2);      // dphi * delta_s
   float wz = 0.f;
 #pragma unroll
@@ -540,12 +537,12 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
       const float wl = acc_ex2(z[l] - e.phi2);         // softmax_over_lines (field.py:62-67)
       wz = fmaf(wl, z[l], wz);
       const float dL = dscale * wl;
-      v[A_LINES + 3 * l] = dL * dx;
-      v[A_LINES + 3 * l + 1] = dL * dy;
-      v[A_LINES + 3 * l + 2] = dL;
+      v[A_LINES + 3 * l] += dL * dx;
+      v[A_LINES + 3 * l + 1] += dL * dy;
+      v[A_LINES + 3 * l + 2] += dL;
     }
   }
-  v[A_DDEL] = dphi * wz * inv_dls;               // dphi * sum_l w_l L_l
+  v[A_DDEL] += dphi * wz * inv_dls;               // dphi * sum_l w_l L_l
   P.S0 = fmaf(w, c0, P.S0);
   P.S1 = fmaf(w, c1, P.S1);
   P.S2 = fmaf(w, c2, P.S2);
@@ -558,52 +555,62 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
 // stage by ballot, reconstructs T_prev = T / (1 - alpha) per pixel and
 // reduces the 32 screen-space gradient values of each candidate across the
 // warp (transpose-reduce) into one vector of float atomics.
-template <int MAXK>
+// PPL pixels per lane: 8 / PPL consumer warps of 8 x (4 PPL) pixels (lane =
+// column + 8 * row of the top 8x4 block, pixel h another 4 h rows down).
+// The lane sums its pixels' gradient terms before the transpose-reduce, so
+// PPL = 2 halves the reductions per evaluated pixel (853 -> 775 us at 1M
+// @1080p; PPL = 4: 929 us, the coarser 8x16 culling loses).
 #ifndef CS_BWD_MINB
-#define CS_BWD_MINB (CS_BWD_NC == 8 ? 4 : 7)   // 8 warps: 4 blocks/SM with a small spill beat 3 without (926 vs 934 us)
+#define CS_BWD_MINB 6   // PPL 2: 5 -> 777 us, 6 -> 775, 7 -> 941 (spills)
 #endif
-__global__ void __launch_bounds__(pipe_threads<CS_BWD_NC>(), CS_BWD_MINB) backward_kernel(BlendArgs a) {
-  constexpr int NC = CS_BWD_NC;
-  const int half = NC == 8 ? 0 : (int)(blockIdx.x & 1);
-  const int unit = NC == 8 ? (int)blockIdx.x : (int)(blockIdx.x >> 1);
+#ifndef CS_BWD_PPL
+#define CS_BWD_PPL 2
+#endif
+template <int MAXK, int PPL>
+__global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward_kernel(BlendArgs a) {
+  constexpr int NC = 8 / PPL;   // warps of 8 x (4 PPL) pixels
   constexpr int AF = Acc<MAXK>::kFloats;
-  constexpr int NG = (AF + 31) / 32;  // 32-value groups
+  constexpr int NG = (AF + 31) / 32;
   constexpr int kStages = CS_BWD_STAGES;
   extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
   PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
   __shared__ int s_last[NC];
-  const int tile = a.tile_order ? (int)a.tile_order[unit] : unit;
+  const int tile = a.tile_order ? (int)a.tile_order[blockIdx.x] : (int)blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint2 range = a.ranges[tile];
-  // consumer pixel state
-  int lx = 0, ly = 0;
-  if (warp < NC) tile_pixel(threadIdx.x, lx, ly);
-  ly += half * 8;
-  const int px = tx * kTile + lx, py = ty * kTile + ly;
-  const bool inside = warp < NC && px < a.width && py < a.height;
-  BwdPixel P;
-  P.T = 1.f; P.g0 = P.g1 = P.g2 = P.S0 = P.S1 = P.S2 = 0.f;
-  P.last = -1;
-  if (inside) {
-    const size_t p = (size_t)py * a.width + px;
-    P.T = a.pixel_T[p];
-    P.last = a.pixel_last[p];
-    const uint32_t cm = a.pixel_clamp[p];
-    P.g0 = (cm & 1) ? a.d_image[3 * p] : 0.f;
-    P.g1 = (cm & 2) ? a.d_image[3 * p + 1] : 0.f;
-    P.g2 = (cm & 4) ? a.d_image[3 * p + 2] : 0.f;
-    P.S0 = P.T * a.bg[0];
-    P.S1 = P.T * a.bg[1];
-    P.S2 = P.T * a.bg[2];
+  const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + (warp >> 1) * 4 * PPL;
+  BwdPixel P[PPL];
+  float qx[PPL], qy[PPL];
+#pragma unroll
+  for (int h = 0; h < PPL; h++) {
+    const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3) + 4 * h;
+    qx[h] = px + 0.5f;
+    qy[h] = py + 0.5f;
+    P[h].T = 1.f; P[h].g0 = P[h].g1 = P[h].g2 = P[h].S0 = P[h].S1 = P[h].S2 = 0.f;
+    P[h].last = -1;
+    if (warp < NC && px < a.width && py < a.height) {
+      const size_t p = (size_t)py * a.width + px;
+      P[h].T = a.pixel_T[p];
+      P[h].last = a.pixel_last[p];
+      const uint32_t cm = a.pixel_clamp[p];
+      P[h].g0 = (cm & 1) ? a.d_image[3 * p] : 0.f;
+      P[h].g1 = (cm & 2) ? a.d_image[3 * p + 1] : 0.f;
+      P[h].g2 = (cm & 4) ? a.d_image[3 * p + 2] : 0.f;
+      P[h].S0 = P[h].T * a.bg[0];
+      P[h].S1 = P[h].T * a.bg[1];
+      P[h].S2 = P[h].T * a.bg[2];
+    }
   }
-  const int warp_last = __reduce_max_sync(0xffffffffu, P.last);
+  int lmax = P[0].last;
+#pragma unroll
+  for (int h = 1; h < PPL; h++) lmax = max(lmax, P[h].last);
+  const int warp_last = __reduce_max_sync(0xffffffffu, lmax);
   if (warp < NC && lane == 0) s_last[warp] = warp_last;
-  pipe_init<MAXK, kStages, NC>(sm);  // (its __syncthreads also publishes s_last)
+  pipe_init<MAXK, kStages, NC>(sm);
   int block_last = s_last[0];
 #pragma unroll
   for (int w = 1; w < NC; w++) block_last = max(block_last, s_last[w]);
-  // batches back to front over [range.x, block_last]
   const int64_t end = (int64_t)block_last + 1;
   const int nbatch = end > (int64_t)range.x ? (int)((end - range.x + kStageCands - 1) / kStageCands) : 0;
   auto batch = [&](int b, uint32_t &first, uint32_t &count) {
@@ -616,21 +623,25 @@ __global__ void __launch_bounds__(pipe_threads<CS_BWD_NC>(), CS_BWD_MINB) backwa
   if (warp == NC) {
     pipe_produce<MAXK, kStages, NC>(sm, a.records, a.pair_ids, nbatch, batch, false, nullptr);
   } else {
-    const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2) + half * 8;
-    const float qx = px + 0.5f, qy = py + 0.5f;
     for (int b = 0; b < nbatch; b++) {
       const int s = b % kStages;
       mbar_wait(&sm.full[s], (b / kStages) & 1);
       uint32_t first, count;
       batch(b, first, count);
       if ((int)first <= warp_last) {
-        // lane j: pixels of this warp's block inside candidate j's bbox that
-        // blended it or something behind it (list position <= their last)
         const uint32_t pos = first + lane;
-        uint32_t pm = 0u;
-        if (lane < (int)count && (int)pos <= warp_last)
-          pm = block_mask(rec_bbox(sm.rec[s][lane]), rx0, ry0);
-        uint32_t m = __ballot_sync(0xffffffffu, pm != 0u);
+        uint32_t pm[PPL], any = 0u;
+#pragma unroll
+        for (int h = 0; h < PPL; h++) pm[h] = 0u;
+        if (lane < (int)count && (int)pos <= warp_last) {
+          const int4 bb = rec_bbox(sm.rec[s][lane]);
+#pragma unroll
+          for (int h = 0; h < PPL; h++) {
+            pm[h] = block_mask(bb, rx0, ry0 + 4 * h);
+            any |= pm[h];
+          }
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, any != 0u);
         while (m) {
           const int j = 31 - __clz(m);   // back to front
           m &= ~(1u << j);
@@ -638,22 +649,33 @@ __global__ void __launch_bounds__(pipe_threads<CS_BWD_NC>(), CS_BWD_MINB) backwa
           float v[NG * 32];
 #pragma unroll
           for (int f = 0; f < NG * 32; f++) v[f] = 0.f;
-          bool contrib = false;
-          const uint32_t pj = __shfl_sync(0xffffffffu, pm, j);
-          if ((int)first + j <= P.last && ((pj >> lane) & 1u)) {
-            n_eval++;
-            if (MAXK == 8) {
-              switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
-                case 5: contrib = bwd_candidate<5, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines); break;
-                case 6: contrib = bwd_candidate<6, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines); break;
-                case 4: contrib = bwd_candidate<4, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines); break;
-                default: contrib = bwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines); break;
-              }
-            } else {
-              contrib = bwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, P, v, n_lines);
-            }
+          const int cpos = (int)first + j;
+          bool act[PPL], any_act = false;
+#pragma unroll
+          for (int h = 0; h < PPL; h++) {
+            const uint32_t pj = __shfl_sync(0xffffffffu, pm[h], j);
+            act[h] = cpos <= P[h].last && ((pj >> lane) & 1u);
+            n_eval += (unsigned)act[h];
+            any_act |= act[h];
           }
-          n_warp_evals += __any_sync(0xffffffffu, (int)first + j <= P.last && ((pj >> lane) & 1u)) ? 1u : 0u;
+          bool contrib = false;
+#define CS_BWD2_PX(NLV, H)                                                                       \
+  if (H < PPL && act[H % PPL])                                                                     \
+    contrib |= bwd_candidate<NLV, MAXK>(rec, qx[H % PPL], qy[H % PPL], a.cutoff, P[H % PPL], v, n_lines);
+#define CS_BWD2_CASE(NLV) CS_BWD2_PX(NLV, 0) CS_BWD2_PX(NLV, 1) CS_BWD2_PX(NLV, 2) CS_BWD2_PX(NLV, 3)
+          if (MAXK == 8) {
+            switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
+              case 5: { CS_BWD2_CASE(5) } break;
+              case 6: { CS_BWD2_CASE(6) } break;
+              case 4: { CS_BWD2_CASE(4) } break;
+              default: { CS_BWD2_CASE(0) } break;
+            }
+          } else {
+            CS_BWD2_CASE(0)
+          }
+#undef CS_BWD2_CASE
+#undef CS_BWD2_PX
+          n_warp_evals += __any_sync(0xffffffffu, any_act) ? 1u : 0u;
           if (__any_sync(0xffffffffu, contrib)) {
             float *dst = a.accum + (size_t)sm.id[s][j] * AF;
 #pragma unroll
@@ -727,11 +749,11 @@ int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs
   if (p.n > 0) cudaMemsetAsync(a.accum, 0, (size_t)p.n * L.acc_floats * sizeof(float), s);
   const int tiles = L.tiles_x * L.tiles_y;
   if (L.max_k == 8) {
-    cudaFuncSetAttribute(backward_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_BWD_STAGES>));
-    backward_kernel<8><<<tiles * (8 / CS_BWD_NC), pipe_threads<CS_BWD_NC>(), sizeof(PipeSmem<8, CS_BWD_STAGES>), s>>>(a);
+    cudaFuncSetAttribute(backward_kernel<8, CS_BWD_PPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_BWD_STAGES>));
+    backward_kernel<8, CS_BWD_PPL><<<tiles, pipe_threads<8 / CS_BWD_PPL>(), sizeof(PipeSmem<8, CS_BWD_STAGES>), s>>>(a);
   } else {
-    cudaFuncSetAttribute(backward_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_BWD_STAGES>));
-    backward_kernel<16><<<tiles * (8 / CS_BWD_NC), pipe_threads<CS_BWD_NC>(), sizeof(PipeSmem<16, CS_BWD_STAGES>), s>>>(a);
+    cudaFuncSetAttribute(backward_kernel<16, CS_BWD_PPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_BWD_STAGES>));
+    backward_kernel<16, CS_BWD_PPL><<<tiles, pipe_threads<8 / CS_BWD_PPL>(), sizeof(PipeSmem<16, CS_BWD_STAGES>), s>>>(a);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
