@@ -22,6 +22,8 @@
 // The hull line count of a candidate is uniform across the warp (every lane
 // evaluates the same candidate), so the evaluation is dispatched to a
 // specialisation per count (no per-line predicates).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cs {
@@ -742,11 +744,25 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
 
+// Zeroing the screen-space accumulators (128 MB at 1M convexes):
+// 16-byte streaming stores over a grid of 8 blocks per SM.
+__global__ void __launch_bounds__(512) zero_kernel(float4 *p, size_t n4) {
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (size_t i = (size_t)blockIdx.x * 512 + threadIdx.x; i < n4; i += (size_t)gridDim.x * 512) __stcs(p + i, z);
+}
+
 int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                           const cs_layout &L, char *ws, const float *d_image, cudaStream_t s) {
   BlendArgs a = make_args(cam, set, L, ws);
   a.d_image = d_image;
-  if (p.n > 0) cudaMemsetAsync(a.accum, 0, (size_t)p.n * L.acc_floats * sizeof(float), s);
+  if (p.n > 0) {
+#ifdef CS_MEMSET_ACCUM
+    cudaMemsetAsync(a.accum, 0, (size_t)p.n * L.acc_floats * sizeof(float), s);
+#else
+    const size_t n4 = (size_t)p.n * L.acc_floats / 4;   // acc_floats is a multiple of 4
+    zero_kernel<<<(int)std::min<size_t>((n4 + 511) / 512, 148 * 8), 512, 0, s>>>(reinterpret_cast<float4 *>(a.accum), n4);
+#endif
+  }
   const int tiles = L.tiles_x * L.tiles_y;
   if (L.max_k == 8) {
     cudaFuncSetAttribute(backward_kernel<8, CS_BWD_PPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_BWD_STAGES>));
