@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 3
+#define CS_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define CS_API __attribute__((visibility("default")))
@@ -199,6 +199,18 @@ CS_API int cs_backward_signal(const cs_camera *cam, const cs_settings *set, cons
                               void *workspace, size_t workspace_bytes, int64_t pair_capacity,
                               const float *d_image, const cs_grads *grads, const cs_view_signal *signal,
                               void *stream);
+
+/* General backward: stages first..last (0 = backward blend, 1 = chain), an
+ * optional per-view signal (NULL = none) and flags.  CS_GRADS_OVERWRITE:
+ * the chain WRITES every row of the gradient buffers (rows of convexes this
+ * view did not prepare get zeros) instead of accumulating into them -- the
+ * result of GradientBuffer() + one view, without a zeroing pass or the read
+ * half of the accumulation.  cs_backward == flags 0, stages 0..1. */
+#define CS_GRADS_OVERWRITE 1u
+CS_API int cs_backward_ex(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                          void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                          const float *d_image, const cs_grads *grads, const cs_view_signal *signal,
+                          uint32_t flags, int32_t first_stage, int32_t last_stage, void *stream);
 
 /* Scratch bytes cs_image_loss needs for an H x W image. Host-only. */
 CS_API int cs_image_loss_workspace(int32_t height, int32_t width, size_t *bytes);

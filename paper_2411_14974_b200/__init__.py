@@ -20,6 +20,7 @@ _LAZY = {
     "prepare_view": "rasterizer", "bin_tiles": "rasterizer", "rasterize": "rasterizer",
     "Rasterizer": "rasterizer", "Workspace": "rasterizer", "inspect_frame": "rasterizer",
     "zero_grads": "rasterizer",
+    "empty_grads": "rasterizer",
 }
 
 

@@ -13,9 +13,10 @@ LIB_PATH = os.path.join(_HERE, "libconvexsplat_sm100.so")
 
 EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forward", "cs_backward",
            "cs_forward_stages", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
-           "cs_backward_signal", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step",
+           "cs_backward_signal", "cs_backward_ex", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step",
            "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags", "cs_density_scatter")
-ABI_VERSION = 3
+ABI_VERSION = 4
+GRADS_OVERWRITE = 1   # CS_GRADS_OVERWRITE
 
 _vp = ctypes.c_void_p
 
@@ -112,6 +113,8 @@ def load(path: str = None):
     L.cs_read_counters.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), _vp]
     L.cs_graham_scan_batch.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]
     L.cs_backward_signal.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.POINTER(CsViewSignal), _vp]
+    L.cs_backward_ex.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.POINTER(CsViewSignal), ctypes.c_uint32,
+                                                               ctypes.c_int32, ctypes.c_int32, _vp]
     L.cs_image_loss_workspace.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
     L.cs_image_loss.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_double,
                                 ctypes.c_double, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
@@ -126,7 +129,8 @@ def load(path: str = None):
     L.cs_density_scatter.argtypes = [ctypes.POINTER(CsParams), ctypes.POINTER(CsDensityConfig), _vp, _vp, _vp,
                                      _vp, _vp, ctypes.POINTER(CsSceneOut), _vp, _vp]
     for fn in ("cs_workspace_layout", "cs_forward", "cs_backward", "cs_forward_stages", "cs_backward_stages",
-               "cs_read_counters", "cs_graham_scan_batch", "cs_backward_signal", "cs_image_loss_workspace",
+               "cs_read_counters", "cs_graham_scan_batch", "cs_backward_signal", "cs_backward_ex",
+               "cs_image_loss_workspace",
                "cs_image_loss", "cs_adam_step", "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags",
                "cs_density_scatter"):
         getattr(L, fn).restype = ctypes.c_int

@@ -112,8 +112,11 @@ int cs_forward(const cs_camera *cam, const cs_settings *set, const cs_params *pa
 
 static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
                          size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
-                         const cs_view_signal *sig, int32_t first_stage, int32_t last_stage, void *stream) {
+                         const cs_view_signal *sig, uint32_t flags, int32_t first_stage, int32_t last_stage,
+                         void *stream) {
   if (!params || !grads || !workspace || !d_image) return CS_ERR_ARG;
+  if (flags & ~(uint32_t)CS_GRADS_OVERWRITE) return CS_ERR_ARG;
+  if (sig && (!sig->sigma_signal || !sig->sigma_views || !sig->visible)) return CS_ERR_ARG;
   if (first_stage < 0 || last_stage > 1 || first_stage > last_stage) return CS_ERR_ARG;
   cs_layout L;
   int rc = cs_workspace_layout(cam, set, params->n, params->k, pair_capacity, &L);
@@ -126,30 +129,38 @@ static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_
   char *ws = static_cast<char *>(workspace);
   if (first_stage == 0)
     if ((rc = cs::launch_backward_blend(*cam, *set, *params, L, ws, d_image, s))) return rc;
-  if (last_stage == 1) return cs::launch_chain(*cam, *set, *params, L, ws, *grads, sig, s);
+  if (last_stage == 1)
+    return cs::launch_chain(*cam, *set, *params, L, ws, *grads, sig, (flags & CS_GRADS_OVERWRITE) != 0, s);
   return CS_OK;
 }
 
 int cs_backward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
                        size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
                        int32_t first_stage, int32_t last_stage, void *stream) {
-  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, nullptr,
+  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, nullptr, 0,
                        first_stage, last_stage, stream);
 }
 
 int cs_backward(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
                 size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
                 void *stream) {
-  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, nullptr, 0, 1,
+  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, nullptr, 0, 0, 1,
                        stream);
 }
 
 int cs_backward_signal(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
                        size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
                        const cs_view_signal *signal, void *stream) {
-  if (signal && (!signal->sigma_signal || !signal->sigma_views || !signal->visible)) return CS_ERR_ARG;
-  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, signal, 0, 1,
+  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, signal, 0, 0, 1,
                        stream);
+}
+
+int cs_backward_ex(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                   size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
+                   const cs_view_signal *signal, uint32_t flags, int32_t first_stage, int32_t last_stage,
+                   void *stream) {
+  return backward_impl(cam, set, params, workspace, workspace_bytes, pair_capacity, d_image, grads, signal, flags,
+                       first_stage, last_stage, stream);
 }
 
 int cs_image_loss_workspace(int32_t height, int32_t width, size_t *bytes) {

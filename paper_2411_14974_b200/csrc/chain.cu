@@ -10,7 +10,8 @@
 //   SH VJP + view-direction path (backward.py:277-282, harmonics.py:112-128)
 // Discrete state (hull cycle, anchor) is read from the forward workspace;
 // projection, depth, scale and view direction are recomputed from the
-// parameters.  Gradients are accumulated (+=) into the caller's buffers.
+// parameters.  Gradients are accumulated (+=) into the caller's buffers, or
+// written (CS_GRADS_OVERWRITE).
 #include "common.cuh"
 
 namespace cs {
@@ -49,6 +50,14 @@ __device__ __forceinline__ void red_add4(float4 *p, float4 v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
+// Gradient output: += (RED) or, with CS_GRADS_OVERWRITE, a plain store (the
+// caller's buffers are written, not read: no zeroing pass, no read half).
+template <bool OW> __device__ __forceinline__ void grad_out(float *p, float v) {
+  if (OW) *p = v; else red_add(p, v);
+}
+template <bool OW> __device__ __forceinline__ void grad_out4(float4 *p, float4 v) {
+  if (OW) *p = v; else red_add4(p, v);
+}
 
 // d(Y_b)/d(dir) . v_b added into (gx, gy, gz): eval_sh_basis_grad
 // (harmonics.py:62-98) row b, written out (b is a compile-time constant).
@@ -85,6 +94,7 @@ __device__ __forceinline__ void add_basis_grad(int b, float v, float x, float y,
 // direction gradient dY/ddir^T (sh . d_eff).  Streams the 16x3 rows as
 // float4 (two reads of sh, one vector reduction into d_sh) so no per-thread
 // 48-float arrays stay live.
+template <bool OW>
 __device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const float *sh, const float *d_color,
                                        float *d_sh, float *ddir) {
   float Y[kShCoeffs];
@@ -140,7 +150,9 @@ __device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const
           }
         }
       }
-      red_add4(dsh4 + q, make_float4(de[0], de[1], de[2], de[3]));
+      grad_out4<OW>(dsh4 + q, make_float4(de[0], de[1], de[2], de[3]));
+    } else if (OW) {
+      dsh4[q] = make_float4(0.f, 0.f, 0.f, 0.f);   // coefficients above sh_degree
     }
   }
   ddir[0] = gx; ddir[1] = gy; ddir[2] = gz;
@@ -157,7 +169,7 @@ __device__ __forceinline__ G g_rcp(G x) { return __frcp_rn(x); }
 __device__ __forceinline__ G g_rsqrt(G x) { return rsqrtf(x); }
 #endif
 
-template <int MAXK>
+template <int MAXK, bool OW>
 __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainArgs a) {
   constexpr int kChainThreads = chain_threads<MAXK>();
   // per-thread slots for the dynamically indexed per-point arrays
@@ -165,9 +177,31 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
   __shared__ G s_dx[MAXK][kChainThreads], s_dy[MAXK][kChainThreads];
   const int t = threadIdx.x;
   const int64_t i = (int64_t)blockIdx.x * kChainThreads + t;
-  if (i >= a.n || a.touched[i] == 0) return;  // not prepared for this view
   constexpr int RF = Rec<MAXK>::kFloats;
   constexpr int AF = Acc<MAXK>::kFloats;
+#ifndef CS_CHAIN_NO_PREFETCH
+  if (t == 0 && (int64_t)(blockIdx.x + 1) * kChainThreads <= a.n) {
+    // the block's rows of SH / points (read after the hull work) start moving
+    // into L2 as contiguous bulk reads while the threads load their
+    // accumulators
+    const int64_t base = (int64_t)blockIdx.x * kChainThreads;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.points + base * a.k * 3),
+                 "r"((uint32_t)(kChainThreads * a.k * 3 * 4)) : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.sh + base * kShCoeffs * 3),
+                 "r"((uint32_t)(kChainThreads * kShCoeffs * 3 * 4)) : "memory");
+  }
+#endif
+  if (i >= a.n) return;
+  if (a.touched[i] == 0) {   // not prepared for this view: zero gradient
+    if (OW) {
+      for (int q = 0; q < 3 * a.k; q++) a.g.d_points[i * 3 * a.k + q] = 0.f;
+      float4 *dsh4 = reinterpret_cast<float4 *>(a.g.d_sh + i * kShCoeffs * 3);
+#pragma unroll
+      for (int q = 0; q < kShCoeffs * 3 / 4; q++) dsh4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a.g.d_raw_delta[i] = 0.f; a.g.d_raw_sigma[i] = 0.f; a.g.d_raw_opacity[i] = 0.f; a.g.d_raw_mask[i] = 0.f;
+    }
+    return;
+  }
   const int k = a.k;
   const G inv_k = G(1) / (G)k;
   // the convex's screen-space accumulators, loaded as float4 up front
@@ -278,7 +312,7 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
   float dir[3] = {0.f, 0.f, 1.f};
   if (d2 > 0.f) { dir[0] = vx * idist; dir[1] = vy * idist; dir[2] = vz * idist; }
   float ddirf[3];
-  sh_vjp(dir[0], dir[1], dir[2], a.sh_degree, a.sh + i * kShCoeffs * 3, dcol, a.g.d_sh + i * kShCoeffs * 3, ddirf);
+  sh_vjp<OW>(dir[0], dir[1], dir[2], a.sh_degree, a.sh + i * kShCoeffs * 3, dcol, a.g.d_sh + i * kShCoeffs * 3, ddirf);
   const float dot = dir[0] * ddirf[0] + dir[1] * ddirf[1] + dir[2] * ddirf[2];
   // projection Jacobian + depth + centre paths into d_points (backward.py:248-269, 281-282)
   G common[3];
@@ -299,12 +333,12 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
         dz = -((s_x[j][t] - (G)ox) * gx + (s_y[j][t] - (G)oy) * gy) * izc[j];
       }
 #pragma unroll
-      for (int c = 0; c < 3; c++) red_add(dp + 3 * j + c, (float)fma(d0, R[c], fma(d1, R[3 + c], fma(dz, R[6 + c], common[c]))));
+      for (int c = 0; c < 3; c++) grad_out<OW>(dp + 3 * j + c, (float)fma(d0, R[c], fma(d1, R[3 + c], fma(dz, R[6 + c], common[c]))));
     }
   }
-  red_add(a.g.d_raw_delta + i, (float)(ddel * s * delta));
+  grad_out<OW>(a.g.d_raw_delta + i, (float)(ddel * s * delta));
   const float d_rs = (float)(dsig * s * sigma);
-  red_add(a.g.d_raw_sigma + i, d_rs);
+  grad_out<OW>(a.g.d_raw_sigma + i, d_rs);
   if (a.sig.sigma_signal) {   // trainer.py:192-193, this view's contribution only
     const float vis = a.sig.visible[i] ? 1.f : 0.f;
     red_add(a.sig.sigma_signal + i, fabsf(d_rs) * vis);
@@ -313,12 +347,13 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
   const float o = 1.f / (1.f + __expf(-a.raw_opacity[i]));
   const float m = 1.f / (1.f + __expf(-a.raw_mask[i]));
   const float doe = (float)acc[A_DOEFF];
-  red_add(a.g.d_raw_opacity + i, doe * o * (1.f - o));
-  red_add(a.g.d_raw_mask + i, doe * o * m * (1.f - m));
+  grad_out<OW>(a.g.d_raw_opacity + i, doe * o * (1.f - o));
+  grad_out<OW>(a.g.d_raw_mask + i, doe * o * m * (1.f - m));
 }
 
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                 const cs_layout &L, char *ws, const cs_grads &g, const cs_view_signal *sig, cudaStream_t s) {
+                 const cs_layout &L, char *ws, const cs_grads &g, const cs_view_signal *sig, bool overwrite,
+                 cudaStream_t s) {
   if (p.n == 0) return CS_OK;
   ChainArgs a;
   a.cam = cam;
@@ -339,10 +374,13 @@ int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &
   a.touched = reinterpret_cast<const uint32_t *>(ws + L.tiles_touched);
   a.g = g;
   a.sig = sig ? *sig : cs_view_signal{nullptr, nullptr, nullptr};
-  if (L.max_k == 8)
-    chain_kernel<8><<<(int)((p.n + 127) / 128), chain_threads<8>(), 0, s>>>(a);
-  else
-    chain_kernel<16><<<(int)((p.n + 63) / 64), chain_threads<16>(), 0, s>>>(a);
+  if (L.max_k == 8) {
+    if (overwrite) chain_kernel<8, true><<<(int)((p.n + 127) / 128), chain_threads<8>(), 0, s>>>(a);
+    else chain_kernel<8, false><<<(int)((p.n + 127) / 128), chain_threads<8>(), 0, s>>>(a);
+  } else {
+    if (overwrite) chain_kernel<16, true><<<(int)((p.n + 63) / 64), chain_threads<16>(), 0, s>>>(a);
+    else chain_kernel<16, false><<<(int)((p.n + 63) / 64), chain_threads<16>(), 0, s>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
 

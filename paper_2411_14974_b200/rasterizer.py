@@ -201,27 +201,27 @@ class Rasterizer:
                                                  stream), "cs_forward_stages")
 
     def launch_backward(self, fr: Frame, d_image: torch.Tensor, grads: dict, first_stage: int = 0,
-                        last_stage: int = 1, signal=None):
-        """Backward stages (0 blend, 1 chain) into ``grads`` (+=), no sync.
-        ``signal`` = (sigma_signal, sigma_views, visible) tensors: also
-        accumulate the view's densification signal (trainer.py:192-193)."""
+                        last_stage: int = 1, signal=None, overwrite: bool = False):
+        """Backward stages (0 blend, 1 chain) into ``grads`` (+=, or written
+        when ``overwrite``: every row, zeros for convexes the view did not
+        prepare), no sync.  ``signal`` = (sigma_signal, sigma_views, visible)
+        tensors: also accumulate the view's densification signal
+        (trainer.py:192-193)."""
         g = _lib.CsGrads(grads["points"].data_ptr(), grads["raw_delta"].data_ptr(), grads["raw_sigma"].data_ptr(),
                          grads["raw_opacity"].data_ptr(), grads["raw_mask"].data_ptr(), grads["sh"].data_ptr())
         ws = fr.workspace
         stream = torch.cuda.current_stream(self.device).cuda_stream
+        sig = None
         if signal is not None:
             if (first_stage, last_stage) != (0, 1):
                 raise ValueError("the sigma signal needs the full backward")
             sig = _lib.CsViewSignal(signal[0].data_ptr(), signal[1].data_ptr(), signal[2].data_ptr())
-            _lib.check(_lib.load().cs_backward_signal(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
-                                                      ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
-                                                      d_image.data_ptr(), ctypes.byref(g), ctypes.byref(sig),
-                                                      stream), "cs_backward_signal")
-            return
-        _lib.check(_lib.load().cs_backward_stages(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
-                                                  ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
-                                                  d_image.data_ptr(), ctypes.byref(g), first_stage, last_stage,
-                                                  stream), "cs_backward_stages")
+        _lib.check(_lib.load().cs_backward_ex(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
+                                              ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
+                                              d_image.data_ptr(), ctypes.byref(g),
+                                              ctypes.byref(sig) if sig is not None else None,
+                                              _lib.GRADS_OVERWRITE if overwrite else 0, first_stage, last_stage,
+                                              stream), "cs_backward_ex")
 
     @staticmethod
     def read_stats(fr: Frame) -> dict:
@@ -232,24 +232,25 @@ class Rasterizer:
         out.update(n_visible=int(c[0]), n_pairs=int(c[1]), overflow=int(c[2]))
         return out
 
-    def backward(self, frame: Frame, d_image: torch.Tensor, grads: dict) -> dict:
-        """Accumulate (+=) gradients of sum(d_image * image) into ``grads``."""
+    def backward(self, frame: Frame, d_image: torch.Tensor, grads: dict, overwrite: bool = False) -> dict:
+        """Accumulate (+=) gradients of sum(d_image * image) into ``grads``,
+        or write them (``overwrite``: ``grads`` may be uninitialised)."""
         d_image = d_image.to(device=self.device, dtype=torch.float32).contiguous()
         H, W = frame.cam_c.height, frame.cam_c.width
         if tuple(d_image.shape) != (H, W, 3):
             raise ValueError(f"d_image must be ({H}, {W}, 3), got {tuple(d_image.shape)}")
-        g = _lib.CsGrads(grads["points"].data_ptr(), grads["raw_delta"].data_ptr(), grads["raw_sigma"].data_ptr(),
-                         grads["raw_opacity"].data_ptr(), grads["raw_mask"].data_ptr(), grads["sh"].data_ptr())
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        ws = frame.workspace
-        _lib.check(_lib.load().cs_backward(ctypes.byref(frame.cam_c), ctypes.byref(frame.set_c),
-                                           ctypes.byref(frame.params_c), ws.ptr, ws.nbytes, frame.capacity,
-                                           d_image.data_ptr(), ctypes.byref(g), stream), "cs_backward")
+        self.launch_backward(frame, d_image, grads, overwrite=overwrite)
         return grads
 
 
 def zero_grads(st: SceneTensors) -> dict:
     return {name: torch.zeros_like(getattr(st, name)) for name in
+            ("points", "raw_delta", "raw_sigma", "raw_opacity", "raw_mask", "sh")}
+
+
+def empty_grads(st: SceneTensors) -> dict:
+    """Uninitialised gradient buffers for an overwriting backward."""
+    return {name: torch.empty_like(getattr(st, name)) for name in
             ("points", "raw_delta", "raw_sigma", "raw_opacity", "raw_mask", "sh")}
 
 
@@ -282,9 +283,10 @@ class _RasterizeFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, d_image, *_unused):
         fr = ctx.frame
-        grads = zero_grads(fr.scene)
         if d_image is not None:
-            ctx.rasterizer.backward(fr, d_image, grads)
+            grads = ctx.rasterizer.backward(fr, d_image, empty_grads(fr.scene), overwrite=True)
+        else:
+            grads = zero_grads(fr.scene)
         ctx.frame = None
         return (None, None, None, None, None, grads["points"], grads["raw_delta"], grads["raw_sigma"],
                 grads["raw_opacity"], grads["raw_mask"], grads["sh"])
@@ -332,7 +334,7 @@ def backward(scene, cam: Camera, d_image, mode: ScalingMode = ScalingMode.DEPTH,
     r = default_rasterizer()
     st = as_scene_tensors(scene, r.device)
     fr = r.forward(st, cam, mode, settings)
-    grads = r.backward(fr, torch.as_tensor(np.asarray(d_image), dtype=torch.float32), zero_grads(st))
+    grads = r.backward(fr, torch.as_tensor(np.asarray(d_image), dtype=torch.float32), empty_grads(st), overwrite=True)
     f64 = {k: _np(v).astype(np.float64) for k, v in grads.items()}
     return GradientBuffer(d_points=f64["points"], d_raw_delta=f64["raw_delta"], d_raw_sigma=f64["raw_sigma"],
                           d_raw_opacity=f64["raw_opacity"], d_sh=f64["sh"], d_raw_mask=f64["raw_mask"],
@@ -446,5 +448,5 @@ def bin_tiles(prepared: PreparedView, width: int, height: int, tile_size: int = 
 
 
 __all__ = ["Rasterizer", "Workspace", "Frame", "rasterize", "render", "render_reference", "backward",
-           "prepare_view", "bin_tiles", "inspect_frame", "zero_grads", "default_rasterizer",
+           "prepare_view", "bin_tiles", "inspect_frame", "zero_grads", "empty_grads", "default_rasterizer",
            "camera_struct", "settings_struct", "params_struct", "SH_COEFFS"]
