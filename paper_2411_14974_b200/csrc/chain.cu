@@ -46,17 +46,10 @@ template <int MAXK> __host__ __device__ constexpr int chain_threads() { return M
 __device__ __forceinline__ void red_add(float *p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
-__device__ __forceinline__ void red_add4(float4 *p, float4 v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
 // Gradient output: += (RED) or, with CS_GRADS_OVERWRITE, a plain store (the
 // caller's buffers are written, not read: no zeroing pass, no read half).
 template <bool OW> __device__ __forceinline__ void grad_out(float *p, float v) {
   if (OW) *p = v; else red_add(p, v);
-}
-template <bool OW> __device__ __forceinline__ void grad_out4(float4 *p, float4 v) {
-  if (OW) *p = v; else red_add4(p, v);
 }
 
 // d(Y_b)/d(dir) . v_b added into (gx, gy, gz): eval_sh_basis_grad
@@ -90,13 +83,13 @@ __device__ __forceinline__ void add_basis_grad(int b, float v, float x, float y,
   }
 }
 
-// SH colour VJP (harmonics.py:112-128): d_sh += Y (x) d_eff and the
-// direction gradient dY/ddir^T (sh . d_eff).  Streams the 16x3 rows as
-// float4 (two reads of sh, one vector reduction into d_sh) so no per-thread
-// 48-float arrays stay live.
-template <bool OW>
-__device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const float *sh, const float *d_color,
-                                       float *d_sh, float *ddir) {
+// SH colour VJP (harmonics.py:112-128): d_sh = Y (x) d_eff and the
+// direction gradient dY/ddir^T (sh . d_eff), on the convex's SH row staged
+// in shared memory (`row`, 48 floats, loaded by a bulk copy at kernel
+// start): d_sh is written back into the row in place and leaves by one bulk
+// store (overwrite) or bulk float reduction (+=).
+__device__ __forceinline__ void sh_vjp_row(float x, float y, float z, int deg, float *row, const float *d_color,
+                                           float *ddir) {
   float Y[kShCoeffs];
   Y[0] = kC0;
   const float xx = x * x, yy = y * y, zz = z * z;
@@ -113,13 +106,12 @@ __device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const
     Y[14] = kC35 * z * (xx - yy); Y[15] = kC36 * x * (xx - 3.0f * yy);
   }
   const int nb = (deg + 1) * (deg + 1);
-  const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
-  float4 *dsh4 = reinterpret_cast<float4 *>(d_sh);
+  float4 *row4 = reinterpret_cast<float4 *>(row);
   float raw[3] = {0.5f, 0.5f, 0.5f};
 #pragma unroll
   for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
     if (4 * q < 3 * nb) {
-      const float4 v = __ldg(sh4 + q);
+      const float4 v = row4[q];
       const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int r = 0; r < 4; r++) {
@@ -134,26 +126,24 @@ __device__ __forceinline__ void sh_vjp(float x, float y, float z, int deg, const
   float gx = 0.0f, gy = 0.0f, gz = 0.0f, vb = 0.0f;
 #pragma unroll
   for (int q = 0; q < kShCoeffs * 3 / 4; q++) {
+    float de[4] = {0.f, 0.f, 0.f, 0.f};
     if (4 * q < 3 * nb) {
-      const float4 v = __ldg(sh4 + q);
+      const float4 v = row4[q];
       const float e[4] = {v.x, v.y, v.z, v.w};
-      float de[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int r = 0; r < 4; r++) {
         const int f = 4 * q + r, b = f / 3, c = f % 3;
         if (b < nb) {
           de[r] = Y[b] * deff[c];
           vb = fmaf(e[r], deff[c], vb);
-          if (c == 2) {  // row b complete: its direction-gradient term
+          if (c == 2) {
             add_basis_grad(b, vb, x, y, z, gx, gy, gz);
             vb = 0.0f;
           }
         }
       }
-      grad_out4<OW>(dsh4 + q, make_float4(de[0], de[1], de[2], de[3]));
-    } else if (OW) {
-      dsh4[q] = make_float4(0.f, 0.f, 0.f, 0.f);   // coefficients above sh_degree
     }
+    row4[q] = make_float4(de[0], de[1], de[2], de[3]);   // zeros above sh_degree
   }
   ddir[0] = gx; ddir[1] = gy; ddir[2] = gz;
 }
@@ -175,29 +165,36 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
   // per-thread slots for the dynamically indexed per-point arrays
   __shared__ G s_x[MAXK][kChainThreads], s_y[MAXK][kChainThreads];
   __shared__ G s_dx[MAXK][kChainThreads], s_dy[MAXK][kChainThreads];
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t i = (int64_t)blockIdx.x * kChainThreads + t;
   constexpr int RF = Rec<MAXK>::kFloats;
   constexpr int AF = Acc<MAXK>::kFloats;
-#ifndef CS_CHAIN_NO_PREFETCH
-  if (t == 0 && (int64_t)(blockIdx.x + 1) * kChainThreads <= a.n) {
-    // the block's rows of SH / points (read after the hull work) start moving
-    // into L2 as contiguous bulk reads while the threads load their
-    // accumulators
-    const int64_t base = (int64_t)blockIdx.x * kChainThreads;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.points + base * a.k * 3),
-                 "r"((uint32_t)(kChainThreads * a.k * 3 * 4)) : "memory");
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.sh + base * kShCoeffs * 3),
-                 "r"((uint32_t)(kChainThreads * kShCoeffs * 3 * 4)) : "memory");
+  constexpr int kShRow = kShCoeffs * 3;
+  // SH rows: one 192-byte bulk copy per prepared convex, issued first so it
+  // lands while the geometry is recomputed; 208-byte slots keep the per-lane
+  // float4 reads free of bank conflicts
+  constexpr int kShStride = kShRow + 4;
+  __shared__ __align__(16) float s_sh[kChainThreads * kShStride];
+  __shared__ __align__(8) uint64_t s_shbar[kChainThreads / 32];
+  float *const shrow = s_sh + t * kShStride;
+  const bool active = i < a.n && a.touched[i] != 0;
+  {
+    const uint32_t act = __ballot_sync(0xffffffffu, active);
+    if (lane == 0) {
+      mbar_init(&s_shbar[w], 1);
+      fence_mbar_init();
+      if (act) mbar_expect_tx(&s_shbar[w], (uint32_t)__popc(act) * kShRow * 4);
+    }
+    __syncwarp();
+    if (active) tma_bulk_g2s(shrow, a.sh + i * kShRow, kShRow * 4, &s_shbar[w]);
   }
-#endif
   if (i >= a.n) return;
-  if (a.touched[i] == 0) {   // not prepared for this view: zero gradient
+  if (!active) {   // not prepared for this view: zero gradient
     if (OW) {
       for (int q = 0; q < 3 * a.k; q++) a.g.d_points[i * 3 * a.k + q] = 0.f;
-      float4 *dsh4 = reinterpret_cast<float4 *>(a.g.d_sh + i * kShCoeffs * 3);
+      float4 *dsh4 = reinterpret_cast<float4 *>(a.g.d_sh + i * kShRow);
 #pragma unroll
-      for (int q = 0; q < kShCoeffs * 3 / 4; q++) dsh4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < kShRow / 4; q++) dsh4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       a.g.d_raw_delta[i] = 0.f; a.g.d_raw_sigma[i] = 0.f; a.g.d_raw_opacity[i] = 0.f; a.g.d_raw_mask[i] = 0.f;
     }
     return;
@@ -312,7 +309,11 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
   float dir[3] = {0.f, 0.f, 1.f};
   if (d2 > 0.f) { dir[0] = vx * idist; dir[1] = vy * idist; dir[2] = vz * idist; }
   float ddirf[3];
-  sh_vjp<OW>(dir[0], dir[1], dir[2], a.sh_degree, a.sh + i * kShCoeffs * 3, dcol, a.g.d_sh + i * kShCoeffs * 3, ddirf);
+  mbar_wait(&s_shbar[w], 0);
+  sh_vjp_row(dir[0], dir[1], dir[2], a.sh_degree, shrow, dcol, ddirf);
+  fence_proxy_async_smem();
+  if (OW) tma_bulk_s2g(a.g.d_sh + i * kShRow, shrow, kShRow * 4);
+  else tma_bulk_s2g_add(a.g.d_sh + i * kShRow, shrow, kShRow * 4);
   const float dot = dir[0] * ddirf[0] + dir[1] * ddirf[1] + dir[2] * ddirf[2];
   // projection Jacobian + depth + centre paths into d_points (backward.py:248-269, 281-282)
   G common[3];
@@ -349,6 +350,7 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
   const float doe = (float)acc[A_DOEFF];
   grad_out<OW>(a.g.d_raw_opacity + i, doe * o * (1.f - o));
   grad_out<OW>(a.g.d_raw_mask + i, doe * o * m * (1.f - m));
+  tma_bulk_commit_and_wait_read();   // the d_sh row has left shared memory
 }
 
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
