@@ -160,7 +160,7 @@ __device__ __forceinline__ G g_rsqrt(G x) { return rsqrtf(x); }
 #endif
 
 template <int MAXK, bool OW>
-__global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainArgs a) {   // 5: the SH staging limits it anyway
   constexpr int kChainThreads = chain_threads<MAXK>();
   // per-thread slots for the dynamically indexed per-point arrays
   __shared__ G s_x[MAXK][kChainThreads], s_y[MAXK][kChainThreads];
@@ -211,7 +211,26 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
       acc[4 * q] = v.x; acc[4 * q + 1] = v.y; acc[4 * q + 2] = v.z; acc[4 * q + 3] = v.w;
     }
   }
-  const float2 anchor = *reinterpret_cast<const float2 *>(a.records + i * RF);
+  // every other per-convex input is loaded up front too (one exposed
+  // latency instead of a chain of them)
+  float pts[MAXK * 3];
+  {
+    const float *pp = a.points + i * k * 3;
+#pragma unroll
+    for (int q = 0; q < MAXK * 3; q++) pts[q] = q < 3 * k ? __ldg(pp + q) : 0.f;
+  }
+  const float raw_delta = __ldg(a.raw_delta + i), raw_sigma = __ldg(a.raw_sigma + i);
+  const float raw_opacity = __ldg(a.raw_opacity + i), raw_mask = __ldg(a.raw_mask + i);
+  uint8_t hb[MAXK];
+  if (MAXK == 8) {
+    const uint2 hw = __ldg(reinterpret_cast<const uint2 *>(a.hull + i * MAXK));
+#pragma unroll
+    for (int j = 0; j < 4; j++) { hb[j] = (hw.x >> (8 * j)) & 0xff; hb[j + 4] = (hw.y >> (8 * j)) & 0xff; }
+  } else {
+#pragma unroll
+    for (int j = 0; j < MAXK; j++) hb[j] = a.hull[i * MAXK + j];
+  }
+  const float2 anchor = __ldg(reinterpret_cast<const float2 *>(a.records + i * RF));
   G R[9];
 #pragma unroll
   for (int q = 0; q < 9; q++) R[q] = (G)a.cam.R[q];
@@ -227,8 +246,7 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
 #pragma unroll
   for (int j = 0; j < MAXK; j++) {
     if (j < k) {
-      const float *pp = a.points + (i * k + j) * 3;
-      const float q0 = pp[0], q1 = pp[1], q2 = pp[2];
+      const float q0 = pts[3 * j], q1 = pts[3 * j + 1], q2 = pts[3 * j + 2];
       cx += q0; cy += q1; cz += q2;
       const double p0 = q0, p1 = q1, p2 = q2;
       const double xc = fma(p2, Rd[2], fma(p1, Rd[1], p0 * Rd[0])) + a.cam.t[0];
@@ -248,15 +266,6 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
       s_dx[j][t] = 0;
       s_dy[j][t] = 0;
     }
-  }
-  uint8_t hb[MAXK];
-  if (MAXK == 8) {
-    const uint2 hw = *reinterpret_cast<const uint2 *>(a.hull + i * MAXK);
-#pragma unroll
-    for (int j = 0; j < 4; j++) { hb[j] = (hw.x >> (8 * j)) & 0xff; hb[j + 4] = (hw.y >> (8 * j)) & 0xff; }
-  } else {
-#pragma unroll
-    for (int j = 0; j < MAXK; j++) hb[j] = a.hull[i * MAXK + j];
   }
   int h = 0;
 #pragma unroll
@@ -297,7 +306,7 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
     case CS_SCALE_DEPTH: s = dsc; sgrad = 1; break;
     default: s = dsc * dsc; sgrad = G(2) * depth; break;
   }
-  const G delta = exp((G)a.raw_delta[i]), sigma = exp((G)a.raw_sigma[i]);
+  const G delta = exp((G)raw_delta), sigma = exp((G)raw_sigma);
   const G ddel = (G)acc[A_DDEL], dsig = (G)acc[A_DSIG];
   const G d_depth = a.cam.ortho ? G(0) : (ddel * delta + dsig * sigma) * sgrad;
   // view direction (rasterize.py:110-113) and SH VJP (harmonics.py:112-128)
@@ -345,8 +354,8 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 6) chain_kernel(ChainAr
     red_add(a.sig.sigma_signal + i, fabsf(d_rs) * vis);
     red_add(a.sig.sigma_views + i, vis);
   }
-  const float o = 1.f / (1.f + __expf(-a.raw_opacity[i]));
-  const float m = 1.f / (1.f + __expf(-a.raw_mask[i]));
+  const float o = 1.f / (1.f + __expf(-raw_opacity));
+  const float m = 1.f / (1.f + __expf(-raw_mask));
   const float doe = (float)acc[A_DOEFF];
   grad_out<OW>(a.g.d_raw_opacity + i, doe * o * (1.f - o));
   grad_out<OW>(a.g.d_raw_mask + i, doe * o * m * (1.f - m));
