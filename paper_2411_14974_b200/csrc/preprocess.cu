@@ -348,11 +348,14 @@ template <int MAXK>
 __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, double *X,
                                                double *Y) {
   const int k = a.k;
+  // the scalar parameters are loaded up front (their latency overlaps)
+  const float r_mask = __ldg(a.raw_mask + i), r_delta = __ldg(a.raw_delta + i);
+  const float r_sigma = __ldg(a.raw_sigma + i), ro = __ldg(a.raw_opacity + i);
   a.touched[i] = 0u;
   a.depth_keys[i] = kCulledKey;
   a.order[i] = (uint32_t)i;
   // rasterize.py:89 mask gate (model.py:105-107, expit = 1/(1+exp(-x)))
-  const double mask = 1.0 / (1.0 + exp(-(double)a.raw_mask[i]));
+  const double mask = 1.0 / (1.0 + exp(-(double)r_mask));
   if (mask <= kMaskGate) return false;
   // projection.py:22-40
   const double *R = a.cam.R;
@@ -383,9 +386,8 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   // rasterize.py:99-103
   const double depth = zsum / k;
   const double s = depth_scale(a.mode, a.cam.ortho ? 1.0 : depth);
-  const double delta_s = s * exp((double)a.raw_delta[i]);
-  const double sigma_s = s * exp((double)a.raw_sigma[i]);
-  const float ro = a.raw_opacity[i];
+  const double delta_s = s * exp((double)r_delta);
+  const double sigma_s = s * exp((double)r_sigma);
   const double o = 1.0 / (1.0 + exp(-(double)ro));
   // projection.py:157-163
   if (o <= a.cutoff) return false;
