@@ -307,7 +307,10 @@ def main():
     gen = torch.Generator(device=dev).manual_seed(args.seed)
     d_image = torch.randn((cam.height, cam.width, 3), generator=gen, device=dev) * 1e-3
     grads = rz.zero_grads(st)
-    r.launch_backward(fr, d_image, grads)
+    # one untimed counted pass for the work statistics (roofline accounting);
+    # the timed passes run the uncounted kernels
+    r.launch_forward(fr, 0, 2, work_counters=True)
+    r.launch_backward(fr, d_image, grads, work_counters=True)
     stats = r.read_stats(fr)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)            # > 126 MB L2
     stream = torch.cuda.current_stream(dev)

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 4
+#define CS_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define CS_API __attribute__((visibility("default")))
@@ -109,7 +109,8 @@ typedef struct cs_layout {
     size_t total_bytes;
     size_t counters;          /* uint32[32]: [0] n_visible [1] n_pairs [2] overflow;
                                  uint64[8] at word 16: work stats (forward evaluations,
-                                 line evaluations, blends; backward evaluations, lines) */
+                                 line evaluations, blends; backward evaluations, lines),
+                                 counted only with CS_WORK_COUNTERS */
     size_t records;           /* float[n][rec_floats] per-convex blend records */
     size_t hull;              /* uint8[n][max_k]  hull cycle (indices into the K points) */
     size_t bbox;              /* int32[n][4]  x0,x1,y0,y1 half-open pixel rect */
@@ -169,6 +170,16 @@ CS_API int cs_backward_stages(const cs_camera *cam, const cs_settings *set, cons
                               const float *d_image, const cs_grads *grads, int32_t first_stage,
                               int32_t last_stage, void *stream);
 
+/* Stage-wise forward with flags.  CS_WORK_COUNTERS: the blend kernels also
+ * count their work (evaluations, line evaluations, blends, warp
+ * evaluations) into the workspace counters -- diagnostics for the roofline
+ * accounting, ~7% slower blends, off in cs_forward / cs_forward_stages. */
+#define CS_WORK_COUNTERS 2u
+CS_API int cs_forward_ex(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                         void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                         const cs_frame *frame, uint32_t flags, int32_t first_stage, int32_t last_stage,
+                         void *stream);
+
 /* Convenience: copy counters[0..3] to host (synchronises `stream`). */
 CS_API int cs_read_counters(const void *workspace, uint32_t *host_out4, void *stream);
 
@@ -205,7 +216,8 @@ CS_API int cs_backward_signal(const cs_camera *cam, const cs_settings *set, cons
  * the chain WRITES every row of the gradient buffers (rows of convexes this
  * view did not prepare get zeros) instead of accumulating into them -- the
  * result of GradientBuffer() + one view, without a zeroing pass or the read
- * half of the accumulation.  cs_backward == flags 0, stages 0..1. */
+ * half of the accumulation.  CS_WORK_COUNTERS: count the backward blend's
+ * work (see cs_forward_ex).  cs_backward == flags 0, stages 0..1. */
 #define CS_GRADS_OVERWRITE 1u
 CS_API int cs_backward_ex(const cs_camera *cam, const cs_settings *set, const cs_params *params,
                           void *workspace, size_t workspace_bytes, int64_t pair_capacity,

@@ -12,11 +12,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libconvexsplat_sm100.so")
 
 EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forward", "cs_backward",
-           "cs_forward_stages", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
+           "cs_forward_stages", "cs_forward_ex", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
            "cs_backward_signal", "cs_backward_ex", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step",
            "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags", "cs_density_scatter")
-ABI_VERSION = 4
+ABI_VERSION = 5
 GRADS_OVERWRITE = 1   # CS_GRADS_OVERWRITE
+WORK_COUNTERS = 2     # CS_WORK_COUNTERS
 
 _vp = ctypes.c_void_p
 
@@ -109,6 +110,7 @@ def load(path: str = None):
     L.cs_backward.argtypes = [ctypes.POINTER(CsCamera), ctypes.POINTER(CsSettings), ctypes.POINTER(CsParams),
                               _vp, ctypes.c_size_t, ctypes.c_int64, _vp, ctypes.POINTER(CsGrads), _vp]
     L.cs_forward_stages.argtypes = L.cs_forward.argtypes[:-1] + [ctypes.c_int32, ctypes.c_int32, _vp]
+    L.cs_forward_ex.argtypes = L.cs_forward.argtypes[:-1] + [ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, _vp]
     L.cs_backward_stages.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.c_int32, ctypes.c_int32, _vp]
     L.cs_read_counters.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), _vp]
     L.cs_graham_scan_batch.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]
@@ -128,7 +130,8 @@ def load(path: str = None):
                                    _vp, _vp]
     L.cs_density_scatter.argtypes = [ctypes.POINTER(CsParams), ctypes.POINTER(CsDensityConfig), _vp, _vp, _vp,
                                      _vp, _vp, ctypes.POINTER(CsSceneOut), _vp, _vp]
-    for fn in ("cs_workspace_layout", "cs_forward", "cs_backward", "cs_forward_stages", "cs_backward_stages",
+    for fn in ("cs_workspace_layout", "cs_forward", "cs_backward", "cs_forward_stages", "cs_forward_ex",
+               "cs_backward_stages",
                "cs_read_counters", "cs_graham_scan_batch", "cs_backward_signal", "cs_backward_ex",
                "cs_image_loss_workspace",
                "cs_image_loss", "cs_adam_step", "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags",

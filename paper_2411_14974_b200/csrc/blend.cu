@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 
+
 namespace cs {
 
 struct BlendArgs {
@@ -331,7 +332,7 @@ struct FwdPixel {
 
 // One candidate at one pixel: evaluate, and blend iff (T >= floor if floor >
 // 0) and alpha >= cutoff (rasterize.py:194-204).  Returns whether it blended.
-template <int NL, int MAXK>
+template <int NL, int MAXK, bool STATS>
 __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float qx, float qy, float cutoff, float floor_,
                                               bool use_floor, int pos, FwdPixel &P, unsigned &n_lines) {
   const float4 h0 = rec[0], h2 = rec[2];
@@ -339,7 +340,7 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float qx, float
   L.load(rec, __float_as_int(h2.z));
   float z[LineSet<NL, MAXK>::kN];
   const Eval e = eval_field<NL, MAXK>(L, h0.z, h0.w, qx - h0.x, qy - h0.y, z);
-  n_lines += L.nl;
+  if (STATS) n_lines += L.nl;
   if (!(e.alpha >= cutoff)) return false;
   const float4 h1 = rec[1];
   const float w = P.T * e.alpha;
@@ -356,7 +357,7 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float qx, float
 }
 
 // Forward blend (rasterize.py:178-209), one 16x16 tile per block.
-template <int MAXK>
+template <int MAXK, bool STATS>
 #ifndef CS_FWD_MINB
 #define CS_FWD_MINB (CS_FWD_NC == 8 ? 4 : 7)
 #endif
@@ -415,24 +416,24 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
           const uint32_t pj = __shfl_sync(0xffffffffu, pm, j);
           const bool act = !P.done && ((pj >> lane) & 1u);
           if (!__any_sync(0xffffffffu, act)) continue;   // its pixels died earlier in this stage
-          n_warp_evals++;
+          if (STATS) n_warp_evals++;
 #ifdef CS_NO_EVAL
           if (false) {
 #else
           if (act) {
 #endif
-            n_eval++;
+            if (STATS) n_eval++;
             const int pos = (int)first + j;
             if (MAXK == 8) {
               switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
-                case 5: blended = fwd_candidate<5, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-                case 6: blended = fwd_candidate<6, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-                case 4: blended = fwd_candidate<4, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-                case 3: blended = fwd_candidate<3, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-                default: blended = fwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                case 5: blended = fwd_candidate<5, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                case 6: blended = fwd_candidate<6, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                case 4: blended = fwd_candidate<4, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                case 3: blended = fwd_candidate<3, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
+                default: blended = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
               }
             } else {
-              blended = fwd_candidate<0, MAXK>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
+              blended = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
             }
           }
           if (__any_sync(0xffffffffu, blended)) {
@@ -466,10 +467,12 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
                                    ((v2 >= 0.f && v2 <= 1.f) << 2));
     }
   }
-  block_add_u64(a.stats + S_FWD_EVALS, n_eval);
-  block_add_u64(a.stats + S_FWD_LINES, n_lines);
-  block_add_u64(a.stats + S_FWD_BLENDS, n_blend);
-  block_add_u64(a.stats + S_FWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
+  if (STATS) {
+    block_add_u64(a.stats + S_FWD_EVALS, n_eval);
+    block_add_u64(a.stats + S_FWD_LINES, n_lines);
+    block_add_u64(a.stats + S_FWD_BLENDS, n_blend);
+    block_add_u64(a.stats + S_FWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
+  }
 }
 
 // 32 per-lane values -> lane L holds the warp sum of value L.
@@ -498,7 +501,7 @@ struct BwdPixel {
 // reconstruct T_prev = T / (1 - alpha), and add the pixel's 32 screen-space
 // gradient terms to v (unchanged when it did not blend).  Returns whether
 // it did.
-template <int NL, int MAXK, int VN>
+template <int NL, int MAXK, bool STATS, int VN>
 __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float qy, float cutoff, BwdPixel &P,
                                               float (&v)[VN], unsigned &n_lines) {
   const float4 h0 = rec[0], h2 = rec[2];
@@ -509,7 +512,7 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
   const float dx = qx - h0.x, dy = qy - h0.y;
   const float o = h0.w, sig = h0.z, dls = h2.y, inv_dls = h2.w;
   const Eval e = eval_field<NL, MAXK, true>(L, sig, o, dx, dy, z);
-  n_lines += L.nl;
+  if (STATS) n_lines += L.nl;
   if (!(e.alpha >= cutoff)) return false;
   const float4 h1 = rec[1];
   const float om = fmaxf(fmaf(o, e.J, h2.x), 1e-6f);  // 1 - alpha
@@ -568,7 +571,7 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
 #ifndef CS_BWD_PPL
 #define CS_BWD_PPL 2
 #endif
-template <int MAXK, int PPL>
+template <int MAXK, int PPL, bool STATS>
 __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward_kernel(BlendArgs a) {
   constexpr int NC = 8 / PPL;   // warps of 8 x (4 PPL) pixels
   constexpr int AF = Acc<MAXK>::kFloats;
@@ -657,13 +660,13 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           for (int h = 0; h < PPL; h++) {
             const uint32_t pj = __shfl_sync(0xffffffffu, pm[h], j);
             act[h] = cpos <= P[h].last && ((pj >> lane) & 1u);
-            n_eval += (unsigned)act[h];
+            if (STATS) n_eval += (unsigned)act[h];
             any_act |= act[h];
           }
           bool contrib = false;
 #define CS_BWD2_PX(NLV, H)                                                                       \
   if (H < PPL && act[H % PPL])                                                                     \
-    contrib |= bwd_candidate<NLV, MAXK>(rec, qx[H % PPL], qy[H % PPL], a.cutoff, P[H % PPL], v, n_lines);
+    contrib |= bwd_candidate<NLV, MAXK, STATS>(rec, qx[H % PPL], qy[H % PPL], a.cutoff, P[H % PPL], v, n_lines);
 #define CS_BWD2_CASE(NLV) CS_BWD2_PX(NLV, 0) CS_BWD2_PX(NLV, 1) CS_BWD2_PX(NLV, 2) CS_BWD2_PX(NLV, 3)
           if (MAXK == 8) {
             switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
@@ -677,7 +680,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           }
 #undef CS_BWD2_CASE
 #undef CS_BWD2_PX
-          n_warp_evals += __any_sync(0xffffffffu, any_act) ? 1u : 0u;
+          if (STATS) n_warp_evals += __any_sync(0xffffffffu, any_act) ? 1u : 0u;
           if (__any_sync(0xffffffffu, contrib)) {
             float *dst = a.accum + (size_t)sm.id[s][j] * AF;
 #pragma unroll
@@ -694,9 +697,11 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
       if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
   }
-  block_add_u64(a.stats + S_BWD_EVALS, n_eval);
-  block_add_u64(a.stats + S_BWD_LINES, n_lines);
-  block_add_u64(a.stats + S_BWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
+  if (STATS) {
+    block_add_u64(a.stats + S_BWD_EVALS, n_eval);
+    block_add_u64(a.stats + S_BWD_LINES, n_lines);
+    block_add_u64(a.stats + S_BWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
+  }
 }
 
 static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const cs_layout &L, char *ws) {
@@ -724,7 +729,7 @@ static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const c
 }
 
 int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                         const cs_layout &L, char *ws, const cs_frame &f, cudaStream_t s) {
+                         const cs_layout &L, char *ws, const cs_frame &f, bool stats, cudaStream_t s) {
   BlendArgs a = make_args(cam, set, L, ws);
   a.image = f.image;
   a.final_T = f.final_T;
@@ -735,11 +740,13 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
   if (f.visible && p.n > 0) cudaMemsetAsync(f.visible, 0, (size_t)p.n, s);
   const int tiles = L.tiles_x * L.tiles_y;
   if (L.max_k == 8) {
-    cudaFuncSetAttribute(forward_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
-    forward_kernel<8><<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<8, CS_FWD_STAGES>), s>>>(a);
+    auto k = stats ? forward_kernel<8, true> : forward_kernel<8, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
+    k<<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<8, CS_FWD_STAGES>), s>>>(a);
   } else {
-    cudaFuncSetAttribute(forward_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_FWD_STAGES>));
-    forward_kernel<16><<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
+    auto k = stats ? forward_kernel<16, true> : forward_kernel<16, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_FWD_STAGES>));
+    k<<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
@@ -752,7 +759,7 @@ __global__ void __launch_bounds__(512) zero_kernel(float4 *p, size_t n4) {
 }
 
 int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                          const cs_layout &L, char *ws, const float *d_image, cudaStream_t s) {
+                          const cs_layout &L, char *ws, const float *d_image, bool stats, cudaStream_t s) {
   BlendArgs a = make_args(cam, set, L, ws);
   a.d_image = d_image;
   if (p.n > 0) {
@@ -765,11 +772,13 @@ int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs
   }
   const int tiles = L.tiles_x * L.tiles_y;
   if (L.max_k == 8) {
-    cudaFuncSetAttribute(backward_kernel<8, CS_BWD_PPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_BWD_STAGES>));
-    backward_kernel<8, CS_BWD_PPL><<<tiles, pipe_threads<8 / CS_BWD_PPL>(), sizeof(PipeSmem<8, CS_BWD_STAGES>), s>>>(a);
+    auto k = stats ? backward_kernel<8, CS_BWD_PPL, true> : backward_kernel<8, CS_BWD_PPL, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_BWD_STAGES>));
+    k<<<tiles, pipe_threads<8 / CS_BWD_PPL>(), sizeof(PipeSmem<8, CS_BWD_STAGES>), s>>>(a);
   } else {
-    cudaFuncSetAttribute(backward_kernel<16, CS_BWD_PPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_BWD_STAGES>));
-    backward_kernel<16, CS_BWD_PPL><<<tiles, pipe_threads<8 / CS_BWD_PPL>(), sizeof(PipeSmem<16, CS_BWD_STAGES>), s>>>(a);
+    auto k = stats ? backward_kernel<16, CS_BWD_PPL, true> : backward_kernel<16, CS_BWD_PPL, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_BWD_STAGES>));
+    k<<<tiles, pipe_threads<8 / CS_BWD_PPL>(), sizeof(PipeSmem<16, CS_BWD_STAGES>), s>>>(a);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }

@@ -79,10 +79,11 @@ int cs_workspace_layout(const cs_camera *cam, const cs_settings *set, int64_t n,
   return CS_OK;
 }
 
-int cs_forward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
-                      size_t workspace_bytes, int64_t pair_capacity, const cs_frame *frame, int32_t first_stage,
-                      int32_t last_stage, void *stream) {
+int cs_forward_ex(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                  size_t workspace_bytes, int64_t pair_capacity, const cs_frame *frame, uint32_t flags,
+                  int32_t first_stage, int32_t last_stage, void *stream) {
   if (!params || !frame || !workspace) return CS_ERR_ARG;
+  if (flags & ~(uint32_t)CS_WORK_COUNTERS) return CS_ERR_ARG;
   if (first_stage < 0 || last_stage > 2 || first_stage > last_stage) return CS_ERR_ARG;
   cs_layout L;
   int rc = cs_workspace_layout(cam, set, params->n, params->k, pair_capacity, &L);
@@ -101,8 +102,16 @@ int cs_forward_stages(const cs_camera *cam, const cs_settings *set, const cs_par
   if (first_stage <= 1 && last_stage >= 1)
     if ((rc = cs::launch_binning(*cam, *set, *params, L, ws, pair_capacity, s))) return rc;
   if (first_stage <= 2 && last_stage >= 2)
-    if ((rc = cs::launch_forward_blend(*cam, *set, *params, L, ws, *frame, s))) return rc;
+    if ((rc = cs::launch_forward_blend(*cam, *set, *params, L, ws, *frame, (flags & CS_WORK_COUNTERS) != 0, s)))
+      return rc;
   return CS_OK;
+}
+
+int cs_forward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                      size_t workspace_bytes, int64_t pair_capacity, const cs_frame *frame, int32_t first_stage,
+                      int32_t last_stage, void *stream) {
+  return cs_forward_ex(cam, set, params, workspace, workspace_bytes, pair_capacity, frame, 0, first_stage, last_stage,
+                       stream);
 }
 
 int cs_forward(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
@@ -115,7 +124,7 @@ static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_
                          const cs_view_signal *sig, uint32_t flags, int32_t first_stage, int32_t last_stage,
                          void *stream) {
   if (!params || !grads || !workspace || !d_image) return CS_ERR_ARG;
-  if (flags & ~(uint32_t)CS_GRADS_OVERWRITE) return CS_ERR_ARG;
+  if (flags & ~(uint32_t)(CS_GRADS_OVERWRITE | CS_WORK_COUNTERS)) return CS_ERR_ARG;
   if (sig && (!sig->sigma_signal || !sig->sigma_views || !sig->visible)) return CS_ERR_ARG;
   if (first_stage < 0 || last_stage > 1 || first_stage > last_stage) return CS_ERR_ARG;
   cs_layout L;
@@ -128,7 +137,8 @@ static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char *ws = static_cast<char *>(workspace);
   if (first_stage == 0)
-    if ((rc = cs::launch_backward_blend(*cam, *set, *params, L, ws, d_image, s))) return rc;
+    if ((rc = cs::launch_backward_blend(*cam, *set, *params, L, ws, d_image, (flags & CS_WORK_COUNTERS) != 0, s)))
+      return rc;
   if (last_stage == 1)
     return cs::launch_chain(*cam, *set, *params, L, ws, *grads, sig, (flags & CS_GRADS_OVERWRITE) != 0, s);
   return CS_OK;

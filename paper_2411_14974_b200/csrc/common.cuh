@@ -201,9 +201,9 @@ int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_par
 int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                    const cs_layout &L, char *ws, int64_t cap, cudaStream_t s);
 int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                         const cs_layout &L, char *ws, const cs_frame &f, cudaStream_t s);
+                         const cs_layout &L, char *ws, const cs_frame &f, bool stats, cudaStream_t s);
 int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                          const cs_layout &L, char *ws, const float *d_image, cudaStream_t s);
+                          const cs_layout &L, char *ws, const float *d_image, bool stats, cudaStream_t s);
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                  const cs_layout &L, char *ws, const cs_grads &g, const cs_view_signal *sig, bool overwrite,
                  cudaStream_t s);

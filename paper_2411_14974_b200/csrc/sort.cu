@@ -25,9 +25,18 @@ namespace cs {
 
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
-constexpr int kSortThreads = 512;
+#ifndef CS_SORT_THREADS
+#define CS_SORT_THREADS 512
+#endif
+#ifndef CS_SORT_ITEMS
+#define CS_SORT_ITEMS 8
+#endif
+#ifndef CS_SORT_MINB
+#define CS_SORT_MINB 2
+#endif
+constexpr int kSortThreads = CS_SORT_THREADS;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 8;
+constexpr int kSortItems = CS_SORT_ITEMS;
 constexpr int kSortChunk = kSortThreads * kSortItems;  // 4096 keys per chunk
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
@@ -118,7 +127,7 @@ constexpr size_t onesweep_dyn_smem() { return (size_t)kSortChunk * (sizeof(KeyT)
 // is first scattered into shared memory in digit order so that the global
 // writes come out as contiguous runs per digit (coalesced).
 template <typename KeyT>
-__global__ void __launch_bounds__(kSortThreads, 2) onesweep_kernel(PassArgs<KeyT> a) {
+__global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(PassArgs<KeyT> a) {
   extern __shared__ __align__(16) unsigned char onesweep_dyn[];
   KeyT *s_keys = reinterpret_cast<KeyT *>(onesweep_dyn);
   uint32_t *s_vals = reinterpret_cast<uint32_t *>(onesweep_dyn + sizeof(KeyT) * kSortChunk);

@@ -189,19 +189,21 @@ class Rasterizer:
             if cap >= (1 << 30):
                 raise _lib.CsError(f"{fr.n_pairs} tile pairs exceed the supported 2^30")
 
-    def launch_forward(self, fr: Frame, first_stage: int = 0, last_stage: int = 2):
+    def launch_forward(self, fr: Frame, first_stage: int = 0, last_stage: int = 2, work_counters: bool = False):
         """Re-run forward stages of an existing frame (same scene tensors,
         camera, workspace and outputs) without any host synchronisation;
-        stages: 0 preprocess, 1 depth order + binning, 2 blend."""
+        stages: 0 preprocess, 1 depth order + binning, 2 blend.
+        ``work_counters``: the blend also counts its work (``read_stats``)."""
         ws = fr.workspace
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.check(_lib.load().cs_forward_stages(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
-                                                 ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
-                                                 ctypes.byref(fr.extras["frame_c"]), first_stage, last_stage,
-                                                 stream), "cs_forward_stages")
+        _lib.check(_lib.load().cs_forward_ex(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
+                                             ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
+                                             ctypes.byref(fr.extras["frame_c"]),
+                                             _lib.WORK_COUNTERS if work_counters else 0, first_stage, last_stage,
+                                             stream), "cs_forward_ex")
 
     def launch_backward(self, fr: Frame, d_image: torch.Tensor, grads: dict, first_stage: int = 0,
-                        last_stage: int = 1, signal=None, overwrite: bool = False):
+                        last_stage: int = 1, signal=None, overwrite: bool = False, work_counters: bool = False):
         """Backward stages (0 blend, 1 chain) into ``grads`` (+=, or written
         when ``overwrite``: every row, zeros for convexes the view did not
         prepare), no sync.  ``signal`` = (sigma_signal, sigma_views, visible)
@@ -220,12 +222,14 @@ class Rasterizer:
                                               ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
                                               d_image.data_ptr(), ctypes.byref(g),
                                               ctypes.byref(sig) if sig is not None else None,
-                                              _lib.GRADS_OVERWRITE if overwrite else 0, first_stage, last_stage,
+                                              (_lib.GRADS_OVERWRITE if overwrite else 0) |
+                                              (_lib.WORK_COUNTERS if work_counters else 0), first_stage, last_stage,
                                               stream), "cs_backward_ex")
 
     @staticmethod
     def read_stats(fr: Frame) -> dict:
-        """Work counters of the last forward/backward on this workspace (syncs)."""
+        """Work counters of the last forward/backward on this workspace (syncs);
+        the blend counts are filled only by calls with ``work_counters``."""
         c = fr.workspace.counters().cpu()
         stats = c[16:32].view(torch.int64).numpy()
         out = {name: int(stats[i]) for i, name in enumerate(STAT_NAMES)}
