@@ -48,6 +48,12 @@ struct BlendArgs {
   const float *d_image;
   float *accum;
   unsigned long long *stats;
+  // blend masks: word (range.x / 32 + tile + b) of array q = which of the
+  // 32 candidates of forward batch b some pixel of the tile's 8x4 block q
+  // blended (8 arrays of mask_words words in the scratch); the backward
+  // skips the others
+  uint32_t *blend_mask;
+  uint32_t mask_words;
 };
 
 struct Eval {
@@ -445,7 +451,12 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
             }
           }
         }
-        if (lane == 0 && vis) atomicOr(&sm.vis[s], vis);
+        if (lane == 0) {
+          if (vis) atomicOr(&sm.vis[s], vis);
+          // word (range.x / 32 + tile + b) of this block's mask: unique per
+          // (tile, batch), written for every batch the warp processed
+          a.blend_mask[(size_t)(warp + (NC == 8 ? 0 : 4 * half)) * a.mask_words + (range.x >> 5) + tile + b] = vis;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
@@ -630,9 +641,24 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
   } else {
     for (int b = 0; b < nbatch; b++) {
       const int s = b % kStages;
-      mbar_wait(&sm.full[s], (b / kStages) & 1);
       uint32_t first, count;
       batch(b, first, count);
+      // the forward's blend masks of this warp's 8x4 blocks for the batch
+      // (loaded before the wait): candidates none of a block's pixels
+      // blended are skipped for it
+      uint32_t fm[PPL];
+      if ((int)first <= warp_last) {
+#pragma unroll
+        for (int h = 0; h < PPL; h++) {
+          const int sub = ((((ry0 - ty * kTile) >> 2) + h) << 1) | ((rx0 - tx * kTile) >> 3);
+          const uint32_t rel = first - range.x;   // forward batch rel / 32, bit rel % 32
+          const uint32_t *mk = a.blend_mask + (size_t)sub * a.mask_words + (range.x >> 5) + tile + (rel >> 5);
+          const uint32_t sh = rel & 31u;
+          const uint32_t w0 = __ldg(mk), w1 = sh ? __ldg(mk + 1) : 0u;
+          fm[h] = sh ? (w0 >> sh) | (w1 << (32u - sh)) : w0;
+        }
+      }
+      mbar_wait(&sm.full[s], (b / kStages) & 1);
       if ((int)first <= warp_last) {
         const uint32_t pos = first + lane;
         uint32_t pm[PPL], any = 0u;
@@ -642,7 +668,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           const int4 bb = rec_bbox(sm.rec[s][lane]);
 #pragma unroll
           for (int h = 0; h < PPL; h++) {
-            pm[h] = block_mask(bb, rx0, ry0 + 4 * h);
+            pm[h] = ((fm[h] >> lane) & 1u) ? block_mask(bb, rx0, ry0 + 4 * h) : 0u;
             any |= pm[h];
           }
         }
@@ -719,6 +745,8 @@ static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const c
   a.pixel_last = reinterpret_cast<int32_t *>(ws + L.pixel_last);
   a.pixel_T = reinterpret_cast<float *>(ws + L.pixel_T);
   a.pixel_clamp = reinterpret_cast<uint8_t *>(ws + L.pixel_clamp);
+  a.blend_mask = reinterpret_cast<uint32_t *>(ws + L.scratch + blend_mask_offset());
+  a.mask_words = blend_mask_words((int64_t)((L.pair_ids - L.pair_tiles) / sizeof(uint32_t)), L.tiles_x * L.tiles_y);
   a.accum = reinterpret_cast<float *>(ws + L.grad_accum);
   a.stats = reinterpret_cast<unsigned long long *>(ws + L.counters + sizeof(uint32_t) * C_STATS);
   a.image = a.final_T = a.weight_sum = a.depth = nullptr;

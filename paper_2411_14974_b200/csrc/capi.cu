@@ -72,7 +72,7 @@ int cs_workspace_layout(const cs_camera *cam, const cs_settings *set, int64_t n,
   L.pixel_T = take(sizeof(float) * npix);
   L.pixel_clamp = take(npix);
   L.grad_accum = take(sizeof(float) * un * L.acc_floats);
-  L.scratch_bytes = cs::scratch_bytes(n, pair_capacity, pp, nullptr, nullptr);
+  L.scratch_bytes = cs::scratch_bytes(n, pair_capacity, pp, tiles, nullptr, nullptr);
   L.scratch = take(L.scratch_bytes);
   L.total_bytes = off;
   *out = L;

@@ -74,7 +74,7 @@ struct Layout {
   cs_layout l;
 };
 
-inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Order-preserving map of a double to uint64 (ascending).
 __device__ __forceinline__ uint64_t orderable_bits(double d) {
@@ -221,6 +221,9 @@ int launch_density_scatter(const cs_params &P, const cs_density_config &c, const
                            const int64_t *n_surv, const cs_scene_out &o, int64_t *index_map, cudaStream_t s);
 int launch_hull_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts,
                       int32_t *hull, int32_t *hull_n, cudaStream_t s);
-size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, struct Scratch *sc, char *base);
+size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, int tiles, struct Scratch *sc, char *base);
+// forward blend masks (8 bit arrays of blend_mask_words words) in the scratch, after the tile order
+uint32_t blend_mask_words(int64_t cap, int tiles);
+constexpr size_t blend_mask_offset() { return align_up(sizeof(uint32_t) * kMaxTileOrder, 256); }
 int pair_sort_passes(int tiles);
 }  // namespace cs

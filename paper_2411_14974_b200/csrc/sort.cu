@@ -626,13 +626,18 @@ struct Scratch {
   size_t lookback_words;
 };
 
-size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, Scratch *sc, char *base) {
+uint32_t blend_mask_words(int64_t cap, int tiles) {
+  return (uint32_t)(align_up((size_t)cap * sizeof(uint32_t), 256) / sizeof(uint32_t) / 32 + tiles + 2);
+}
+
+size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, int tiles, Scratch *sc, char *base) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return base ? base + o : nullptr; };
   const size_t dchunks = (size_t)((n + kSortChunk - 1) / kSortChunk);
   const size_t pchunks = (size_t)((cap + kSortChunk - 1) / kSortChunk);
   const size_t lb_words = (8 * dchunks + pair_passes * pchunks) * kRadix;
   take(sizeof(uint32_t) * kMaxTileOrder);   // tile_order first: the blends find it at scratch + 0
+  take(sizeof(uint32_t) * 8 * (size_t)blend_mask_words(cap, tiles));   // then the blend masks (blend_mask_offset)
   char *p0 = take(sizeof(uint64_t) * n);
   char *p1 = take(sizeof(uint32_t) * n);
   char *p2 = take(sizeof(uint32_t) * cap);
@@ -663,7 +668,7 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
   const int tiles = L.tiles_x * L.tiles_y;
   const int pp = pair_sort_passes(tiles);
   Scratch sc;
-  scratch_bytes(p.n, cap, pp, &sc, ws + L.scratch);
+  scratch_bytes(p.n, cap, pp, tiles, &sc, ws + L.scratch);
   uint32_t *counters = reinterpret_cast<uint32_t *>(ws + L.counters);
   uint64_t *dkeys = reinterpret_cast<uint64_t *>(ws + L.depth_keys);
   uint32_t *order = reinterpret_cast<uint32_t *>(ws + L.order);

@@ -370,13 +370,14 @@ def inspect_frame(fr: Frame) -> dict:
     keys = _np(ws.region("depth_keys", torch.int64, n)).view(np.uint64)[order]
     ranges = _np(ws.region("tile_ranges", torch.int32, 2 * tiles)).reshape(tiles, 2).astype(np.int64)
     pair_ids = _np(ws.region("pair_ids", torch.int32, P)).astype(np.int64)
-    pair_tiles = _np(ws.region("pair_tiles", torch.int32, P)).astype(np.int64)
     recs = _np(ws.region("records", torch.float32, n * L.rec_floats)).reshape(n, L.rec_floats)
     off = np.zeros(tiles + 1, np.int64)
     counts = np.zeros(tiles, np.int64)
     nz = ranges[:, 1] > ranges[:, 0]
     counts[nz] = ranges[nz, 1] - ranges[nz, 0]
     off[1:] = np.cumsum(counts)
+    # tile of every list entry (CSR order)
+    pair_tiles = np.repeat(np.arange(tiles, dtype=np.int64), counts)
     return dict(order=order, hull=hull, bbox=bbox, depth=_decode_depth(keys), tile_ranges=ranges,
                 pair_ids=pair_ids, pair_tiles=pair_tiles, tile_offsets=off, records=recs,
                 tiles_x=L.tiles_x, tiles_y=L.tiles_y, n_visible=V, n_pairs=P)
