@@ -29,7 +29,6 @@ struct PreArgs {
   uint8_t *hull;
   int4 *bbox;
   uint64_t *depth_keys;
-  uint32_t *order;
   uint32_t *touched;
   uint32_t *counters;
   double cam_center[3];
@@ -353,7 +352,6 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   const float r_sigma = __ldg(a.raw_sigma + i), ro = __ldg(a.raw_opacity + i);
   a.touched[i] = 0u;
   a.depth_keys[i] = kCulledKey;
-  a.order[i] = (uint32_t)i;
   // rasterize.py:89 mask gate (model.py:105-107, expit = 1/(1+exp(-x)))
   const double mask = 1.0 / (1.0 + exp(-(double)r_mask));
   if (mask <= kMaskGate) return false;
@@ -597,7 +595,6 @@ int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_par
   a.hull = reinterpret_cast<uint8_t *>(ws + L.hull);
   a.bbox = reinterpret_cast<int4 *>(ws + L.bbox);
   a.depth_keys = reinterpret_cast<uint64_t *>(ws + L.depth_keys);
-  a.order = reinterpret_cast<uint32_t *>(ws + L.order);
   a.touched = reinterpret_cast<uint32_t *>(ws + L.tiles_touched);
   a.counters = reinterpret_cast<uint32_t *>(ws + L.counters);
   camera_center(cam, a.cam_center);
