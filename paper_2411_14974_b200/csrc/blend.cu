@@ -431,13 +431,11 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
             if (STATS) n_eval++;
             const int pos = (int)first + j;
             if (MAXK == 8) {
-              switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
-                case 5: blended = fwd_candidate<5, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-                case 6: blended = fwd_candidate<6, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-                case 4: blended = fwd_candidate<4, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-                case 3: blended = fwd_candidate<3, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-                default: blended = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines); break;
-              }
+              const int nl = __float_as_int(rec[2].z);   // warp-uniform line count (an if chain: a switch became a jump table)
+              if (nl == 5) blended = fwd_candidate<5, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
+              else if (nl == 6) blended = fwd_candidate<6, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
+              else if (nl == 4) blended = fwd_candidate<4, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
+              else blended = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
             } else {
               blended = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
             }
@@ -695,12 +693,11 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
     contrib |= bwd_candidate<NLV, MAXK, STATS>(rec, qx[H % PPL], qy[H % PPL], a.cutoff, P[H % PPL], v, n_lines);
 #define CS_BWD2_CASE(NLV) CS_BWD2_PX(NLV, 0) CS_BWD2_PX(NLV, 1) CS_BWD2_PX(NLV, 2) CS_BWD2_PX(NLV, 3)
           if (MAXK == 8) {
-            switch (__float_as_int(rec[2].z)) {  // warp-uniform line count
-              case 5: { CS_BWD2_CASE(5) } break;
-              case 6: { CS_BWD2_CASE(6) } break;
-              case 4: { CS_BWD2_CASE(4) } break;
-              default: { CS_BWD2_CASE(0) } break;
-            }
+            const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
+            if (nl == 5) { CS_BWD2_CASE(5) }
+            else if (nl == 6) { CS_BWD2_CASE(6) }
+            else if (nl == 4) { CS_BWD2_CASE(4) }
+            else { CS_BWD2_CASE(0) }
           } else {
             CS_BWD2_CASE(0)
           }
