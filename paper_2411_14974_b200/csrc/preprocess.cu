@@ -192,6 +192,13 @@ struct NibbleListT {
     w = (w & low(i)) | ((w >> 4) & ~low(i));
     n--;
   }
+  // entries start, start+1, ..., n-1, 0, ..., start-1 (cyclic rotation)
+  __device__ __forceinline__ NibbleListT rotated(int start) const {
+    NibbleListT r;
+    r.n = n;
+    r.w = start == 0 ? w : (((w >> (4 * start)) | (w << (4 * (n - start)))) & low(n));
+    return r;
+  }
 };
 // 8 entries fit a 32-bit word (the K <= 8 kernels: cheaper shifts than 64-bit)
 using NibbleList = NibbleListT<uint64_t>;
@@ -270,8 +277,8 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
   while (changed && st.n >= 3) {
     changed = false;
     const int sn = st.n;
-    for (int q = 0; q < sn; q++) {
-      if (cross(st.get((q - 1 + sn) % sn), st.get(q), st.get((q + 1) % sn)) <= kCrossTol) {
+    for (int q = 0; q < sn; q++) {   // neighbours without integer modulo
+      if (cross(st.get(q == 0 ? sn - 1 : q - 1), st.get(q), st.get(q + 1 == sn ? 0 : q + 1)) <= kCrossTol) {
         st.erase(q);
         changed = true;
         break;
@@ -282,8 +289,7 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
   int start = 0;
   for (int q = 0; q < st.n; q++)
     if (st.get(q) == ref) { start = q; break; }
-  out = NL();
-  for (int q = 0; q < st.n; q++) out.push(st.get((start + q) % st.n));
+  out = st.rotated(start);
   return out.n;
 #undef GX
 #undef GY
