@@ -482,16 +482,20 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   a.touched[i] = (uint32_t)(((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1));
   a.depth_keys[i] = orderable_bits(depth);
   // rasterize.py:110-114 view direction; harmonics.py:101-109 colour (float32,
-  // SH rows read straight from global: 12 x 16-byte loads per thread)
-  const double dvx = cx / k - a.cam_center[0], dvy = cy / k - a.cam_center[1], dvz = cz / k - a.cam_center[2];
-  const double dist = sqrt(dvx * dvx + dvy * dvy + dvz * dvz);
+  // SH rows read straight from global: 12 x 16-byte loads per thread).  The
+  // direction only feeds the continuous colour: centre offset in float64
+  // (no cancellation), normalisation in float32 (no float64 divisions).
+  const double ik = 1.0 / k;
+  const float vx = (float)(cx * ik - a.cam_center[0]), vy = (float)(cy * ik - a.cam_center[1]),
+              vz = (float)(cz * ik - a.cam_center[2]);
+  const float d2 = vx * vx + vy * vy + vz * vz;
   float dx = 0.f, dy = 0.f, dz = 1.f;
-  if (dist > 0.0) { dx = (float)(dvx / dist); dy = (float)(dvy / dist); dz = (float)(dvz / dist); }
+  if (d2 > 0.f) { const float rs = rsqrtf(d2); dx = vx * rs; dy = vy * rs; dz = vz * rs; }
   float col[3];
   sh_colour(dx, dy, dz, a.sh_degree, a.sh + i * kShCoeffs * 3, col);
   dst[0] = make_float4((float)axd, (float)ayd, (float)sigma_s, (float)o);
   dst[1] = make_float4(col[0], col[1], col[2], (float)depth);
-  dst[2] = make_float4(1.f / (1.f + __expf(ro)), (float)dls, __int_as_float(h), (float)(1.0 / dls));
+  dst[2] = make_float4(1.f / (1.f + __expf(ro)), (float)dls, __int_as_float(h), __frcp_rn((float)dls));
   dst[3] = make_float4(__int_as_float(x0), __int_as_float(x1), __int_as_float(y0), __int_as_float(y1));
   return true;
 }
