@@ -74,7 +74,7 @@ __device__ __forceinline__ uint32_t block_mask(int4 b, int rx0, int ry0) {
   const int r0 = max(b.z - ry0, 0), r1 = min(b.w - ry0, 4);
   if (c1 <= c0 || r1 <= r0) return 0u;
   const uint32_t cols = (1u << c1) - (1u << c0);                                  // < 256
-  const uint32_t rows = (uint32_t)(((1ull << (8 * r1)) - (1ull << (8 * r0))) / 255ull);  // 0x01 per row byte
+  const uint32_t rows = (0x01010101u >> (8 * (4 - (r1 - r0)))) << (8 * r0);         // 0x01 per row byte
   return cols * rows;
 }
 __device__ __forceinline__ int4 rec_bbox(const float4 *rec) {
