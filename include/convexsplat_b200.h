@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 5
+#define CS_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define CS_API __attribute__((visibility("default")))
@@ -231,10 +231,12 @@ CS_API int cs_image_loss_workspace(int32_t height, int32_t width, size_t *bytes)
  * ssim_with_grad (losses.py:58-101): (1-lambda) L1 + lambda (1-SSIM)/2 +
  * beta mean(sigmoid(raw_mask)), 11x11 sigma-1.5 Gaussian on the valid region.
  * rendered/target [H,W,3]; d_image [H,W,3] is WRITTEN (d loss / d rendered);
- * d_raw_mask [n] is ACCUMULATED (+=) like trainer.py:176.  stats[4] (device,
- * written): sum |rendered - target|, sum over channels of sum of the SSIM map,
- * sum sigmoid(raw_mask), number of valid SSIM positions per channel.
- * total = (1-lambda) stats0/(3HW) + lambda (1 - stats1/(3 stats3))/2 + beta stats2/n. */
+ * d_raw_mask [n] is ACCUMULATED (+=) like trainer.py:176.  stats[9] (device,
+ * written): [0] sum |rendered - target|, [1] sum over channels of sum of the
+ * SSIM map, [2] sum sigmoid(raw_mask), [3] number of valid SSIM positions per
+ * channel; then the values [4] total = (1-lambda) l1 + lambda dssim + beta
+ * mask_term, [5] l1 = stats0/(3HW), [6] ssim = stats1/(3 stats3), [7] dssim =
+ * (1 - ssim)/2, [8] mask_term = stats2/n. */
 CS_API int cs_image_loss(int32_t height, int32_t width, const float *rendered, const float *target,
                          const float *raw_mask, int64_t n, double lambda_dssim, double beta_mask,
                          float *d_image, float *d_raw_mask, double *stats, void *workspace,

@@ -15,7 +15,7 @@ EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forwa
            "cs_forward_stages", "cs_forward_ex", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
            "cs_backward_signal", "cs_backward_ex", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step",
            "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags", "cs_density_scatter")
-ABI_VERSION = 5
+ABI_VERSION = 6
 GRADS_OVERWRITE = 1   # CS_GRADS_OVERWRITE
 WORK_COUNTERS = 2     # CS_WORK_COUNTERS
 

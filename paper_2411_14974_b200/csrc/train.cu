@@ -189,6 +189,17 @@ __global__ void loss_stats_init_kernel(double *stats, double valid) {
   stats[0] = 0.0; stats[1] = 0.0; stats[2] = 0.0; stats[3] = valid;
 }
 
+// The loss values from the sums (losses.py:129-155), one thread: the caller
+// reads device scalars without further kernels.
+__global__ void loss_finalize_kernel(double *stats, int H, int W, int64_t n, double lam, double beta) {
+  const double l1 = stats[0] / (3.0 * H * W);
+  const double ssim = stats[1] / (3.0 * stats[3]);
+  const double dssim = (1.0 - ssim) / 2.0;
+  const double mask_term = n ? stats[2] / (double)n : 0.0;
+  stats[4] = (1.0 - lam) * l1 + lam * dssim + beta * mask_term;
+  stats[5] = l1; stats[6] = ssim; stats[7] = dssim; stats[8] = mask_term;
+}
+
 // ------------------------------------------------------------------ Adam
 struct AdamArgs {
   cs_adam_tensor t[8];
@@ -238,6 +249,7 @@ int launch_image_loss(int H, int W, const float *img, const float *tgt, const fl
     const int blocks = (int)std::min<int64_t>((n + kLossThreads - 1) / kLossThreads, 148 * 8);
     mask_term_kernel<<<blocks, kLossThreads, 0, s>>>(raw_mask, n, (float)beta, d_raw_mask, stats);
   }
+  loss_finalize_kernel<<<1, 1, 0, s>>>(stats, H, W, n, lam, beta);
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
 

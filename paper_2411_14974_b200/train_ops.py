@@ -41,7 +41,7 @@ class LossWorkspace:
         if self.buffer is None or self.buffer.numel() < nbytes.value or self.buffer.device != torch.device(device):
             self.buffer = torch.empty(max(nbytes.value, 16), dtype=torch.uint8, device=device)
         if self.stats is None or self.stats.device != torch.device(device):
-            self.stats = torch.zeros(4, dtype=torch.float64, device=device)
+            self.stats = torch.zeros(9, dtype=torch.float64, device=device)
 
 
 def image_loss(rendered: torch.Tensor, target: torch.Tensor, raw_mask: torch.Tensor, lambda_dssim: float = 0.2,
@@ -72,13 +72,8 @@ def image_loss(rendered: torch.Tensor, target: torch.Tensor, raw_mask: torch.Ten
                                          d_raw_mask.data_ptr() if d_raw_mask is not None else None,
                                          ws.stats.data_ptr(), ws.buffer.data_ptr(), ws.buffer.numel(), stream),
                "cs_image_loss")
-    st = ws.stats
-    l1 = st[0] / (3.0 * H * W)
-    ssim = st[1] / (3.0 * st[3])
-    dssim = (1.0 - ssim) / 2.0
-    mask_term = st[2] / n if n else torch.zeros((), dtype=torch.float64, device=rendered.device)
-    total = (1.0 - lambda_dssim) * l1 + lambda_dssim * dssim + beta_mask * mask_term
-    return {"total": total, "l1": l1, "dssim": dssim, "ssim": ssim, "mask_term": mask_term, "d_image": d_image}
+    st = ws.stats.clone()   # values formed on the device (stats[4:9]); the clone survives the next call
+    return {"total": st[4], "l1": st[5], "dssim": st[7], "ssim": st[6], "mask_term": st[8], "d_image": d_image}
 
 
 class FusedAdam:

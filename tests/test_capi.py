@@ -129,7 +129,7 @@ def test_training_entry_points_validate_before_launching(lib):
     cfg = _lib.CsDensityConfig()
     assert lib.cs_density_flags(ctypes.byref(p), None, None, None, None, None, None, None) == 1
     assert lib.cs_density_flags(ctypes.byref(p), None, ctypes.byref(cfg), None, None, None, None, None) == 0
-    assert lib.cs_abi_version() == _lib.ABI_VERSION == 5
+    assert lib.cs_abi_version() == _lib.ABI_VERSION == 6
 
 
 def test_backward_ex_validates_flags_and_signal(lib):
