@@ -26,7 +26,7 @@ struct Win {
   float w[kWin];
 };
 
-constexpr int kLossTW = 32, kLossTH = 16, kLossThreads = 256;
+constexpr int kLossThreads = 256;
 
 __device__ __forceinline__ void atomic_add_block_sum(double *dst, double v) {
   __shared__ double s_part[kLossThreads / 32];
@@ -40,18 +40,24 @@ __device__ __forceinline__ void atomic_add_block_sum(double *dst, double v) {
   }
 }
 
-// One 32x16 tile of the valid grid of one channel (blockIdx.z).  maps:
+// One 32x32 tile of the valid grid of one channel (blockIdx.z).  maps:
 // [3 channels][3: dMx, dVxx, dVxy][Hv*Wv], scaled by 1/(3 Hv Wv).
+// Register-blocked separable window: the horizontal pass gives each thread
+// 4 adjacent outputs of a row (14 inputs loaded once), the vertical pass 4
+// adjacent outputs of a column (14 rows of the 5 moments loaded once).
+constexpr int kSsimT = 32;            // output tile side
+constexpr int kSsimR = kSsimT + kHalo;
+constexpr int kSsimB = 4;             // outputs per thread and pass
+
 __global__ void __launch_bounds__(kLossThreads) ssim_moments_kernel(int H, int W, const float *img, const float *tgt,
                                                                     float *maps, double *stats, Win win) {
-  constexpr int RW = kLossTW + kHalo, RH = kLossTH + kHalo;
-  __shared__ float sx[RH][RW], sy[RH][RW];
-  __shared__ float hs[5][RH][kLossTW];
+  __shared__ float sx[kSsimR][kSsimR], sy[kSsimR][kSsimR];
+  __shared__ float hs[5][kSsimR][kSsimT];
   const int c = blockIdx.z;
   const int Hv = H - kHalo, Wv = W - kHalo;
-  const int ox = blockIdx.x * kLossTW, oy = blockIdx.y * kLossTH;
-  for (int q = threadIdx.x; q < RH * RW; q += kLossThreads) {
-    const int r = q / RW, col = q % RW;
+  const int ox = blockIdx.x * kSsimT, oy = blockIdx.y * kSsimT;
+  for (int q = threadIdx.x; q < kSsimR * kSsimR; q += kLossThreads) {
+    const int r = q / kSsimR, col = q % kSsimR;
     const int gy = oy + r, gx = ox + col;
     float xv = 0.f, yv = 0.f;
     if (gy < H && gx < W) {
@@ -63,72 +69,97 @@ __global__ void __launch_bounds__(kLossThreads) ssim_moments_kernel(int H, int W
     sy[r][col] = yv;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < RH * kLossTW; q += kLossThreads) {  // horizontal window
-    const int r = q / kLossTW, col = q % kLossTW;
-    float mx = 0.f, my = 0.f, vxx = 0.f, vyy = 0.f, vxy = 0.f;
+  // horizontal: item = (row, 4-column group)
+  for (int q = threadIdx.x; q < kSsimR * (kSsimT / kSsimB); q += kLossThreads) {
+    const int r = q / (kSsimT / kSsimB), c0 = (q % (kSsimT / kSsimB)) * kSsimB;
+    float xv[kSsimB + kHalo], yv[kSsimB + kHalo];
 #pragma unroll
-    for (int u = 0; u < kWin; u++) {
-      const float w = win.w[u], xv = sx[r][col + u], yv = sy[r][col + u];
-      mx = fmaf(w, xv, mx);
-      my = fmaf(w, yv, my);
-      vxx = fmaf(w, xv * xv, vxx);
-      vyy = fmaf(w, yv * yv, vyy);
-      vxy = fmaf(w, xv * yv, vxy);
+    for (int u = 0; u < kSsimB + kHalo; u++) { xv[u] = sx[r][c0 + u]; yv[u] = sy[r][c0 + u]; }
+#pragma unroll
+    for (int o = 0; o < kSsimB; o++) {
+      float mx = 0.f, my = 0.f, vxx = 0.f, vyy = 0.f, vxy = 0.f;
+#pragma unroll
+      for (int u = 0; u < kWin; u++) {
+        const float w = win.w[u], a = xv[o + u], b = yv[o + u];
+        mx = fmaf(w, a, mx);
+        my = fmaf(w, b, my);
+        vxx = fmaf(w, a * a, vxx);
+        vyy = fmaf(w, b * b, vyy);
+        vxy = fmaf(w, a * b, vxy);
+      }
+      hs[0][r][c0 + o] = mx; hs[1][r][c0 + o] = my; hs[2][r][c0 + o] = vxx; hs[3][r][c0 + o] = vyy;
+      hs[4][r][c0 + o] = vxy;
     }
-    hs[0][r][col] = mx; hs[1][r][col] = my; hs[2][r][col] = vxx; hs[3][r][col] = vyy; hs[4][r][col] = vxy;
   }
   __syncthreads();
+  // vertical: item = (column, 4-row group)
   const float scale = 1.f / (3.f * (float)Hv * (float)Wv);
+  const size_t plane = (size_t)Hv * Wv;
+  float *mc = maps + (size_t)c * 3 * plane;
   double ssum = 0.0;
-  for (int q = threadIdx.x; q < kLossTH * kLossTW; q += kLossThreads) {  // vertical window
-    const int r = q / kLossTW, col = q % kLossTW;
-    const int gy = oy + r, gx = ox + col;
-    if (gy >= Hv || gx >= Wv) continue;
-    float M[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int q = threadIdx.x; q < kSsimT * (kSsimT / kSsimB); q += kLossThreads) {
+    const int col = q % kSsimT, r0 = (q / kSsimT) * kSsimB;
+    float M[kSsimB][5];
 #pragma unroll
-    for (int u = 0; u < kWin; u++) {
-      const float w = win.w[u];
+    for (int o = 0; o < kSsimB; o++)
 #pragma unroll
-      for (int f = 0; f < 5; f++) M[f] = fmaf(w, hs[f][r + u][col], M[f]);
+      for (int f = 0; f < 5; f++) M[o][f] = 0.f;
+#pragma unroll
+    for (int u = 0; u < kSsimB + kHalo; u++) {
+      float h[5];
+#pragma unroll
+      for (int f = 0; f < 5; f++) h[f] = hs[f][r0 + u][col];
+#pragma unroll
+      for (int o = 0; o < kSsimB; o++) {
+        const int t = u - o;   // window tap of output row r0 + o
+        if (t >= 0 && t < kWin) {
+#pragma unroll
+          for (int f = 0; f < 5; f++) M[o][f] = fmaf(win.w[t], h[f], M[o][f]);
+        }
+      }
     }
-    const float Mx = M[0], My = M[1];
-    const float mux = Mx + 0.5f, muy = My + 0.5f;
-    const float sxx = M[2] - Mx * Mx, syy = M[3] - My * My, sxy = M[4] - Mx * My;
-    const float a1 = 2.f * mux * muy + kC1, a2 = 2.f * sxy + kC2;
-    const float b1 = mux * mux + muy * muy + kC1, b2 = sxx + syy + kC2;
-    const float inv = 1.f / (b1 * b2);
-    const float smap = a1 * a2 * inv;
-    ssum += smap;
-    // d smap / d (Mx, Vxx, Vxy) of the shifted statistics (same derivative
-    // as losses.py:86-94 in exact arithmetic)
-    const float dMx = 2.f * muy * a2 * inv - 2.f * mux * smap / b1 + 2.f * Mx * smap / b2 - 2.f * My * a1 * inv;
-    const float dVxx = -smap / b2;
-    const float dVxy = 2.f * a1 * inv;
-    const size_t o = (size_t)gy * Wv + gx, plane = (size_t)Hv * Wv;
-    float *mc = maps + (size_t)c * 3 * plane;
-    mc[o] = scale * dMx;
-    mc[plane + o] = scale * dVxx;
-    mc[2 * plane + o] = scale * dVxy;
+#pragma unroll
+    for (int o = 0; o < kSsimB; o++) {
+      const int gy = oy + r0 + o, gx = ox + col;
+      if (gy >= Hv || gx >= Wv) continue;
+      const float Mx = M[o][0], My = M[o][1];
+      const float mux = Mx + 0.5f, muy = My + 0.5f;
+      const float sxx = M[o][2] - Mx * Mx, syy = M[o][3] - My * My, sxy = M[o][4] - Mx * My;
+      const float a1 = 2.f * mux * muy + kC1, a2 = 2.f * sxy + kC2;
+      const float b1 = mux * mux + muy * muy + kC1, b2 = sxx + syy + kC2;
+      const float inv = 1.f / (b1 * b2);
+      const float smap = a1 * a2 * inv;
+      ssum += smap;
+      // d smap / d (Mx, Vxx, Vxy) of the shifted statistics (same derivative
+      // as losses.py:86-94 in exact arithmetic)
+      const float dMx = 2.f * muy * a2 * inv - 2.f * mux * smap / b1 + 2.f * Mx * smap / b2 - 2.f * My * a1 * inv;
+      const float dVxx = -smap / b2;
+      const float dVxy = 2.f * a1 * inv;
+      const size_t oo = (size_t)gy * Wv + gx;
+      mc[oo] = scale * dMx;
+      mc[plane + oo] = scale * dVxx;
+      mc[2 * plane + oo] = scale * dVxy;
+    }
   }
   atomic_add_block_sum(stats + 1, ssum);
 }
 
-// d_image for one 32x16 tile of the full image, one channel: transposed
-// window over the coefficient maps (losses.py:45-55), combined with the
+// d_image for one 32x32 tile of the full image, one channel: transposed
+// window over the coefficient maps (losses.py:45-55; the Gaussian is
+// symmetric, so the transposed window is the window), combined with the
 // pixel (losses.py:96-100), plus the L1 term; accumulates sum |diff|.
 __global__ void __launch_bounds__(kLossThreads) ssim_adjoint_kernel(int H, int W, const float *img, const float *tgt,
                                                                     const float *maps, float lam, float *d_image,
                                                                     double *stats, Win win) {
-  constexpr int RW = kLossTW + kHalo, RH = kLossTH + kHalo;
-  __shared__ float sm[3][RH][RW];
-  __shared__ float hs[3][RH][kLossTW];
+  __shared__ float sm[3][kSsimR][kSsimR];
+  __shared__ float hs[3][kSsimR][kSsimT];
   const int c = blockIdx.z;
   const int Hv = H - kHalo, Wv = W - kHalo;
-  const int ox = blockIdx.x * kLossTW, oy = blockIdx.y * kLossTH;
+  const int ox = blockIdx.x * kSsimT, oy = blockIdx.y * kSsimT;
   const size_t plane = (size_t)Hv * Wv;
   const float *mc = maps + (size_t)c * 3 * plane;
-  for (int q = threadIdx.x; q < RH * RW; q += kLossThreads) {   // map rows oy-10.., cols ox-10..
-    const int r = q / RW, col = q % RW;
+  for (int q = threadIdx.x; q < kSsimR * kSsimR; q += kLossThreads) {   // map rows oy-10.., cols ox-10..
+    const int r = q / kSsimR, col = q % kSsimR;
     const int my = oy - kHalo + r, mx = ox - kHalo + col;
     const bool in = my >= 0 && my < Hv && mx >= 0 && mx < Wv;
     const size_t o = in ? (size_t)my * Wv + mx : 0;
@@ -136,39 +167,56 @@ __global__ void __launch_bounds__(kLossThreads) ssim_adjoint_kernel(int H, int W
     for (int f = 0; f < 3; f++) sm[f][r][col] = in ? mc[f * plane + o] : 0.f;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < RH * kLossTW; q += kLossThreads) {  // out col x takes map cols x-10..x
-    const int r = q / kLossTW, col = q % kLossTW;
-    float a[3] = {0.f, 0.f, 0.f};
+  for (int q = threadIdx.x; q < kSsimR * (kSsimT / kSsimB); q += kLossThreads) {   // horizontal
+    const int r = q / (kSsimT / kSsimB), c0 = (q % (kSsimT / kSsimB)) * kSsimB;
 #pragma unroll
-    for (int v = 0; v < kWin; v++) {
-      const float w = win.w[v];
+    for (int f = 0; f < 3; f++) {
+      float v[kSsimB + kHalo];
 #pragma unroll
-      for (int f = 0; f < 3; f++) a[f] = fmaf(w, sm[f][r][col + kHalo - v], a[f]);
+      for (int u = 0; u < kSsimB + kHalo; u++) v[u] = sm[f][r][c0 + u];
+#pragma unroll
+      for (int o = 0; o < kSsimB; o++) {
+        float acc = 0.f;
+#pragma unroll
+        for (int u = 0; u < kWin; u++) acc = fmaf(win.w[kHalo - u], v[o + u], acc);
+        hs[f][r][c0 + o] = acc;
+      }
     }
-#pragma unroll
-    for (int f = 0; f < 3; f++) hs[f][r][col] = a[f];
   }
   __syncthreads();
   const float l1s = (1.f - lam) / (3.f * (float)H * (float)W);
   double asum = 0.0;
-  for (int q = threadIdx.x; q < kLossTH * kLossTW; q += kLossThreads) {
-    const int r = q / kLossTW, col = q % kLossTW;
-    const int gy = oy + r, gx = ox + col;
-    if (gy >= H || gx >= W) continue;
-    float a[3] = {0.f, 0.f, 0.f};
+  for (int q = threadIdx.x; q < kSsimT * (kSsimT / kSsimB); q += kLossThreads) {   // vertical + pixel terms
+    const int col = q % kSsimT, r0 = (q / kSsimT) * kSsimB;
+    float A[kSsimB][3];
 #pragma unroll
-    for (int u = 0; u < kWin; u++) {
-      const float w = win.w[u];
+    for (int o = 0; o < kSsimB; o++) { A[o][0] = 0.f; A[o][1] = 0.f; A[o][2] = 0.f; }
 #pragma unroll
-      for (int f = 0; f < 3; f++) a[f] = fmaf(w, hs[f][r + kHalo - u][col], a[f]);
+    for (int u = 0; u < kSsimB + kHalo; u++) {
+      const float h0 = hs[0][r0 + u][col], h1 = hs[1][r0 + u][col], h2 = hs[2][r0 + u][col];
+#pragma unroll
+      for (int o = 0; o < kSsimB; o++) {
+        const int t = u - o;
+        if (t >= 0 && t < kWin) {
+          const float w = win.w[kHalo - t];
+          A[o][0] = fmaf(w, h0, A[o][0]);
+          A[o][1] = fmaf(w, h1, A[o][1]);
+          A[o][2] = fmaf(w, h2, A[o][2]);
+        }
+      }
     }
-    const size_t p = ((size_t)gy * W + gx) * 3 + c;
-    const float x = img[p], y = tgt[p];
-    const float d_ssim = a[0] + 2.f * (x - 0.5f) * a[1] + (y - 0.5f) * a[2];
-    const float diff = x - y;
-    asum += fabsf(diff);
-    const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);   // np.sign
-    d_image[p] = l1s * sgn - 0.5f * lam * d_ssim;                       // losses.py:154
+#pragma unroll
+    for (int o = 0; o < kSsimB; o++) {
+      const int gy = oy + r0 + o, gx = ox + col;
+      if (gy >= H || gx >= W) continue;
+      const size_t p = ((size_t)gy * W + gx) * 3 + c;
+      const float x = img[p], y = tgt[p];
+      const float d_ssim = A[o][0] + 2.f * (x - 0.5f) * A[o][1] + (y - 0.5f) * A[o][2];
+      const float diff = x - y;
+      asum += fabsf(diff);
+      const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);   // np.sign
+      d_image[p] = l1s * sgn - 0.5f * lam * d_ssim;                       // losses.py:154
+    }
   }
   atomic_add_block_sum(stats + 0, asum);
 }
@@ -241,9 +289,9 @@ int launch_image_loss(int H, int W, const float *img, const float *tgt, const fl
   const int Hv = H - kHalo, Wv = W - kHalo;
   loss_stats_init_kernel<<<1, 1, 0, s>>>(stats, (double)Hv * (double)Wv);
   float *maps = static_cast<float *>(ws);
-  dim3 gv((Wv + kLossTW - 1) / kLossTW, (Hv + kLossTH - 1) / kLossTH, 3);
+  dim3 gv((Wv + kSsimT - 1) / kSsimT, (Hv + kSsimT - 1) / kSsimT, 3);
   ssim_moments_kernel<<<gv, kLossThreads, 0, s>>>(H, W, img, tgt, maps, stats, win);
-  dim3 gf((W + kLossTW - 1) / kLossTW, (H + kLossTH - 1) / kLossTH, 3);
+  dim3 gf((W + kSsimT - 1) / kSsimT, (H + kSsimT - 1) / kSsimT, 3);
   ssim_adjoint_kernel<<<gf, kLossThreads, 0, s>>>(H, W, img, tgt, maps, (float)lam, d_image, stats, win);
   if (n > 0) {
     const int blocks = (int)std::min<int64_t>((n + kLossThreads - 1) / kLossThreads, 148 * 8);
