@@ -321,46 +321,60 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    def fwd_step(ev):
-        ev[0].record(stream)
-        r.launch_forward(fr, 0, 0)
-        ev[1].record(stream)
-        r.launch_forward(fr, 1, 1)
-        ev[2].record(stream)
-        r.launch_forward(fr, 2, 2)
-        ev[3].record(stream)
+    # The C-ABI launches of a frame are captured once into CUDA graphs and
+    # replayed (stream-ordered device work only: no host sync inside a
+    # frame, so a graph is exactly the frame; replay removes the launch gaps
+    # between the ~15 kernels and memsets).  Whole-frame graphs give the
+    # headline times; per-stage graphs give the stage breakdown.
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
 
-    def fwdbwd_step(ev):
-        ev[0].record(stream)
+    def fwdbwd():
         r.launch_forward(fr, 0, 2)
-        ev[1].record(stream)
         r.launch_backward(fr, d_image, grads, 0, 0)
-        ev[2].record(stream)
         r.launch_backward(fr, d_image, grads, 1, 1, overwrite=True)   # fresh gradients, no zeroing pass
-        ev[3].record(stream)
 
-    def timed(step_fn, k):
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
+    torch.cuda.synchronize(dev)
+    g_fwd = capture(lambda: r.launch_forward(fr, 0, 2))
+    g_fstage = [capture(lambda k=k: r.launch_forward(fr, k, k)) for k in range(3)]
+    g_fb = capture(fwdbwd)
+    g_b0 = capture(lambda: r.launch_backward(fr, d_image, grads, 0, 0))
+    g_b1 = capture(lambda: r.launch_backward(fr, d_image, grads, 1, 1, overwrite=True))
+    torch.cuda.synchronize(dev)
+
+    def timed(graphs, k):
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(graphs) + 1)] for _ in range(k)]
         for i in range(k):
             flush.zero_()                          # untimed L2 flush between frames
-            step_fn(evs[i])
+            evs[i][0].record(stream)
+            for j, g in enumerate(graphs):
+                g.replay()
+                evs[i][j + 1].record(stream)
         torch.cuda.synchronize(dev)
-        stages = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(3)] for e in evs])
-        return stages                               # ms, [k, 3]
+        return np.array([[e[j].elapsed_time(e[j + 1]) for j in range(len(graphs))] for e in evs])   # ms
 
     for _ in range(args.warmup):
-        fwd_step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
-        fwdbwd_step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+        timed([g_fwd], 1)
+        timed(g_fstage, 1)
+        timed([g_fb], 1)
+        timed([g_fwd, g_b0, g_b1], 1)
     barrier()
     with ClockSampler(local) as clocks:
         barrier()
-        fwd = timed(fwd_step, args.steps)
+        fwd_whole = timed([g_fwd], args.steps)
         barrier()
-        fb = timed(fwdbwd_step, args.steps)
+        fwd = timed(g_fstage, args.steps)
+        barrier()
+        fb_whole = timed([g_fb], args.steps)
+        barrier()
+        fb = timed([g_fwd, g_b0, g_b1], args.steps)
         barrier()
     clock = clocks.summary()
-    fwd_ms_local = float(fwd.sum(axis=1).mean())
-    fb_ms_local = float(fb.sum(axis=1).mean())
+    fwd_ms_local = float(fwd_whole.sum(axis=1).mean())
+    fb_ms_local = float(fb_whole.sum(axis=1).mean())
     t = torch.tensor([fwd_ms_local, fb_ms_local], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -494,6 +508,7 @@ def main():
                                "DEPTH scaling, RenderSettings() defaults; each rank renders a replica view",
                    "convexes": n, "width": args.width, "height": args.height, "visible": V, "pairs": P,
                    "l2": "flushed before every timed step (512 MB write, untimed)",
+                   "launch": "CUDA graph replay of the frame's C-ABI launches (captured once)",
                    "parallelism": f"replicas x{world}"},
         "fwd_bwd_iters_per_s": world * 1000.0 / fb_ms, "fwd_bwd_ms": fb_ms,
         "stage_ms": {"preprocess": float(stage_ms[0]), "binning": float(stage_ms[1]), "blend": float(stage_ms[2]),
@@ -501,10 +516,12 @@ def main():
                      "backward_blend": float(bwd_ms[1]), "chain": float(bwd_ms[2])},
         "work": {k2: int(v) for k2, v in stats.items()},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clock, "train_step": train,
-        "gpu_launches": args.steps * launches_fwd + args.steps * (launches_fwd + 3),
+        # timed: whole-frame and per-stage graphs of the forward, then of fwd+bwd
+        "gpu_launches": 2 * args.steps * (launches_fwd + (launches_fwd + 3)),
         "gpu_launches_detail": f"{launches_fwd} per forward (1 preprocess, 6 depth order: key32 + offsets + "
                                f"3 onesweep + fix-up, 1 scan+duplicate, {1 + pp} pair sort, 1 ranges, 1 tile order, "
-                               f"1 blend), 3 per backward (accumulator zeroing, blend, chain)",
+                               f"1 blend), 3 per backward (accumulator zeroing, blend, chain); each timed "
+                               f"twice (whole-frame graph, per-stage graphs)",
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
