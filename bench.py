@@ -499,7 +499,7 @@ def main():
                           f"+ {cs_['tiles_sampled']}/{cs_['tiles_total']} random tiles, extrapolated"),
                "fwd_bwd_iters_per_s": 1.0 / cs_["fwd_bwd_frame_s"], "cpu": cpu_model(), "detail": cs_}
 
-    launches_fwd = 12 + pp
+    launches_fwd = 13 + pp
     line = {
         "metric": METRIC, "value": world * 1000.0 / fwd_ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": fwd_ms, "higher_is_better": True, "scaling": "weak",
@@ -518,7 +518,7 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clock, "train_step": train,
         # timed: whole-frame and per-stage graphs of the forward, then of fwd+bwd
         "gpu_launches": 2 * args.steps * (launches_fwd + (launches_fwd + 3)),
-        "gpu_launches_detail": f"{launches_fwd} per forward (1 preprocess, 6 depth order: key32 + offsets + "
+        "gpu_launches_detail": f"{launches_fwd} per forward (1 preprocess, 1 scratch clear, 6 depth order: key32 + offsets + "
                                f"3 onesweep + fix-up, 1 scan+duplicate, {1 + pp} pair sort, 1 ranges, 1 tile order, "
                                f"1 blend), 3 per backward (accumulator zeroing, blend, chain); each timed "
                                f"twice (whole-frame graph, per-stage graphs)",

@@ -655,6 +655,20 @@ size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, int tiles, Scratch
   return off;
 }
 
+struct ClearList {
+  uint2 *p[4];
+  uint64_t n[4];   // 8-byte words
+};
+__global__ void __launch_bounds__(256) clear_kernel(ClearList c) {
+  const uint64_t stride = (uint64_t)gridDim.x * 256;
+  uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    for (; i < c.n[r]; i += stride) c.p[r][i] = make_uint2(0u, 0u);
+    i -= c.n[r];
+  }
+}
+
 int pair_sort_passes(int tiles) {
   int bits = 0;
   while ((1 << bits) < tiles) bits++;
@@ -678,9 +692,18 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
   uint32_t *pids = reinterpret_cast<uint32_t *>(ws + L.pair_ids);
   uint2 *ranges = reinterpret_cast<uint2 *>(ws + L.tile_ranges);
 
-  cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 16 * kRadix, s);
-  cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * sc.lookback_words, s);
-  cudaMemsetAsync(ranges, 0, sizeof(uint2) * tiles, s);   // empty tiles (and n == 0) read (0, 0)
+  // one clearing kernel instead of four memsets: digit histograms, look-back
+  // flags, tile ranges (empty tiles and n == 0 read (0, 0)), scan block sums
+  const uint32_t dchunks = (n + kDupThreads * kDupRounds - 1) / (kDupThreads * kDupRounds);
+  {
+    ClearList cl;
+    cl.p[0] = reinterpret_cast<uint2 *>(sc.hist); cl.n[0] = sizeof(uint32_t) * 16 * kRadix / 8;
+    cl.p[1] = reinterpret_cast<uint2 *>(sc.lookback); cl.n[1] = sizeof(uint32_t) * sc.lookback_words / 8;
+    cl.p[2] = ranges; cl.n[2] = (uint64_t)tiles;
+    cl.p[3] = reinterpret_cast<uint2 *>(sc.block_sums); cl.n[3] = dchunks;
+    const uint64_t total = cl.n[0] + cl.n[1] + cl.n[2] + cl.n[3];
+    clear_kernel<<<(int)std::min<uint64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(cl);
+  }
   if (n > 0) {
     // depth order: 24-bit keys, 3 passes (odd: start in the alternate
     // buffers so the result ends in (keys32, order)), then the exact fix-up
@@ -695,8 +718,6 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
     // pairs land in the buffer that makes the sorted result end in (ptiles, pids)
     uint32_t *dt = (pp & 1) ? sc.ptiles_alt : ptiles;
     uint32_t *di = (pp & 1) ? sc.pids_alt : pids;
-    const uint32_t dchunks = (n + kDupThreads * kDupRounds - 1) / (kDupThreads * kDupRounds);
-    cudaMemsetAsync(sc.block_sums, 0, sizeof(uint64_t) * dchunks, s);
     duplicate_scan_kernel<<<dchunks, kDupThreads, 0, s>>>(
         order, touched, reinterpret_cast<const int4 *>(ws + L.bbox), n, (uint32_t)cap, L.tiles_x, pp, dt, di,
         sc.hist + 8 * kRadix, offs, reinterpret_cast<unsigned long long *>(sc.block_sums), counters + C_CHUNK0 + 6,
