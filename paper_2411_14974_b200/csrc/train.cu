@@ -72,20 +72,23 @@ __global__ void __launch_bounds__(kLossThreads) ssim_moments_kernel(int H, int W
   // horizontal: item = (row, 4-column group)
   for (int q = threadIdx.x; q < kSsimR * (kSsimT / kSsimB); q += kLossThreads) {
     const int r = q / (kSsimT / kSsimB), c0 = (q % (kSsimT / kSsimB)) * kSsimB;
-    float xv[kSsimB + kHalo], yv[kSsimB + kHalo];
+    float xv[kSsimB + kHalo], yv[kSsimB + kHalo], xx[kSsimB + kHalo], yy[kSsimB + kHalo], xy[kSsimB + kHalo];
 #pragma unroll
-    for (int u = 0; u < kSsimB + kHalo; u++) { xv[u] = sx[r][c0 + u]; yv[u] = sy[r][c0 + u]; }
+    for (int u = 0; u < kSsimB + kHalo; u++) {   // products once per input, not once per tap
+      xv[u] = sx[r][c0 + u]; yv[u] = sy[r][c0 + u];
+      xx[u] = xv[u] * xv[u]; yy[u] = yv[u] * yv[u]; xy[u] = xv[u] * yv[u];
+    }
 #pragma unroll
     for (int o = 0; o < kSsimB; o++) {
       float mx = 0.f, my = 0.f, vxx = 0.f, vyy = 0.f, vxy = 0.f;
 #pragma unroll
       for (int u = 0; u < kWin; u++) {
-        const float w = win.w[u], a = xv[o + u], b = yv[o + u];
-        mx = fmaf(w, a, mx);
-        my = fmaf(w, b, my);
-        vxx = fmaf(w, a * a, vxx);
-        vyy = fmaf(w, b * b, vyy);
-        vxy = fmaf(w, a * b, vxy);
+        const float w = win.w[u];
+        mx = fmaf(w, xv[o + u], mx);
+        my = fmaf(w, yv[o + u], my);
+        vxx = fmaf(w, xx[o + u], vxx);
+        vyy = fmaf(w, yy[o + u], vyy);
+        vxy = fmaf(w, xy[o + u], vxy);
       }
       hs[0][r][c0 + o] = mx; hs[1][r][c0 + o] = my; hs[2][r][c0 + o] = vxx; hs[3][r][c0 + o] = vyy;
       hs[4][r][c0 + o] = vxy;
@@ -131,9 +134,10 @@ __global__ void __launch_bounds__(kLossThreads) ssim_moments_kernel(int H, int W
       const float smap = a1 * a2 * inv;
       ssum += smap;
       // d smap / d (Mx, Vxx, Vxy) of the shifted statistics (same derivative
-      // as losses.py:86-94 in exact arithmetic)
-      const float dMx = 2.f * muy * a2 * inv - 2.f * mux * smap / b1 + 2.f * Mx * smap / b2 - 2.f * My * a1 * inv;
-      const float dVxx = -smap / b2;
+      // as losses.py:86-94 in exact arithmetic); 1/b1 = b2 inv, 1/b2 = b1 inv
+      const float sb1 = smap * (b2 * inv), sb2 = smap * (b1 * inv);
+      const float dMx = 2.f * muy * a2 * inv - 2.f * mux * sb1 + 2.f * Mx * sb2 - 2.f * My * a1 * inv;
+      const float dVxx = -sb2;
       const float dVxy = 2.f * a1 * inv;
       const size_t oo = (size_t)gy * Wv + gx;
       mc[oo] = scale * dMx;
