@@ -449,7 +449,16 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    mufu_peak = N_SMS * MUFU_PER_CLK_PER_SM * sm_max * 1e6 / 1e9          # Gop/s
+    mufu_peak = N_SMS * MUFU_PER_CLK_PER_SM * sm_max * 1e6 / 1e9          # Gop/s, derived
+    mufu_source = (f"derived: {N_SMS} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x {sm_max:.0f} MHz "
+                   "(sm_max_mhz of MEASURED_PEAKS.json)")
+    try:   # measured on a B200 by tools/mufu_peak.cu (ex2 throughput at the max SM clock)
+        mp = json.load(open(os.path.join(ROOT, "profiles", "mufu_peak.json")))
+        mufu_peak = float(mp["mufu_ex2_gops"]) * sm_max / float(mp["sm_clock_mhz"])
+        mufu_source = (f"measured: tools/mufu_peak.cu, {mp['mufu_ex2_gops']} Gop/s ex2 at {mp['sm_clock_mhz']} MHz "
+                       f"({mp['per_sm_per_clk']} per SM per clock; profiles/mufu_peak.json)")
+    except (OSError, ValueError, KeyError):
+        pass
     k = st.k
     pre_bytes = n * (k * 12 + 4 * 4 + 48 * 4) + n * (8 + 4 + 4) + V * (L.rec_floats * 4 + L.max_k + 16)
     bin_bytes = (n * 8 + 8 * n * 12 * 2            # depth sort: histogram + 8 passes of (key, id)
@@ -480,9 +489,7 @@ def main():
             traffic = None
     roofline = {"kernel": dominant, "bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
                 "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic,
-                "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if dom["bound"] == "hbm" else
-                                f"derived: {N_SMS} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x {sm_max:.0f} MHz "
-                                "(sm_max_mhz of MEASURED_PEAKS.json)"),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if dom["bound"] == "hbm" else mufu_source,
                 "stages": stage_info}
 
     # ---- config 5: view-sharded training step (B views, all_reduce of the gradients)
