@@ -37,7 +37,11 @@ struct ChainArgs {
   cs_view_signal sig;   // sigma_signal == nullptr: no densification signal
 };
 
+#ifdef CS_CHAIN_F64   // float64 geometry arrays: half the threads keep the static shared memory under 48 KB
+template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 64 : 32; }
+#else
 template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 128 : 64; }
+#endif
 
 // Accumulation into the caller's gradient buffers (+=, GradientBuffer.add).
 // Every convex has one owning thread, so these need no atomicity; they are
@@ -386,11 +390,11 @@ int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &
   a.g = g;
   a.sig = sig ? *sig : cs_view_signal{nullptr, nullptr, nullptr};
   if (L.max_k == 8) {
-    if (overwrite) chain_kernel<8, true><<<(int)((p.n + 127) / 128), chain_threads<8>(), 0, s>>>(a);
-    else chain_kernel<8, false><<<(int)((p.n + 127) / 128), chain_threads<8>(), 0, s>>>(a);
+    if (overwrite) chain_kernel<8, true><<<(int)((p.n + chain_threads<8>() - 1) / chain_threads<8>()), chain_threads<8>(), 0, s>>>(a);
+    else chain_kernel<8, false><<<(int)((p.n + chain_threads<8>() - 1) / chain_threads<8>()), chain_threads<8>(), 0, s>>>(a);
   } else {
-    if (overwrite) chain_kernel<16, true><<<(int)((p.n + 63) / 64), chain_threads<16>(), 0, s>>>(a);
-    else chain_kernel<16, false><<<(int)((p.n + 63) / 64), chain_threads<16>(), 0, s>>>(a);
+    if (overwrite) chain_kernel<16, true><<<(int)((p.n + chain_threads<16>() - 1) / chain_threads<16>()), chain_threads<16>(), 0, s>>>(a);
+    else chain_kernel<16, false><<<(int)((p.n + chain_threads<16>() - 1) / chain_threads<16>()), chain_threads<16>(), 0, s>>>(a);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
