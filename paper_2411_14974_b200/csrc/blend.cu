@@ -208,6 +208,7 @@ struct PipeSmem {
   static constexpr int kRing = kStages;
   float4 rec[kStages][kStageCands][Rec<MAXK>::kFloats / 4];
   uint32_t id[kStages][kStageCands];
+  uint8_t bmask[kStages][kStageCands];   // forward: 8x4 blocks that may reach the cutoff (bit = warp)
   uint32_t vis[kStages];
   uint64_t full[kStages];
   uint64_t empty[kStages];
@@ -229,10 +230,50 @@ __device__ __forceinline__ void flush_visible(PipeSmem<MAXK, kStages> &sm, int s
   __syncwarp();
 }
 
+// Forward block culling by the producer (otherwise idle between stage
+// fills): for candidate j and the tile's 8x4 block q, the LSE is at least the
+// largest line value, and each line's minimum over the block's pixel centres
+// is at a corner, so phi2 >= max_l min_corner z_l.  When even that bound
+// keeps o I below the cutoff at every pixel of the block -- sig * lb >
+// log2(o / cutoff - 1), with a margin far above the float32 evaluation's
+// error -- the block cannot blend the candidate and its warp skips it.
+struct BlockCull {
+  float qx0, qy0;   // pixel-centre coordinates of the tile's first pixel
+  float cutoff;
+};
+template <int MAXK>
+__device__ __forceinline__ uint32_t block_cull_mask(const float *rec, const BlockCull &bc) {
+  const float4 h0 = __ldg(reinterpret_cast<const float4 *>(rec)), h2 = __ldg(reinterpret_cast<const float4 *>(rec) + 2);
+  const int nl = min(__float_as_int(h2.z), MAXK);
+  const float thr = __log2f(h0.w / bc.cutoff - 1.f);
+  const float dx0 = bc.qx0 - h0.x, dy0 = bc.qy0 - h0.y;
+  float lb[8];
+#pragma unroll
+  for (int q = 0; q < 8; q++) lb[q] = -INFINITY;
+  for (int l = 0; l < nl; l++) {
+    const float A = __ldg(rec + R_HEADER + 3 * l), B = __ldg(rec + R_HEADER + 3 * l + 1),
+                C = __ldg(rec + R_HEADER + 3 * l + 2);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const float xl = dx0 + (float)((q & 1) * 8), yl = dy0 + (float)((q >> 1) * 4);
+      const float zx = fminf(A * xl, A * (xl + 7.f)), zy = fminf(B * yl, B * (yl + 3.f));
+      lb[q] = fmaxf(lb[q], C + zx + zy);
+    }
+  }
+  uint32_t m = 0xffu;
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    const float v = h0.z * lb[q];
+    if (v - thr > 1e-3f * (1.f + fabsf(thr) + fabsf(v))) m &= ~(1u << q);
+  }
+  return m;
+}
+
 // Producer warp: batch b covers pair indices first(b) .. first(b)+count(b)-1.
 template <int MAXK, int kStages, int NC, typename Batch>
 __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const float *records, const uint32_t *pair_ids,
-                                             int nbatch, Batch batch, bool forward, uint8_t *visible) {
+                                             int nbatch, Batch batch, bool forward, uint8_t *visible,
+                                             const BlockCull *cull = nullptr) {
   constexpr int RB = Rec<MAXK>::kFloats * 4;
   const int lane = threadIdx.x & 31;
   int issued = 0;
@@ -273,6 +314,10 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
       next_id = lane < (int)c1 ? __ldg(pair_ids + f1 + lane) : 0u;
     }
     if (lane < (int)count) sm.id[s][lane] = id;
+    if (cull)
+      sm.bmask[s][lane] = (uint8_t)(lane < (int)count ? block_cull_mask<MAXK>(records + (size_t)id * Rec<MAXK>::kFloats,
+                                                                              *cull)
+                                                       : 0xffu);
     __syncwarp();
 #ifdef CS_PRODUCER_TMA
     if (lane == 0) mbar_expect_tx(&sm.full[s], count * RB);
@@ -382,11 +427,18 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
   pipe_init<MAXK, kStages, NC>(sm);
   unsigned n_eval = 0, n_lines = 0, n_blend = 0, n_warp_evals = 0;
   if (warp == NC) {
+#ifndef CS_NO_BLOCK_CULL
+    const BlockCull bc{(float)(tx * kTile) + 0.5f, (float)(ty * kTile) + 0.5f, a.cutoff};
+    const bool cull = NC == 8 && a.cutoff > 0.f;
+#else
+    const BlockCull bc{0.f, 0.f, 0.f};
+    const bool cull = false;
+#endif
     pipe_produce<MAXK, kStages, NC>(sm, a.records, a.pair_ids, nbatch,
                        [&](int b, uint32_t &first, uint32_t &count) {
                          first = range.x + (uint32_t)b * kStageCands;
                          count = min((uint32_t)kStageCands, range.y - first);
-                       }, true, a.visible);
+                       }, true, a.visible, cull ? &bc : nullptr);
   } else {
     int lx, ly;
     tile_pixel(threadIdx.x, lx, ly);
@@ -411,7 +463,12 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
         const int count = (int)min((uint32_t)kStageCands, range.y - first);
         // lane j: pixels of this warp's block inside candidate j's bbox and alive
         const uint32_t alive = __ballot_sync(0xffffffffu, !P.done);
-        const uint32_t pm = lane < count ? block_mask(rec_bbox(sm.rec[s][lane]), rx0, ry0) & alive : 0u;
+#ifndef CS_NO_BLOCK_CULL
+        const bool may = NC != 8 || !(a.cutoff > 0.f) || ((sm.bmask[s][lane] >> warp) & 1u);
+#else
+        const bool may = true;
+#endif
+        const uint32_t pm = lane < count && may ? block_mask(rec_bbox(sm.rec[s][lane]), rx0, ry0) & alive : 0u;
         uint32_t m = __ballot_sync(0xffffffffu, pm != 0u);
         uint32_t vis = 0;
         while (m) {
