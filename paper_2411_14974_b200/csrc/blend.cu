@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
   if (warp == NC) {
 #ifndef CS_NO_BLOCK_CULL
     const BlockCull bc{(float)(tx * kTile) + 0.5f, (float)(ty * kTile) + 0.5f, a.cutoff};
-    const bool cull = NC == 8 && a.cutoff > 0.f;
+    // (a counting run evaluates every candidate: its work counts are the
+    // algorithmic E_fwd of the roofline accounting)
+    const bool cull = !STATS && NC == 8 && a.cutoff > 0.f;
 #else
     const BlockCull bc{0.f, 0.f, 0.f};
     const bool cull = false;
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
         // lane j: pixels of this warp's block inside candidate j's bbox and alive
         const uint32_t alive = __ballot_sync(0xffffffffu, !P.done);
 #ifndef CS_NO_BLOCK_CULL
-        const bool may = NC != 8 || !(a.cutoff > 0.f) || ((sm.bmask[s][lane] >> warp) & 1u);
+        const bool may = STATS || NC != 8 || !(a.cutoff > 0.f) || ((sm.bmask[s][lane] >> warp) & 1u);
 #else
         const bool may = true;
 #endif
