@@ -395,11 +395,10 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_scan_kernel(
       ty0 = b.z / kTile;
       wdt = (b.y - 1) / kTile - tx0 + 1;
       inv_wdt = 1.f / (float)wdt;
-      if (off64 + cnt[k] <= cap) {   // digit histograms of the pairs that will be sorted
+      if (passes > 1 && off64 + cnt[k] <= cap) {   // higher-digit histograms, per run of equal digits
         const int ty1 = (b.w - 1) / kTile;
         for (int ty = ty0; ty <= ty1; ty++) {
           const uint32_t t0 = (uint32_t)(ty * tiles_x + tx0), t1 = t0 + (uint32_t)wdt - 1;
-          for (uint32_t tt = t0; tt <= t1; tt++) atomicAdd(&s_h[0][tt & (kRadix - 1)], 1u);
           for (int ps = 1; ps < passes; ps++) {
             const int sh = ps * kRadixBits;
             uint32_t seg = t0;
@@ -436,8 +435,12 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_scan_kernel(
       const uint32_t owner_id = __shfl_sync(0xffffffffu, id[k], lo);
       const uint64_t pos = wbase + p;
       if (p < wtotal && pos < cap) {
-        pair_tiles[pos] = (uint32_t)(ty * tiles_x + tx);
+        const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
+        pair_tiles[pos] = tile;
         pair_ids[pos] = owner_id;
+        // low-digit histogram here, one pair per lane (a per-convex loop
+        // over its tiles diverged across the warp)
+        atomicAdd(&s_h[0][tile & (kRadix - 1)], 1u);
       }
     }
   }
