@@ -199,6 +199,18 @@ __global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(Pa
   }
   const uint32_t dex = block_exclusive_scan256(sum, s_warp);
   if (owner) s_dexcl[d] = dex;
+  __syncthreads();
+  // local scatter into digit order first: the predecessors' prefixes get
+  // the scatter's time to appear before the look-back reads them
+#pragma unroll
+  for (int i = 0; i < kSortItems; i++) {
+    const uint32_t dd = dig[i];
+    if (dd < kRadix) {
+      const uint32_t pos = s_dexcl[dd] + s_hist[w][dd] + rank[i];
+      s_keys[pos] = key[i];
+      s_vals[pos] = val[i];
+    }
+  }
   uint32_t excl = 0;
   if (owner && chunk > 0) {
     // windowed decoupled look-back: kLookback independent loads per round, so
@@ -226,16 +238,6 @@ __global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(Pa
     lb[chunk * kRadix + d] = kFlagPrefix | (excl + sum);
   }
   if (owner) s_base[d] = a.offsets[d] + excl;
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < kSortItems; i++) {
-    const uint32_t dd = dig[i];
-    if (dd < kRadix) {
-      const uint32_t pos = s_dexcl[dd] + s_hist[w][dd] + rank[i];
-      s_keys[pos] = key[i];
-      s_vals[pos] = val[i];
-    }
-  }
   __syncthreads();
   for (uint32_t q = t; q < nvalid; q += kSortThreads) {
     const KeyT kk = s_keys[q];
