@@ -215,8 +215,13 @@ __global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(Pa
   if (owner && chunk > 0) {
     // windowed decoupled look-back: kLookback independent loads per round, so
     // the walk over not-yet-resolved predecessors costs one L2 round trip per
-    // kLookback chunks instead of one per chunk
-    constexpr int kLookback = 16;
+    // kLookback chunks instead of one per chunk (4: wider windows re-read
+    // more unpublished entries; binning 4 / 8 / 16 / 32: 243 / 243 / 251 /
+    // 264 us)
+#ifndef CS_LOOKBACK
+#define CS_LOOKBACK 4
+#endif
+    constexpr int kLookback = CS_LOOKBACK;
     int c = (int)chunk - 1;
     bool done = false;
     while (!done) {
