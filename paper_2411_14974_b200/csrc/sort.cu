@@ -295,7 +295,10 @@ static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uin
 // The 8-bit digit histograms of the tile keys for the pair sort are
 // accumulated on the way (shared-memory atomics, one global add per bin).
 constexpr int kDupThreads = 256;
-constexpr int kDupRounds = 4;   // ranks per block = kDupRounds * kDupThreads (fewer histogram flushes)
+#ifndef CS_DUP_ROUNDS
+#define CS_DUP_ROUNDS 4
+#endif
+constexpr int kDupRounds = CS_DUP_ROUNDS;   // ranks per block = kDupRounds * kDupThreads (fewer histogram flushes)
 
 // Fused scan + duplicate: every block takes the next 1024 depth ranks (a
 // dynamic chunk id, so predecessors are always resident), sums their tile
@@ -655,7 +658,7 @@ size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, int tiles, Scratch
   char *p4 = take(sizeof(uint32_t) * 16 * kRadix);
   char *p5 = take(sizeof(uint32_t) * 16 * kRadix);
   char *p6 = take(sizeof(uint32_t) * lb_words);
-  char *p7 = take(sizeof(uint64_t) * ((n + 1023) / 1024 + 2));   // duplicate-scan look-back
+  char *p7 = take(sizeof(uint64_t) * ((n + kDupThreads * kDupRounds - 1) / (kDupThreads * kDupRounds) + 2));   // duplicate-scan look-back
   if (sc) {
     sc->dkeys_alt = (uint64_t *)p0; sc->dvals_alt = (uint32_t *)p1;
     sc->ptiles_alt = (uint32_t *)p2; sc->pids_alt = (uint32_t *)p3;
