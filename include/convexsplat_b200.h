@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 6
+#define CS_ABI_VERSION 7
 
 #if defined(__GNUC__)
 #define CS_API __attribute__((visibility("default")))
@@ -42,7 +42,8 @@ enum cs_status {
     CS_ERR_ARG = 1,           /* bad argument (null pointer, K out of range, bad sizes) */
     CS_ERR_CUDA = 2,          /* a kernel launch failed (cudaGetLastError) */
     CS_ERR_WORKSPACE = 3,     /* workspace smaller than cs_workspace_size() */
-    CS_ERR_UNSUPPORTED = 4    /* tile size other than 16, sh_degree outside 0..3 */
+    CS_ERR_NONFINITE = 4,     /* a gradient row came out inf/NaN (cs_read_status) */
+    CS_ERR_UNSUPPORTED = 5    /* tile size other than 16, sh_degree outside 0..3 */
 };
 
 /* Scaling of delta/sigma with depth: ScalingMode (field.py:17-23). */
@@ -182,6 +183,27 @@ CS_API int cs_forward_ex(const cs_camera *cam, const cs_settings *set, const cs_
 
 /* Convenience: copy counters[0..3] to host (synchronises `stream`). */
 CS_API int cs_read_counters(const void *workspace, uint32_t *host_out4, void *stream);
+
+/* Status of the last frame in this workspace (synchronises `stream`):
+ * CS_ERR_NONFINITE if the last backward's chain stage produced an inf/NaN
+ * gradient row (the values are still written, as the reference's NumPy
+ * backward would return them; trainer.py:172-173 is where the reference
+ * reacts to non-finite values), CS_ERR_WORKSPACE if the last forward's
+ * pairs overflowed the capacity, else CS_OK. */
+CS_API int cs_read_status(const void *workspace, void *stream);
+
+/* Blend decisions of a frame (diagnostics: the decision-forced parity check
+ * of the float64 oracle, tests/).  Re-runs stage 2 of cs_forward on a
+ * workspace whose stages 0..1 ran, with the same kernel the forward uses,
+ * and also writes, for every pixel p (row-major), the pair indices (into
+ * the sorted tile lists) of the candidates it blended, in blend order, to
+ * positions[offsets[p] .. offsets[p] + frame->count[p]).  offsets [H*W]
+ * int64 is the exclusive scan of the count of a previous cs_forward of the
+ * same inputs (the blend is deterministic).  No reference counterpart: the
+ * reference re-decides every blend in float64 (rasterize.py:194-195). */
+CS_API int cs_forward_record(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                             void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                             const cs_frame *frame, const int64_t *offsets, int32_t *positions, void *stream);
 
 /* Batched 2-D hull.  Replaces projection.graham_scan (projection.py:47-113)
  * on m point sets of up to npts (<= 32) float64 points: pts [m,npts,2],

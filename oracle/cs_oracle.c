@@ -457,10 +457,21 @@ typedef struct {
     int64_t n_blend;     /* pairs blended */
 } or_frame;
 
-/* rasterize.py:178-204 for one tile. */
+/* Decisions of another implementation to follow instead of re-deciding
+ * them (the decision-forced check): pixel p blended the pair indices
+ * pos[off[p] .. off[p+1]) in that order, and channel c of its C + T*bg lay
+ * in [0,1] iff bit c of clamp[p].  NULL = decide as the reference does. */
+typedef struct {
+    const int64_t *off;     /* [H*W+1] */
+    const int32_t *pos;     /* [off[H*W]] pair indices into items */
+    const uint8_t *clamp;   /* [H*W] or NULL */
+} or_forced;
+
+/* rasterize.py:178-204 for one tile (with `fd`: the blend decisions of fd
+ * instead of the predicates of rasterize.py:194-195). */
 static void render_tile(const or_camera *cam, const or_settings *st, const or_view *V,
                         const int64_t *tile_off, const int32_t *items, int64_t t, or_frame *F,
-                        int64_t *ne, int64_t *nb) {
+                        int64_t *ne, int64_t *nb, const or_forced *fd, int64_t *cur) {
     const int W = cam->width, H = cam->height, ts = st->tile, k = V->k;
     const int tx_n = (W + ts - 1) / ts;
     const double cut = st->cutoff, flo = st->floor;
@@ -483,13 +494,18 @@ static void render_tile(const or_camera *cam, const or_settings *st, const or_vi
             for (int x = x0; x < x1; x++) {
                 size_t p = (size_t)y * W + x;
                 double T = F->trans[p];
-                if (flo > 0.0 && !(T >= flo)) continue;   /* dead pixel: blend predicate false */
+                if (fd) {
+                    if (!(cur[p] < fd->off[p + 1] && fd->pos[cur[p]] == e)) continue;
+                    cur[p]++;
+                } else if (flo > 0.0 && !(T >= flo)) {
+                    continue;   /* dead pixel: blend predicate false */
+                }
                 double phi, ind;
                 field_at(nrm, off, h, ds, ss, x + 0.5, y + 0.5, dist, &phi, &ind);
                 (*ne)++;
                 double a = o * ind;
                 if (a > OR_ALPHA_MAX) a = OR_ALPHA_MAX;
-                if (!(a >= cut)) continue;
+                if (!fd && !(a >= cut)) continue;
                 double w = T * a;
                 F->image[3 * p] += w * col[0];
                 F->image[3 * p + 1] += w * col[1];
@@ -509,10 +525,27 @@ static void render_tile(const or_camera *cam, const or_settings *st, const or_vi
 /* rasterize.py:156-209.  The frame buffers must be zeroed by the caller;
  * trans is initialised here.  tiles [t_begin, t_end) only (bounded CPU
  * samples); the background composite/clip runs over those tiles' pixels. */
+int or_render_forced(const or_camera *cam, const or_settings *st, const or_view *V, const int64_t *tile_off,
+                     const int32_t *items, int64_t t_begin, int64_t t_end, const int64_t *tile_list,
+                     const or_forced *fd, or_frame *F);
+
 int or_render(const or_camera *cam, const or_settings *st, const or_view *V, const int64_t *tile_off,
               const int32_t *items, int64_t t_begin, int64_t t_end, const int64_t *tile_list, or_frame *F) {
+    return or_render_forced(cam, st, V, tile_off, items, t_begin, t_end, tile_list, NULL, F);
+}
+
+/* or_render with the blend decisions of `fd` (NULL: the reference's own). */
+int or_render_forced(const or_camera *cam, const or_settings *st, const or_view *V, const int64_t *tile_off,
+                     const int32_t *items, int64_t t_begin, int64_t t_end, const int64_t *tile_list,
+                     const or_forced *fd, or_frame *F) {
     const int W = cam->width, H = cam->height, ts = st->tile;
     const int tx_n = (W + ts - 1) / ts;
+    int64_t *cur = NULL;
+    if (fd) {
+        cur = malloc(sizeof(int64_t) * (size_t)W * H);
+        if (!cur) return 1;
+        memcpy(cur, fd->off, sizeof(int64_t) * (size_t)W * H);
+    }
     for (size_t p = 0; p < (size_t)W * H; p++) F->trans[p] = 1.0;
     int64_t ne = 0, nb = 0;
 #ifdef _OPENMP
@@ -520,7 +553,7 @@ int or_render(const or_camera *cam, const or_settings *st, const or_view *V, con
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : ne, nb) num_threads(nt)
 #endif
     for (int64_t q = t_begin; q < t_end; q++)
-        render_tile(cam, st, V, tile_off, items, tile_list ? tile_list[q] : q, F, &ne, &nb);
+        render_tile(cam, st, V, tile_off, items, tile_list ? tile_list[q] : q, F, &ne, &nb, fd, cur);
     F->n_eval = ne;
     F->n_blend = nb;
     /* rasterize.py:206-209 */
@@ -536,6 +569,7 @@ int or_render(const or_camera *cam, const or_settings *st, const or_view *V, con
                 }
             }
     }
+    free(cur);
     return 0;
 }
 
@@ -562,10 +596,13 @@ typedef struct {
 #define OR_ACC(dst, v) ((dst) += (v))
 #endif
 
-/* backward.py:110-205 for one tile */
+/* backward.py:110-205 for one tile.  With `fd`, the blend predicate of
+ * rasterize.py:194-195 / backward.py:146-150 and the clip test of
+ * backward.py:154-158 are replaced by fd's recorded decisions; everything
+ * else (field, transmittance, gradients) is recomputed in float64. */
 static void backward_tile(const or_camera *cam, const or_settings *st, const or_view *V,
                           const int64_t *tile_off, const int32_t *items, int64_t t, const double *d_image,
-                          or_screen *S, uint8_t *visible, int64_t *ne) {
+                          or_screen *S, uint8_t *visible, int64_t *ne, const or_forced *fd) {
     const int W = cam->width, H = cam->height, ts = st->tile, k = V->k;
     const int tx_n = (W + ts - 1) / ts;
     const double cut = st->cutoff, flo = st->floor;
@@ -575,10 +612,12 @@ static void backward_tile(const or_camera *cam, const or_settings *st, const or_
     int th = ty1 - ty0, tw = tx1 - tx0;
     double T[256 * 4], cpre[256 * 4 * 3], S3[256 * 4 * 3], g[256 * 4 * 3];
     int last[256 * 4];
+    int64_t cur[256 * 4];   /* forced: next recorded decision of the pixel */
     if (th * tw > 256 * 4) return;  /* tile sizes above 32x32 unsupported by the oracle */
     for (int p = 0; p < th * tw; p++) {
         T[p] = 1.0; last[p] = -1;
         cpre[3 * p] = cpre[3 * p + 1] = cpre[3 * p + 2] = 0.0;
+        if (fd) cur[p] = fd->off[(size_t)(ty0 + p / tw) * W + tx0 + p % tw];
     }
     double dist[OR_MAXPTS], wts[OR_MAXPTS];
     int64_t e0 = tile_off[t], e1 = tile_off[t + 1];
@@ -600,7 +639,14 @@ static void backward_tile(const or_camera *cam, const or_settings *st, const or_
             field_at(nrm, off, h, ds, ss, x + 0.5, y + 0.5, dist, &phi, &ind);
             double a = o * ind;
             if (a > OR_ALPHA_MAX) a = OR_ALPHA_MAX;
-            int blend = (flo > 0.0) ? (T[p] >= flo && a >= cut) : (a >= cut);
+            int blend;
+            if (fd) {
+                const size_t pix = (size_t)y * W + x;
+                blend = cur[p] < fd->off[pix + 1] && fd->pos[cur[p]] == e;
+                if (blend) cur[p]++;
+            } else {
+                blend = (flo > 0.0) ? (T[p] >= flo && a >= cut) : (a >= cut);
+            }
             if (!blend) continue;
             double w = T[p] * a;
             for (int c = 0; c < 3; c++) cpre[3 * p + c] += w * col[c];
@@ -613,9 +659,11 @@ static void backward_tile(const or_camera *cam, const or_settings *st, const or_
     /* backward.py:154-162 */
     for (int p = 0; p < th * tw; p++) {
         int y = ty0 + p / tw, x = tx0 + p % tw;
+        if (fd) cur[p] = fd->off[(size_t)y * W + x + 1] - 1;   /* reverse cursor */
         for (int c = 0; c < 3; c++) {
             double v = cpre[3 * p + c] + T[p] * st->background[c];
             int inside = (v >= 0.0) && (v <= 1.0);
+            if (fd && fd->clamp) inside = (fd->clamp[(size_t)y * W + x] >> c) & 1;
             g[3 * p + c] = inside ? d_image[((size_t)y * W + x) * 3 + c] : 0.0;
             S3[3 * p + c] = T[p] * st->background[c];
         }
@@ -643,7 +691,13 @@ static void backward_tile(const or_camera *cam, const or_settings *st, const or_
             (*ne)++;
             double a_raw = o * ind;
             double a = a_raw < OR_ALPHA_MAX ? a_raw : OR_ALPHA_MAX;
-            if (!(a >= cut)) continue;
+            if (fd) {
+                const size_t pix = (size_t)y * W + x;
+                if (!(cur[p] >= fd->off[pix] && fd->pos[cur[p]] == e)) continue;
+                cur[p]--;
+            } else if (!(a >= cut)) {
+                continue;
+            }
             touched = 1;
             double om = 1.0 - a;
             double tp = T[p] / om;
@@ -780,9 +834,20 @@ static void chain_one(const or_camera *cam, const or_settings *st, const or_para
 
 /* backward.py:76-212.  Gradient buffers must be zeroed by the caller
  * (accumulation semantics of GradientBuffer.add, backward.py:65-73). */
+int or_backward_forced(const or_camera *cam, const or_settings *st, const or_params *P, const or_view *V,
+                       const int64_t *tile_off, const int32_t *items, const double *d_image,
+                       const int64_t *tile_list, int64_t n_list, const or_forced *fd, or_grads *G);
+
 int or_backward(const or_camera *cam, const or_settings *st, const or_params *P, const or_view *V,
                 const int64_t *tile_off, const int32_t *items, const double *d_image, const int64_t *tile_list,
                 int64_t n_list, or_grads *G) {
+    return or_backward_forced(cam, st, P, V, tile_off, items, d_image, tile_list, n_list, NULL, G);
+}
+
+/* or_backward with the blend / clip decisions of `fd` (NULL: the reference's own). */
+int or_backward_forced(const or_camera *cam, const or_settings *st, const or_params *P, const or_view *V,
+                       const int64_t *tile_off, const int32_t *items, const double *d_image,
+                       const int64_t *tile_list, int64_t n_list, const or_forced *fd, or_grads *G) {
     const int W = cam->width, H = cam->height, ts = st->tile, k = V->k;
     const int64_t T = (int64_t)((W + ts - 1) / ts) * ((H + ts - 1) / ts);
     const int nv = V->n_visible;
@@ -801,7 +866,7 @@ int or_backward(const or_camera *cam, const or_settings *st, const or_params *P,
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : ne) num_threads(nt)
 #endif
     for (int64_t q = 0; q < nt_list; q++)
-        backward_tile(cam, st, V, tile_off, items, tile_list ? tile_list[q] : q, d_image, &S, G->visible, &ne);
+        backward_tile(cam, st, V, tile_off, items, tile_list ? tile_list[q] : q, d_image, &S, G->visible, &ne, fd);
     G->n_eval = ne;
 #ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic, 256) num_threads(nt)
@@ -812,6 +877,55 @@ int or_backward(const or_camera *cam, const or_settings *st, const or_params *P,
 }
 
 int or_max_points(void) { return OR_MAXPTS; }
+
+/* The reference's own blend decisions (rasterize.py:178-204), in the format
+ * of or_forced: with pos == NULL, writes counts[p] (blends of pixel p); with
+ * pos, writes pixel p's blended pair indices at pos[off[p] ...] in blend
+ * order (off = exclusive scan of the counts). */
+int or_blend_decisions(const or_camera *cam, const or_settings *st, const or_view *V, const int64_t *tile_off,
+                       const int32_t *items, int64_t *counts_or_off, int32_t *pos) {
+    const int W = cam->width, H = cam->height, ts = st->tile, k = V->k;
+    const int tx_n = (W + ts - 1) / ts, ty_n = (H + ts - 1) / ts;
+    double dist[OR_MAXPTS];
+    double *T = malloc(sizeof(double) * (size_t)W * H);
+    int64_t *cur = malloc(sizeof(int64_t) * (size_t)W * H);
+    if (!T || !cur) { free(T); free(cur); return 1; }
+    for (size_t p = 0; p < (size_t)W * H; p++) {
+        T[p] = 1.0;
+        cur[p] = pos ? counts_or_off[p] : 0;
+    }
+    for (int64_t t = 0; t < (int64_t)tx_n * ty_n; t++) {
+        int ty = (int)(t / tx_n), tx = (int)(t % tx_n);
+        int ty0 = ty * ts, ty1 = ty0 + ts < H ? ty0 + ts : H;
+        int tx0 = tx * ts, tx1 = tx0 + ts < W ? tx0 + ts : W;
+        for (int64_t e = tile_off[t]; e < tile_off[t + 1]; e++) {
+            int i = V->order[items[e]];
+            const int32_t *bb = V->bbox + 4 * i;
+            int y0 = bb[2] > ty0 ? bb[2] : ty0, y1 = bb[3] < ty1 ? bb[3] : ty1;
+            int x0 = bb[0] > tx0 ? bb[0] : tx0, x1 = bb[1] < tx1 ? bb[1] : tx1;
+            const double *nrm = V->normals + (size_t)i * k * 2, *off = V->offsets + (size_t)i * k;
+            for (int y = y0; y < y1; y++)
+                for (int x = x0; x < x1; x++) {
+                    size_t p = (size_t)y * W + x;
+                    if (st->floor > 0.0 && !(T[p] >= st->floor)) continue;
+                    double phi, ind;
+                    field_at(nrm, off, V->hull_n[i], V->delta_s[i], V->sigma_s[i], x + 0.5, y + 0.5, dist, &phi,
+                             &ind);
+                    double a = V->opacity[i] * ind;
+                    if (a > OR_ALPHA_MAX) a = OR_ALPHA_MAX;
+                    if (!(a >= st->cutoff)) continue;
+                    T[p] *= 1.0 - a;
+                    if (pos) pos[cur[p]] = (int32_t)e;
+                    cur[p]++;
+                }
+        }
+    }
+    if (!pos)
+        for (size_t p = 0; p < (size_t)W * H; p++) counts_or_off[p] = cur[p];
+    free(T);
+    free(cur);
+    return 0;
+}
 
 /* Analysis helper (test/tooling only): for each listed tile, the 256-bit
  * mask (bit = ly*16+lx) of pixels that EVALUATE each candidate of the tile

@@ -14,8 +14,12 @@ LIB_PATH = os.path.join(_HERE, "libconvexsplat_sm100.so")
 EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forward", "cs_backward",
            "cs_forward_stages", "cs_forward_ex", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
            "cs_backward_signal", "cs_backward_ex", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step",
-           "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags", "cs_density_scatter")
-ABI_VERSION = 6
+           "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags", "cs_density_scatter",
+           "cs_read_status", "cs_forward_record")
+ABI_VERSION = 7
+ERR_WORKSPACE = 3     # CS_ERR_WORKSPACE
+ERR_NONFINITE = 4     # CS_ERR_NONFINITE
+ERR_UNSUPPORTED = 5   # CS_ERR_UNSUPPORTED
 GRADS_OVERWRITE = 1   # CS_GRADS_OVERWRITE
 WORK_COUNTERS = 2     # CS_WORK_COUNTERS
 
@@ -113,6 +117,8 @@ def load(path: str = None):
     L.cs_forward_ex.argtypes = L.cs_forward.argtypes[:-1] + [ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, _vp]
     L.cs_backward_stages.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.c_int32, ctypes.c_int32, _vp]
     L.cs_read_counters.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), _vp]
+    L.cs_read_status.argtypes = [_vp, _vp]
+    L.cs_forward_record.argtypes = L.cs_forward.argtypes[:-1] + [_vp, _vp, _vp]
     L.cs_graham_scan_batch.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]
     L.cs_backward_signal.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.POINTER(CsViewSignal), _vp]
     L.cs_backward_ex.argtypes = L.cs_backward.argtypes[:-1] + [ctypes.POINTER(CsViewSignal), ctypes.c_uint32,
@@ -135,7 +141,7 @@ def load(path: str = None):
                "cs_read_counters", "cs_graham_scan_batch", "cs_backward_signal", "cs_backward_ex",
                "cs_image_loss_workspace",
                "cs_image_loss", "cs_adam_step", "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags",
-               "cs_density_scatter"):
+               "cs_density_scatter", "cs_read_status", "cs_forward_record"):
         getattr(L, fn).restype = ctypes.c_int
     if L.cs_abi_version() != ABI_VERSION:
         raise CsError(f"ABI mismatch: library {L.cs_abi_version()} != {ABI_VERSION}")

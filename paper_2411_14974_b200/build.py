@@ -23,7 +23,9 @@ SOURCES = ["preprocess.cu", "sort.cu", "blend.cu", "chain.cu", "train.cu", "scen
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
-PER_FILE = {"preprocess.cu": ["--fmad=false"]}
+# scene_ops.cu: the split / prune decisions follow density.py's float64
+# arithmetic (no contraction of p + s*(p - c) or dx*dx + dy*dy into FMAs)
+PER_FILE = {"preprocess.cu": ["--fmad=false"], "scene_ops.cu": ["--fmad=false"]}
 
 
 def nvcc() -> str:

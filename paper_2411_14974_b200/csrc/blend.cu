@@ -46,7 +46,7 @@ struct BlendArgs {
   uint8_t *pixel_clamp;
   // backward
   const float *d_image;
-  float *accum;
+  AccT *accum;
   unsigned long long *stats;
   // blend masks: word (range.x / 32 + tile + b) of array q = which of the
   // 32 candidates of forward batch b some pixel of the tile's 8x4 block q
@@ -54,6 +54,10 @@ struct BlendArgs {
   // skips the others
   uint32_t *blend_mask;
   uint32_t mask_words;
+  // decision record (forward, REC instantiation only): pixel p's blended
+  // pair indices, in blend order, at rec_pos[rec_off[p] ...]
+  const int64_t *rec_off;
+  int32_t *rec_pos;
 };
 
 struct Eval {
@@ -407,8 +411,9 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float qx, float
   return true;
 }
 
-// Forward blend (rasterize.py:178-209), one 16x16 tile per block.
-template <int MAXK, bool STATS>
+// Forward blend (rasterize.py:178-209), one 16x16 tile per block.  REC:
+// also record every blend decision (diagnostics, cs_forward_record).
+template <int MAXK, bool STATS, bool REC = false>
 #ifndef CS_FWD_MINB
 #define CS_FWD_MINB (CS_FWD_NC == 8 ? 4 : 7)
 #endif
@@ -449,6 +454,8 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
     const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2) + half * 8;
     const bool inside = px < a.width && py < a.height;
     const float qx = px + 0.5f, qy = py + 0.5f;
+    int32_t *rec_dst = nullptr;
+    if (REC && inside) rec_dst = a.rec_pos + a.rec_off[(size_t)py * a.width + px];
     FwdPixel P;
     P.T = 1.f; P.C0 = P.C1 = P.C2 = P.W = P.D = 0.f;
     P.last = -1; P.nblend = 0;
@@ -498,6 +505,7 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
             } else {
               blended = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
             }
+            if (REC && blended) rec_dst[P.nblend - 1] = pos;
           }
           if (__any_sync(0xffffffffu, blended)) {
             vis |= 1u << j;
@@ -692,7 +700,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
     first = (uint32_t)lo;
     count = (uint32_t)(hi - lo);
   };
-  unsigned n_eval = 0, n_lines = 0, n_warp_evals = 0;
+  unsigned n_eval = 0, n_lines = 0, n_warp_evals = 0, n_bblend = 0;
   if (warp == NC) {
     pipe_produce<MAXK, kStages, NC>(sm, a.records, a.pair_ids, nbatch, batch, false, nullptr);
   } else {
@@ -748,8 +756,11 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           }
           bool contrib = false;
 #define CS_BWD2_PX(NLV, H)                                                                       \
-  if (H < PPL && act[H % PPL])                                                                     \
-    contrib |= bwd_candidate<NLV, MAXK, STATS>(rec, qx[H % PPL], qy[H % PPL], a.cutoff, P[H % PPL], v, n_lines);
+  if (H < PPL && act[H % PPL]) {                                                                   \
+    const bool c_ = bwd_candidate<NLV, MAXK, STATS>(rec, qx[H % PPL], qy[H % PPL], a.cutoff, P[H % PPL], v, n_lines); \
+    contrib |= c_;                                                                                 \
+    if (STATS) n_bblend += (unsigned)c_;                                                           \
+  }
 #define CS_BWD2_CASE(NLV) CS_BWD2_PX(NLV, 0) CS_BWD2_PX(NLV, 1) CS_BWD2_PX(NLV, 2) CS_BWD2_PX(NLV, 3)
           if (MAXK == 8) {
             const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
@@ -764,13 +775,13 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
 #undef CS_BWD2_PX
           if (STATS) n_warp_evals += __any_sync(0xffffffffu, any_act) ? 1u : 0u;
           if (__any_sync(0xffffffffu, contrib)) {
-            float *dst = a.accum + (size_t)sm.id[s][j] * AF;
+            AccT *dst = a.accum + (size_t)sm.id[s][j] * AF;
 #pragma unroll
             for (int gi = 0; gi < NG; gi++) {
               float (&vv)[32] = *reinterpret_cast<float (*)[32]>(v + 32 * gi);
               const float sum = transpose_reduce32(vv);
               const int f = gi * 32 + lane;
-              if (f < AF && sum != 0.f) atomicAdd(dst + f, sum);
+              if (f < AF && sum != 0.f) atomicAdd(dst + f, (AccT)sum);
             }
           }
         }
@@ -783,6 +794,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
     block_add_u64(a.stats + S_BWD_EVALS, n_eval);
     block_add_u64(a.stats + S_BWD_LINES, n_lines);
     block_add_u64(a.stats + S_BWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
+    block_add_u64(a.stats + S_BWD_BLENDS, n_bblend);
   }
 }
 
@@ -803,18 +815,24 @@ static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const c
   a.pixel_clamp = reinterpret_cast<uint8_t *>(ws + L.pixel_clamp);
   a.blend_mask = reinterpret_cast<uint32_t *>(ws + L.scratch + blend_mask_offset());
   a.mask_words = blend_mask_words((int64_t)((L.pair_ids - L.pair_tiles) / sizeof(uint32_t)), L.tiles_x * L.tiles_y);
-  a.accum = reinterpret_cast<float *>(ws + L.grad_accum);
+  a.accum = reinterpret_cast<AccT *>(ws + L.grad_accum);
   a.stats = reinterpret_cast<unsigned long long *>(ws + L.counters + sizeof(uint32_t) * C_STATS);
   a.image = a.final_T = a.weight_sum = a.depth = nullptr;
   a.count = nullptr;
   a.visible = nullptr;
   a.d_image = nullptr;
+  a.rec_off = nullptr;
+  a.rec_pos = nullptr;
   return a;
 }
 
 int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                         const cs_layout &L, char *ws, const cs_frame &f, bool stats, cudaStream_t s) {
+                         const cs_layout &L, char *ws, const cs_frame &f, bool stats, cudaStream_t s,
+                         const int64_t *rec_off, int32_t *rec_pos) {
   BlendArgs a = make_args(cam, set, L, ws);
+  a.rec_off = rec_off;
+  a.rec_pos = rec_pos;
+  const bool rec = rec_off != nullptr;
   a.image = f.image;
   a.final_T = f.final_T;
   a.weight_sum = f.weight_sum;
@@ -824,11 +842,11 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
   if (f.visible && p.n > 0) cudaMemsetAsync(f.visible, 0, (size_t)p.n, s);
   const int tiles = L.tiles_x * L.tiles_y;
   if (L.max_k == 8) {
-    auto k = stats ? forward_kernel<8, true> : forward_kernel<8, false>;
+    auto k = rec ? forward_kernel<8, false, true> : stats ? forward_kernel<8, true> : forward_kernel<8, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
     k<<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<8, CS_FWD_STAGES>), s>>>(a);
   } else {
-    auto k = stats ? forward_kernel<16, true> : forward_kernel<16, false>;
+    auto k = rec ? forward_kernel<16, false, true> : stats ? forward_kernel<16, true> : forward_kernel<16, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_FWD_STAGES>));
     k<<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
   }
@@ -848,9 +866,9 @@ int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs
   a.d_image = d_image;
   if (p.n > 0) {
 #ifdef CS_MEMSET_ACCUM
-    cudaMemsetAsync(a.accum, 0, (size_t)p.n * L.acc_floats * sizeof(float), s);
+    cudaMemsetAsync(a.accum, 0, (size_t)p.n * L.acc_floats * sizeof(AccT), s);
 #else
-    const size_t n4 = (size_t)p.n * L.acc_floats / 4;   // acc_floats is a multiple of 4
+    const size_t n4 = (size_t)p.n * L.acc_floats * sizeof(AccT) / 16;   // acc_floats is a multiple of 4
     zero_kernel<<<(int)std::min<size_t>((n4 + 511) / 512, 148 * 8), 512, 0, s>>>(reinterpret_cast<float4 *>(a.accum), n4);
 #endif
   }

@@ -33,6 +33,7 @@ const char *cs_error_string(int code) {
     case CS_ERR_ARG: return "bad argument";
     case CS_ERR_CUDA: return "CUDA launch failure";
     case CS_ERR_WORKSPACE: return "workspace too small";
+    case CS_ERR_NONFINITE: return "non-finite gradient";
     case CS_ERR_UNSUPPORTED: return "unsupported setting (tile size must be 16, sh_degree 0..3)";
     default: return "unknown error";
   }
@@ -71,7 +72,7 @@ int cs_workspace_layout(const cs_camera *cam, const cs_settings *set, int64_t n,
   L.pixel_last = take(sizeof(int32_t) * npix);
   L.pixel_T = take(sizeof(float) * npix);
   L.pixel_clamp = take(npix);
-  L.grad_accum = take(sizeof(float) * un * L.acc_floats);
+  L.grad_accum = take(sizeof(cs::AccT) * un * L.acc_floats);
   L.scratch_bytes = cs::scratch_bytes(n, pair_capacity, pp, tiles, nullptr, nullptr);
   L.scratch = take(L.scratch_bytes);
   L.total_bytes = off;
@@ -107,6 +108,30 @@ int cs_forward_ex(const cs_camera *cam, const cs_settings *set, const cs_params 
   return CS_OK;
 }
 
+int cs_forward_record(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                      size_t workspace_bytes, int64_t pair_capacity, const cs_frame *frame, const int64_t *offsets,
+                      int32_t *positions, void *stream) {
+  if (!params || !frame || !workspace || !offsets || !positions) return CS_ERR_ARG;
+  cs_layout L;
+  int rc = cs_workspace_layout(cam, set, params->n, params->k, pair_capacity, &L);
+  if (rc) return rc;
+  if (workspace_bytes < L.total_bytes) return CS_ERR_WORKSPACE;
+  if (!frame->image || !frame->final_T || !frame->count || !frame->weight_sum) return CS_ERR_ARG;
+  return cs::launch_forward_blend(*cam, *set, *params, L, static_cast<char *>(workspace), *frame, false,
+                                  reinterpret_cast<cudaStream_t>(stream), offsets, positions);
+}
+
+int cs_read_status(const void *workspace, void *stream) {
+  if (!workspace) return CS_ERR_ARG;
+  uint32_t c[cs::C_COUNT];
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(c, workspace, sizeof(c), cudaMemcpyDeviceToHost, s) != cudaSuccess) return CS_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return CS_ERR_CUDA;
+  if (c[cs::C_NONFINITE]) return CS_ERR_NONFINITE;
+  if (c[cs::C_OVERFLOW]) return CS_ERR_WORKSPACE;
+  return CS_OK;
+}
+
 int cs_forward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
                       size_t workspace_bytes, int64_t pair_capacity, const cs_frame *frame, int32_t first_stage,
                       int32_t last_stage, void *stream) {
@@ -136,9 +161,11 @@ static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_
     return CS_ERR_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char *ws = static_cast<char *>(workspace);
-  if (first_stage == 0)
+  if (first_stage == 0) {
+    cudaMemsetAsync(ws + L.counters + sizeof(uint32_t) * cs::C_NONFINITE, 0, sizeof(uint32_t), s);
     if ((rc = cs::launch_backward_blend(*cam, *set, *params, L, ws, d_image, (flags & CS_WORK_COUNTERS) != 0, s)))
       return rc;
+  }
   if (last_stage == 1)
     return cs::launch_chain(*cam, *set, *params, L, ws, *grads, sig, (flags & CS_GRADS_OVERWRITE) != 0, s);
   return CS_OK;

@@ -30,11 +30,13 @@ struct ChainArgs {
   int k, sh_degree, mode;
   double cam_center[3];
   const float *points, *raw_delta, *raw_sigma, *raw_opacity, *raw_mask, *sh;
-  const float *records, *accum;
+  const float *records;
+  const AccT *accum;
   const uint8_t *hull;
   const uint32_t *touched;
   cs_grads g;
   cs_view_signal sig;   // sigma_signal == nullptr: no densification signal
+  uint32_t *nonfinite;  // workspace counter C_NONFINITE: set when a gradient row is not finite
 };
 
 #ifdef CS_CHAIN_F64   // float64 geometry arrays: half the threads keep the static shared memory under 48 KB
@@ -206,14 +208,23 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
   const int k = a.k;
   const G inv_k = G(1) / (G)k;
   // the convex's screen-space accumulators, loaded as float4 up front
-  float acc[AF];
+  AccT acc[AF];
   {
+#ifdef CS_ACC_F64
+    const double2 *acc2 = reinterpret_cast<const double2 *>(a.accum + i * AF);
+#pragma unroll
+    for (int q = 0; q < AF / 2; q++) {
+      const double2 v = __ldg(acc2 + q);
+      acc[2 * q] = v.x; acc[2 * q + 1] = v.y;
+    }
+#else
     const float4 *acc4 = reinterpret_cast<const float4 *>(a.accum + i * AF);
 #pragma unroll
     for (int q = 0; q < AF / 4; q++) {
       const float4 v = __ldg(acc4 + q);
       acc[4 * q] = v.x; acc[4 * q + 1] = v.y; acc[4 * q + 2] = v.z; acc[4 * q + 3] = v.w;
     }
+#endif
   }
   // every other per-convex input is loaded up front too (one exposed
   // latency instead of a chain of them)
@@ -289,8 +300,9 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
       const G nx = ey * il, ny = -ex * il;
       const G gs = (G)acc[A_LINES + 3 * j + 2];
       // reference gn = sum dL*q - gs*v = sum dL*(q-a) - gs*(v-a); u is anchor-relative
-      const G gx = fma(-gs, ux, (G)acc[A_LINES + 3 * j]);
-      const G gy = fma(-gs, uy, (G)acc[A_LINES + 3 * j + 1]);
+      // (the cancellation of the two sums is formed in the accumulator type)
+      const G gx = (G)fma(-acc[A_LINES + 3 * j + 2], (AccT)ux, acc[A_LINES + 3 * j]);
+      const G gy = (G)fma(-acc[A_LINES + 3 * j + 2], (AccT)uy, acc[A_LINES + 3 * j + 1]);
       const G nd = fma(nx, gx, ny * gy);
       const G rx = (gx - nx * nd) * il, ry = (gy - ny * nd) * il;
       s_dx[v][t] += -ry;
@@ -333,6 +345,11 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
 #pragma unroll
   for (int c = 0; c < 3; c++) common[c] = (d_depth * R[6 + c] + (G)((ddirf[c] - dir[c] * dot) * idist)) * inv_k;
   float *dp = a.g.d_points + i * k * 3;
+  // non-finite check: inf/NaN in any input reaches the
+  // accumulators or the per-point terms, and then this sum
+  float chk = 0.f;
+#pragma unroll
+  for (int q = 0; q < AF; q++) chk += (float)acc[q];
 #pragma unroll
   for (int j = 0; j < MAXK; j++) {
     if (j < k) {
@@ -347,7 +364,11 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
         dz = -((s_x[j][t] - (G)ox) * gx + (s_y[j][t] - (G)oy) * gy) * izc[j];
       }
 #pragma unroll
-      for (int c = 0; c < 3; c++) grad_out<OW>(dp + 3 * j + c, (float)fma(d0, R[c], fma(d1, R[3 + c], fma(dz, R[6 + c], common[c]))));
+      for (int c = 0; c < 3; c++) {
+        const float g = (float)fma(d0, R[c], fma(d1, R[3 + c], fma(dz, R[6 + c], common[c])));
+        chk += g;
+        grad_out<OW>(dp + 3 * j + c, g);
+      }
     }
   }
   grad_out<OW>(a.g.d_raw_delta + i, (float)(ddel * s * delta));
@@ -363,6 +384,8 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
   const float doe = (float)acc[A_DOEFF];
   grad_out<OW>(a.g.d_raw_opacity + i, doe * o * (1.f - o));
   grad_out<OW>(a.g.d_raw_mask + i, doe * o * m * (1.f - m));
+  chk += d_rs + (float)(ddel * s * delta) + o + m + dot;
+  if (!isfinite(chk)) atomicOr(a.nonfinite, 1u);
   tma_bulk_commit_and_wait_read();   // the d_sh row has left shared memory
 }
 
@@ -384,11 +407,12 @@ int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &
   a.points = p.points; a.raw_delta = p.raw_delta; a.raw_sigma = p.raw_sigma;
   a.raw_opacity = p.raw_opacity; a.raw_mask = p.raw_mask; a.sh = p.sh;
   a.records = reinterpret_cast<const float *>(ws + L.records);
-  a.accum = reinterpret_cast<const float *>(ws + L.grad_accum);
+  a.accum = reinterpret_cast<const AccT *>(ws + L.grad_accum);
   a.hull = reinterpret_cast<const uint8_t *>(ws + L.hull);
   a.touched = reinterpret_cast<const uint32_t *>(ws + L.tiles_touched);
   a.g = g;
   a.sig = sig ? *sig : cs_view_signal{nullptr, nullptr, nullptr};
+  a.nonfinite = reinterpret_cast<uint32_t *>(ws + L.counters) + C_NONFINITE;
   if (L.max_k == 8) {
     if (overwrite) chain_kernel<8, true><<<(int)((p.n + chain_threads<8>() - 1) / chain_threads<8>()), chain_threads<8>(), 0, s>>>(a);
     else chain_kernel<8, false><<<(int)((p.n + chain_threads<8>() - 1) / chain_threads<8>()), chain_threads<8>(), 0, s>>>(a);

@@ -44,6 +44,13 @@ enum AccField { A_DC = 0, A_DOEFF = 3, A_DSIG = 4, A_DDEL = 5, A_LINES = 8 };
 template <int MAXK> struct Acc {
   static constexpr int kFloats = A_LINES + 3 * MAXK;
 };
+// Accumulator element type: the per-warp float32 partial sums of the
+// backward blend are added into AccT by global atomics.
+#ifdef CS_ACC_F64
+typedef double AccT;
+#else
+typedef float AccT;
+#endif
 
 // Counters at the head of the workspace.
 // C_KMINC / C_KMAX: uint64 complement of the smallest / the largest depth key
@@ -51,12 +58,12 @@ template <int MAXK> struct Acc {
 // depth-sort keys.
 enum Counter {
   C_NVISIBLE = 0, C_NPAIRS = 1, C_OVERFLOW = 2, C_NSORT = 3, C_CHUNK0 = 4, C_STATS = 16, C_KMINC = 32, C_KMAX = 34,
-  C_COUNT = 40
+  C_NONFINITE = 36, C_COUNT = 40
 };
 // uint64 work statistics at word C_STATS (roofline accounting, read by the benchmark)
 enum Stat {
   S_FWD_EVALS = 0, S_FWD_LINES = 1, S_FWD_BLENDS = 2, S_BWD_EVALS = 3, S_BWD_LINES = 4, S_FWD_WARP_EVALS = 5,
-  S_BWD_WARP_EVALS = 6, S_COUNT = 8
+  S_BWD_WARP_EVALS = 6, S_BWD_BLENDS = 7, S_COUNT = 8
 };
 
 // Block-wide sum of a per-thread count, added once per block to a global u64.
@@ -201,7 +208,8 @@ int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_par
 int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                    const cs_layout &L, char *ws, int64_t cap, cudaStream_t s);
 int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                         const cs_layout &L, char *ws, const cs_frame &f, bool stats, cudaStream_t s);
+                         const cs_layout &L, char *ws, const cs_frame &f, bool stats, cudaStream_t s,
+                         const int64_t *rec_off = nullptr, int32_t *rec_pos = nullptr);
 int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                           const cs_layout &L, char *ws, const float *d_image, bool stats, cudaStream_t s);
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,

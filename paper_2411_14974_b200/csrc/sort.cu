@@ -669,14 +669,14 @@ size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, int tiles, Scratch
 }
 
 struct ClearList {
-  uint2 *p[4];
-  uint64_t n[4];   // 8-byte words
+  uint2 *p[5];
+  uint64_t n[5];   // 8-byte words
 };
 __global__ void __launch_bounds__(256) clear_kernel(ClearList c) {
   const uint64_t stride = (uint64_t)gridDim.x * 256;
   uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;
 #pragma unroll
-  for (int r = 0; r < 4; r++) {
+  for (int r = 0; r < 5; r++) {
     for (; i < c.n[r]; i += stride) c.p[r][i] = make_uint2(0u, 0u);
     i -= c.n[r];
   }
@@ -705,8 +705,10 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
   uint32_t *pids = reinterpret_cast<uint32_t *>(ws + L.pair_ids);
   uint2 *ranges = reinterpret_cast<uint2 *>(ws + L.tile_ranges);
 
-  // one clearing kernel instead of four memsets: digit histograms, look-back
+  // one clearing kernel instead of five memsets: digit histograms, look-back
   // flags, tile ranges (empty tiles and n == 0 read (0, 0)), scan block sums
+  // and the sorts' dynamic chunk counters (so stage 1 can run again on its
+  // own, e.g. a replayed stage-1 graph, without stage 0's counter reset)
   const uint32_t dchunks = (n + kDupThreads * kDupRounds - 1) / (kDupThreads * kDupRounds);
   {
     ClearList cl;
@@ -714,7 +716,9 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
     cl.p[1] = reinterpret_cast<uint2 *>(sc.lookback); cl.n[1] = sizeof(uint32_t) * sc.lookback_words / 8;
     cl.p[2] = ranges; cl.n[2] = (uint64_t)tiles;
     cl.p[3] = reinterpret_cast<uint2 *>(sc.block_sums); cl.n[3] = dchunks;
-    const uint64_t total = cl.n[0] + cl.n[1] + cl.n[2] + cl.n[3];
+    static_assert(C_CHUNK0 % 2 == 0 && (C_STATS - C_CHUNK0) % 2 == 0, "chunk counters: whole 8-byte words");
+    cl.p[4] = reinterpret_cast<uint2 *>(counters + C_CHUNK0); cl.n[4] = (C_STATS - C_CHUNK0) / 2;
+    const uint64_t total = cl.n[0] + cl.n[1] + cl.n[2] + cl.n[3] + cl.n[4];
     clear_kernel<<<(int)std::min<uint64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(cl);
   }
   if (n > 0) {

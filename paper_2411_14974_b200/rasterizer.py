@@ -25,7 +25,7 @@ from .scene_tensors import SceneTensors, as_scene_tensors
 
 _COUNTERS = 40
 STAT_NAMES = ("fwd_evals", "fwd_line_evals", "fwd_blends", "bwd_evals", "bwd_line_evals", "fwd_warp_evals",
-              "bwd_warp_evals")
+              "bwd_warp_evals", "bwd_blends")
 
 
 def _device(device=None) -> torch.device:
@@ -233,8 +233,15 @@ class Rasterizer:
         c = fr.workspace.counters().cpu()
         stats = c[16:32].view(torch.int64).numpy()
         out = {name: int(stats[i]) for i, name in enumerate(STAT_NAMES)}
-        out.update(n_visible=int(c[0]), n_pairs=int(c[1]), overflow=int(c[2]))
+        out.update(n_visible=int(c[0]), n_pairs=int(c[1]), overflow=int(c[2]), nonfinite=int(c[36]))
         return out
+
+    def status(self, fr: Frame) -> int:
+        """cs_read_status of the frame's workspace (syncs): 0 ok,
+        _lib.ERR_NONFINITE when the last backward produced an inf/NaN
+        gradient row, _lib.ERR_WORKSPACE when the pairs overflowed."""
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        return int(_lib.load().cs_read_status(fr.workspace.ptr, stream))
 
     def backward(self, frame: Frame, d_image: torch.Tensor, grads: dict, overwrite: bool = False) -> dict:
         """Accumulate (+=) gradients of sum(d_image * image) into ``grads``,
@@ -381,6 +388,34 @@ def inspect_frame(fr: Frame) -> dict:
     return dict(order=order, hull=hull, bbox=bbox, depth=_decode_depth(keys), tile_ranges=ranges,
                 pair_ids=pair_ids, pair_tiles=pair_tiles, tile_offsets=off, records=recs,
                 tiles_x=L.tiles_x, tiles_y=L.tiles_y, n_visible=V, n_pairs=P)
+
+
+def record_blends(fr: Frame):
+    """The frame's blend decisions (diagnostics for the decision-forced
+    parity check, cs_forward_record): (offsets [H*W+1] int64, positions
+    int32 -- pixel p blended the pair indices positions[offsets[p]:
+    offsets[p+1]] in blend order --, clamp [H*W] uint8 -- bit c set iff
+    channel c of C + T*bg lay in [0, 1], the clip test of
+    backward.py:154-158).  Re-runs the frame's blend stage with the same
+    kernel (it is deterministic) while recording."""
+    ws, L = fr.workspace, fr.workspace.layout
+    H, W = fr.cam_c.height, fr.cam_c.width
+    counts = fr.count.reshape(-1).to(torch.int64)
+    offsets = torch.zeros(H * W + 1, dtype=torch.int64, device=counts.device)
+    torch.cumsum(counts, 0, out=offsets[1:])
+    total = int(offsets[-1])
+    pos = torch.full((max(total, 1),), -1, dtype=torch.int32, device=counts.device)
+    starts = offsets[:-1].contiguous()
+    count0 = fr.count.clone()
+    stream = torch.cuda.current_stream(counts.device).cuda_stream
+    _lib.check(_lib.load().cs_forward_record(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
+                                             ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
+                                             ctypes.byref(fr.extras["frame_c"]), starts.data_ptr(),
+                                             pos.data_ptr(), stream), "cs_forward_record")
+    if not torch.equal(fr.count, count0):
+        raise _lib.CsError("cs_forward_record: the re-run blend decided differently")
+    clamp = ws.region("pixel_clamp", torch.uint8, H * W)
+    return _np(offsets), _np(pos)[:total], _np(clamp)
 
 
 @dataclass

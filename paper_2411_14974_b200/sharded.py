@@ -126,6 +126,15 @@ class Adam:
             p.addcdiv_(m, denom, value=-lrs[name] / bc1)
 
 
+class TrainingDiverged(RuntimeError):
+    """trainer.TrainingDiverged (trainer.py:172-173): the loss or a gradient
+    of the step became non-finite."""
+
+    def __init__(self, iteration: int, loss: float):
+        super().__init__(f"training diverged at iteration {iteration}: loss {loss}")
+        self.iteration, self.loss = iteration, loss
+
+
 # --------------------------------------------------------------------------- sharding
 def shard_views(batch: list, rank: int, world: int) -> list:
     """Round-robin assignment: batch position i goes to rank i mod world."""
@@ -226,6 +235,9 @@ class ViewShardedStep:
         check = getattr(self.view_grad_fn, "check_overflow", None)
         while check is not None and check():   # a view overflowed its pair capacity: redo with more room
             info = self.accumulate(batch)
+        diverged = getattr(self.view_grad_fn, "diverged", None)
+        if diverged is not None and diverged():   # trainer.py:172-173 (read with the overflow check)
+            raise TrainingDiverged(self.iteration, float(info["local_loss_sum"]))
         self.reduce(len(batch))
         self.adam.step(self.params, self.flat.grads(), self.lrs(self.iteration), grad_scale=1.0 / len(batch))
         # densification signal since the last densify round (trainer.py:192-193)
@@ -275,7 +287,8 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
     r = rasterizer or default_rasterizer(scene.device)
     lw = LossWorkspace()
     ws = Workspace(scene.device)
-    state = {"cap": None, "max": torch.zeros(2, dtype=torch.int32, device=scene.device)}
+    # device maxima over the step's views: (pairs, overflow, non-finite)
+    state = {"cap": None, "max": torch.zeros(3, dtype=torch.int32, device=scene.device), "bad": False}
 
     def fn(view, grads: dict, signal: dict):
         cam, target = view
@@ -284,18 +297,22 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
             state["cap"] = fr.capacity
         else:
             fr = r.forward(scene, cam, mode, settings, workspace=ws, capacity=state["cap"], check=False)
-        torch.maximum(state["max"], ws.counters()[1:3], out=state["max"])   # (pairs, overflow)
+        torch.maximum(state["max"][0:2], ws.counters()[1:3], out=state["max"][0:2])   # (pairs, overflow)
         loss = cuda_image_loss(fr.image, target, scene.raw_mask, config.lambda_dssim, config.beta_mask,
                                d_raw_mask=grads["raw_mask"], workspace=lw)
         r.launch_backward(fr, loss["d_image"], grads,
                           signal=(signal["sigma_signal"], signal["sigma_views"], fr.visible))
+        # non-finite loss (trainer.py:172) or gradient row (the chain's C_NONFINITE flag)
+        bad = (~torch.isfinite(loss["total"])).to(torch.int32).reshape(1)
+        torch.maximum(state["max"][2:3], torch.maximum(bad, ws.counters()[36:37]), out=state["max"][2:3])
         return loss["total"]
 
     def check_overflow() -> bool:
         """One host read per step: True (and a larger capacity) if any view
         overflowed its pair capacity since the last check."""
-        pairs, ovf = (int(v) for v in state["max"].cpu())
+        pairs, ovf, bad = (int(v) for v in state["max"].cpu())
         state["max"].zero_()
+        state["bad"] = bool(bad) and not ovf
         if ovf:
             state["cap"] = int(pairs * 1.25) + 1024
             if state["cap"] >= (1 << 30):
@@ -305,6 +322,7 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
 
     fn.handles_signal = True
     fn.check_overflow = check_overflow
+    fn.diverged = lambda: state["bad"]
     return fn
 
 
@@ -330,5 +348,5 @@ def torch_view_grad_fn(scene, mode, settings, config: StepConfig = StepConfig(),
     return fn
 
 
-__all__ = ["StepConfig", "image_loss", "ssim", "gaussian_window", "Adam", "position_lr", "shard_views",
+__all__ = ["StepConfig", "TrainingDiverged", "image_loss", "ssim", "gaussian_window", "Adam", "position_lr", "shard_views",
            "FlatGrads", "ViewShardedStep", "rasterizer_view_grad_fn", "torch_view_grad_fn"]

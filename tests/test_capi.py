@@ -76,9 +76,9 @@ def test_layout_rejects_bad_arguments(lib):
     assert lib.cs_workspace_layout(ctypes.byref(cam), ctypes.byref(st), 10, 17, 100, ctypes.byref(L)) == 1
     assert lib.cs_workspace_layout(ctypes.byref(cam), ctypes.byref(st), -1, 6, 100, ctypes.byref(L)) == 1
     cam8, st8 = _structs(settings=RenderSettings(tile_size=8))
-    assert lib.cs_workspace_layout(ctypes.byref(cam8), ctypes.byref(st8), 10, 6, 100, ctypes.byref(L)) == 4
+    assert lib.cs_workspace_layout(ctypes.byref(cam8), ctypes.byref(st8), 10, 6, 100, ctypes.byref(L)) == _lib.ERR_UNSUPPORTED
     camd, std = _structs(settings=RenderSettings(sh_degree=4))
-    assert lib.cs_workspace_layout(ctypes.byref(camd), ctypes.byref(std), 10, 6, 100, ctypes.byref(L)) == 4
+    assert lib.cs_workspace_layout(ctypes.byref(camd), ctypes.byref(std), 10, 6, 100, ctypes.byref(L)) == _lib.ERR_UNSUPPORTED
 
 
 def test_forward_rejects_small_workspace_without_touching_the_gpu(lib):
@@ -92,7 +92,7 @@ def test_forward_rejects_small_workspace_without_touching_the_gpu(lib):
 
 
 def test_error_strings(lib):
-    for code in range(5):
+    for code in range(6):
         assert lib.cs_error_string(code)
     assert b"unknown" in lib.cs_error_string(99)
 
@@ -129,7 +129,7 @@ def test_training_entry_points_validate_before_launching(lib):
     cfg = _lib.CsDensityConfig()
     assert lib.cs_density_flags(ctypes.byref(p), None, None, None, None, None, None, None) == 1
     assert lib.cs_density_flags(ctypes.byref(p), None, ctypes.byref(cfg), None, None, None, None, None) == 0
-    assert lib.cs_abi_version() == _lib.ABI_VERSION == 6
+    assert lib.cs_abi_version() == _lib.ABI_VERSION == 7
 
 
 def test_backward_ex_validates_flags_and_signal(lib):

@@ -98,3 +98,59 @@ def test_backward_matches_reference(name):
                          ("d_sh", "g_sh"), ("d_raw_mask", "g_mask")):
         err = grad_rel_error(gr[ours], g[theirs])
         assert err < 1e-8, (ours, err)
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if "d_image" in gc.load(c)])
+def test_forced_backward_with_own_decisions_is_the_reference(name):
+    """The decision-forced oracle backward (used to compare the GPU at its own
+    discrete decisions) fed the reference's own decisions is the plain
+    oracle backward, bit for bit; the decisions reproduce the counts."""
+    g = gc.load(name)
+    params, cam, st = gc.params(g), gc.camera(g), gc.settings(g)
+    view = oracle.prepare_view(params, cam, st)
+    tiles = oracle.bin_tiles(view, cam["width"], cam["height"], st["tile"])
+    offsets, pos = oracle.blend_decisions(cam, st, view, tiles)
+    np.testing.assert_array_equal(np.diff(offsets).reshape(g["count"].shape), g["count"])
+    plain = oracle.backward(params, cam, st, g["d_image"], view=view, tiles=tiles)
+    forced = oracle.backward(params, cam, st, g["d_image"], view=view, tiles=tiles, forced=(offsets, pos, None))
+    for k in ("d_points", "d_raw_delta", "d_raw_sigma", "d_raw_opacity", "d_sh", "d_raw_mask"):
+        np.testing.assert_array_equal(forced[k], plain[k], err_msg=k)
+
+
+def test_forced_backward_follows_the_given_decisions():
+    """Dropping one recorded blend from a pixel changes exactly the
+    gradients of the convexes that pixel's walk reaches, and the forced walk
+    takes it as given (a flipped threshold decision)."""
+    g = gc.load("config1")
+    params, cam, st = gc.params(g), gc.camera(g), gc.settings(g)
+    view = oracle.prepare_view(params, cam, st)
+    tiles = oracle.bin_tiles(view, cam["width"], cam["height"], st["tile"])
+    offsets, pos = oracle.blend_decisions(cam, st, view, tiles)
+    plain = oracle.backward(params, cam, st, g["d_image"], view=view, tiles=tiles)
+    p = int(np.argmax(np.diff(offsets)))           # the pixel with the most blends
+    drop = int(offsets[p]) + 2                      # its third blend
+    off2 = offsets.copy()
+    off2[p + 1:] -= 1
+    pos2 = np.delete(pos, drop)
+    forced = oracle.backward(params, cam, st, g["d_image"], view=view, tiles=tiles, forced=(off2, pos2, None))
+    items = tiles[1]
+    moved = np.flatnonzero(np.abs(forced["d_raw_opacity"] - plain["d_raw_opacity"]) > 0)
+    # only convexes that pixel blended (at or before the dropped one, whose
+    # transmittance / colour-behind terms change) can move
+    blended = set(view["order"][items[pos[offsets[p]:offsets[p + 1]]]].tolist())
+    assert moved.size > 0 and set(moved.tolist()) <= blended
+
+
+@pytest.mark.parametrize("name", ["config1", "mode_none", "exact7", "alpha_cap"])
+def test_forced_render_with_own_decisions_is_the_reference(name):
+    """The decision-forced oracle render fed the reference's own decisions
+    reproduces the plain render bit for bit."""
+    g = gc.load(name)
+    params, cam, st = gc.params(g), gc.camera(g), gc.settings(g)
+    view = oracle.prepare_view(params, cam, st)
+    tiles = oracle.bin_tiles(view, cam["width"], cam["height"], st["tile"])
+    offsets, pos = oracle.blend_decisions(cam, st, view, tiles)
+    plain = oracle.render(params, cam, st, view=view, tiles=tiles)
+    forced = oracle.render(params, cam, st, view=view, tiles=tiles, forced=(offsets, pos))
+    for k in ("image", "trans", "count", "wsum", "depth", "visible"):
+        np.testing.assert_array_equal(forced[k], plain[k], err_msg=k)
