@@ -112,7 +112,8 @@ typedef struct cs_layout {
                                  uint64[8] at word 16: work stats (forward evaluations,
                                  line evaluations, blends; backward evaluations, lines),
                                  counted only with CS_WORK_COUNTERS */
-    size_t records;           /* float[n][rec_floats] per-convex blend records */
+    size_t records;           /* float[n][rec_floats] per-convex blend record header */
+    size_t lines;             /* double[n][max_k][4] per-convex hull lines (A, B, C, 0; log2 units) */
     size_t hull;              /* uint8[n][max_k]  hull cycle (indices into the K points) */
     size_t bbox;              /* int32[n][4]  x0,x1,y0,y1 half-open pixel rect */
     size_t depth_keys;        /* uint64[n]    f64 bits of the centre depth (~0 culled) */

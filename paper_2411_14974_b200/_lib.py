@@ -79,7 +79,7 @@ class CsDensityConfig(ctypes.Structure):
 
 class CsLayout(ctypes.Structure):
     _fields_ = [(name, ctypes.c_size_t) for name in (
-        "total_bytes", "counters", "records", "hull", "bbox", "depth_keys", "order", "tiles_touched",
+        "total_bytes", "counters", "records", "lines", "hull", "bbox", "depth_keys", "order", "tiles_touched",
         "pair_offsets", "pair_tiles", "pair_ids", "tile_ranges", "pixel_last", "pixel_T", "pixel_clamp",
         "grad_accum", "scratch", "scratch_bytes")] + [
         (name, ctypes.c_int32) for name in ("rec_floats", "acc_floats", "max_k", "tiles_x", "tiles_y",

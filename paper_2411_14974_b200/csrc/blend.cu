@@ -31,6 +31,7 @@ namespace cs {
 
 struct BlendArgs {
   const float *records;
+  const double *lines;
   const uint32_t *pair_ids;
   const uint2 *ranges;
   const uint32_t *tile_order;   // heaviest tiles first (null: index order)
@@ -94,22 +95,25 @@ struct LineSet {
   static constexpr int kN = NL > 0 ? NL : MAXK;
   float c[3 * kN];
   int nl;
+  // stage record planes A[MAXK] | B[MAXK] | C'[MAXK] after the header
   __device__ __forceinline__ void load(const float4 *rec, int nl_rt) {
     nl = NL > 0 ? NL : nl_rt;
 #pragma unroll
-    for (int q = 0; q < (3 * kN + 3) / 4; q++) {
-      const float4 v = rec[R_HEADER / 4 + q];
-      const float e[4] = {v.x, v.y, v.z, v.w};
+    for (int p = 0; p < 3; p++)
 #pragma unroll
-      for (int r = 0; r < 4; r++)
-        if (4 * q + r < 3 * kN) c[4 * q + r] = e[r];
-    }
+      for (int q = 0; q < (kN + 3) / 4; q++) {
+        const float4 v = rec[(R_HEADER + p * MAXK) / 4 + q];
+        const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+          if (4 * q + r < kN) c[3 * (4 * q + r) + p] = e[r];
+      }
   }
   __device__ __forceinline__ bool has(int l) const { return NL > 0 ? true : l < nl; }
 };
 
-// Smooth field of a candidate at anchor-relative pixel (dx, dy), in log2
-// units (field.py:51-72, rasterize.py:147-153):
+// Smooth field of a candidate at pixel (dx, dy) relative to the tile's
+// re-basing point, in log2 units (field.py:51-72, rasterize.py:147-153):
 //   z_l = A_l dx + B_l dy + C_l, phi2 = log2 sum 2^z_l,
 //   I = 1 / (1 + 2^(sigma_s phi2)), alpha = min(o I, ALPHA_MAX).
 // The sum is formed without the max shift (4 instructions per line); when it
@@ -234,51 +238,77 @@ __device__ __forceinline__ void flush_visible(PipeSmem<MAXK, kStages> &sm, int s
   __syncwarp();
 }
 
-// Forward block culling by the producer (otherwise idle between stage
-// fills): for candidate j and the tile's 8x4 block q, the LSE is at least the
-// largest line value, and each line's minimum over the block's pixel centres
-// is at a corner, so phi2 >= max_l min_corner z_l.  When even that bound
-// keeps o I below the cutoff at every pixel of the block -- sig * lb >
+// Per-tile line staging by the producer warp (lane j = candidate j of the
+// batch): every line of the candidate re-based onto the tile's re-basing
+// point T (float64: C' = A (Tx - ax) + B (Ty - ay) + C, then rounded once),
+// written to the stage's A / B / C' planes.
+//
+// Forward block culling (the producer is otherwise idle between stage
+// fills): for the tile's 8x4 block q, the LSE is at least the largest line
+// value, and each line's minimum over the block's pixel centres is at a
+// corner, so phi2 >= max_l min_corner z_l.  When even that bound keeps o I
+// below the cutoff at every pixel of the block -- sig * lb >
 // log2(o / cutoff - 1), with a margin far above the float32 evaluation's
 // error -- the block cannot blend the candidate and its warp skips it.
-struct BlockCull {
-  float qx0, qy0;   // pixel-centre coordinates of the tile's first pixel
-  float cutoff;
+struct TileLines {
+  double tx, ty;    // re-basing point (pixel coordinates)
+  float cutoff;     // > 0: compute the forward cull mask
 };
 template <int MAXK>
-__device__ __forceinline__ uint32_t block_cull_mask(const float *rec, const BlockCull &bc) {
-  const float4 h0 = __ldg(reinterpret_cast<const float4 *>(rec)), h2 = __ldg(reinterpret_cast<const float4 *>(rec) + 2);
+__device__ __forceinline__ uint32_t stage_lines(const float *rec_g, const double *lines_g, float4 *rec_s,
+                                                const TileLines &tl) {
+  const float4 h0 = __ldg(reinterpret_cast<const float4 *>(rec_g)), h2 = __ldg(reinterpret_cast<const float4 *>(rec_g) + 2);
   const int nl = min(__float_as_int(h2.z), MAXK);
-  const float thr = __log2f(h0.w / bc.cutoff - 1.f);
-  const float dx0 = bc.qx0 - h0.x, dy0 = bc.qy0 - h0.y;
+  const double X = tl.tx - (double)h0.x, Y = tl.ty - (double)h0.y;
+  float *As = reinterpret_cast<float *>(rec_s) + R_HEADER, *Bs = As + MAXK, *Cs = As + 2 * MAXK;
+  const bool cull = tl.cutoff > 0.f;
+  const float thr = cull ? __log2f(h0.w / tl.cutoff - 1.f) : 0.f;
+  // block q's pixel-centre corners relative to T: x in {c0, c0 + 7}, y in {r0, r0 + 3}
+  constexpr float d0 = 0.5f - (float)kRebase;
   float lb[8];
 #pragma unroll
   for (int q = 0; q < 8; q++) lb[q] = -INFINITY;
-  for (int l = 0; l < nl; l++) {
-    const float A = __ldg(rec + R_HEADER + 3 * l), B = __ldg(rec + R_HEADER + 3 * l + 1),
-                C = __ldg(rec + R_HEADER + 3 * l + 2);
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const float xl = dx0 + (float)((q & 1) * 8), yl = dy0 + (float)((q >> 1) * 4);
-      const float zx = fminf(A * xl, A * (xl + 7.f)), zy = fminf(B * yl, B * (yl + 3.f));
-      lb[q] = fmaxf(lb[q], C + zx + zy);
+  for (int l = 0; l < MAXK; l++) {
+    if (l < nl) {
+      double A, B, C, pad;
+      ld_global_nc_v4d(lines_g + 4 * l, A, B, C, pad);
+      const float Af = (float)A, Bf = (float)B, Cf = (float)fma(A, X, fma(B, Y, C));
+      As[l] = Af;
+      Bs[l] = Bf;
+      Cs[l] = Cf;
+      if (cull) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const float xl = d0 + (float)((q & 1) * 8), yl = d0 + (float)((q >> 1) * 4);
+          const float zx = fminf(Af * xl, Af * (xl + 7.f)), zy = fminf(Bf * yl, Bf * (yl + 3.f));
+          lb[q] = fmaxf(lb[q], Cf + zx + zy);
+        }
+      }
     }
   }
   uint32_t m = 0xffu;
+  if (cull) {
 #pragma unroll
-  for (int q = 0; q < 8; q++) {
-    const float v = h0.z * lb[q];
-    if (v - thr > 1e-3f * (1.f + fabsf(thr) + fabsf(v))) m &= ~(1u << q);
+    for (int q = 0; q < 8; q++) {
+      const float v = h0.z * lb[q];
+      if (v - thr > 1e-3f * (1.f + fabsf(thr) + fabsf(v))) m &= ~(1u << q);
+    }
   }
   return m;
 }
 
 // Producer warp: batch b covers pair indices first(b) .. first(b)+count(b)-1.
+// Per batch: the candidates' headers by coalesced cp.async gathers (4
+// 16-byte chunks per record, 8 records per warp instruction; `full` counts
+// their completion per lane), their lines re-based onto the tile by
+// stage_lines (plain shared stores, then an explicit release arrive per lane
+// on `full`, which therefore expects 64 arrivals).
 template <int MAXK, int kStages, int NC, typename Batch>
-__device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const float *records, const uint32_t *pair_ids,
-                                             int nbatch, Batch batch, bool forward, uint8_t *visible,
-                                             const BlockCull *cull = nullptr) {
-  constexpr int RB = Rec<MAXK>::kFloats * 4;
+__device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const float *records, const double *lines,
+                                             const uint32_t *pair_ids, int nbatch, Batch batch, bool forward,
+                                             uint8_t *visible, const TileLines &tl, bool cull) {
+  constexpr int RG = Rec<MAXK>::kGlobal;
   const int lane = threadIdx.x & 31;
   int issued = 0;
   bool stopped = false;
@@ -301,11 +331,8 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
       // (done warps lag) keep releasing the issued batches < b normally.
       if (lane == 0) *reinterpret_cast<volatile int *>(&sm.stop) = b + 1;
       __syncwarp();
-#ifdef CS_PRODUCER_TMA
-      if (lane == 0) mbar_arrive(&sm.full[s]);   // wake consumers waiting on batch b
-#else
-      mbar_arrive(&sm.full[s]);                  // all 32 lanes: the barrier counts 32
-#endif
+      mbar_arrive(&sm.full[s]);                  // all 32 lanes, twice: the barrier counts 64
+      mbar_arrive(&sm.full[s]);
       stopped = true;
       break;
     }
@@ -318,34 +345,30 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
       next_id = lane < (int)c1 ? __ldg(pair_ids + f1 + lane) : 0u;
     }
     if (lane < (int)count) sm.id[s][lane] = id;
-    if (cull)
-      sm.bmask[s][lane] = (uint8_t)(lane < (int)count ? block_cull_mask<MAXK>(records + (size_t)id * Rec<MAXK>::kFloats,
-                                                                              *cull)
-                                                       : 0xffu);
-    __syncwarp();
-#ifdef CS_PRODUCER_TMA
-    if (lane == 0) mbar_expect_tx(&sm.full[s], count * RB);
-    __syncwarp();
-    if (lane < (int)count) tma_bulk_g2s(&sm.rec[s][lane][0], records + (size_t)id * Rec<MAXK>::kFloats, RB, &sm.full[s]);
-#else
     {
-      // coalesced gather: each round copies RPR whole records, one 16-byte
-      // chunk per lane (cp.async.cg), so every record is read as contiguous
-      // sectors; the lanes then arrive on `full` when their copies land.
-      constexpr int CPR = Rec<MAXK>::kFloats / 4, RPR = 32 / CPR;
+      // coalesced header gather: each round copies 8 whole headers, one
+      // 16-byte chunk per lane (cp.async.cg), so every header is read as
+      // contiguous sectors; the lanes then arrive on `full` when their
+      // copies land.
+      constexpr int CPR = R_HEADER / 4, RPR = 32 / CPR;
       const int r_in = lane / CPR, c = lane % CPR;
       for (int r0 = 0; r0 < (int)count; r0 += RPR) {
         const int r = r0 + r_in;
         const uint32_t rid = __shfl_sync(0xffffffffu, id, min(r, 31));
-        if (r_in < RPR && r < (int)count) {
-          const float4 *src = reinterpret_cast<const float4 *>(records + (size_t)rid * Rec<MAXK>::kFloats) + c;
+        if (r < (int)count) {
+          const float4 *src = reinterpret_cast<const float4 *>(records + (size_t)rid * RG) + c;
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sm.rec[s][r][c])), "l"(src)
                        : "memory");
         }
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
     }
-#endif
+    uint32_t bm = 0xffu;
+    if (lane < (int)count)
+      bm = stage_lines<MAXK>(records + (size_t)id * RG, lines + (size_t)id * Rec<MAXK>::kLines64, sm.rec[s][lane],
+                             TileLines{tl.tx, tl.ty, cull ? tl.cutoff : 0.f});
+    sm.bmask[s][lane] = (uint8_t)bm;
+    mbar_arrive(&sm.full[s]);   // release: this lane's shared stores
     issued = b + 1;
   }
   // drain: wait until the consumers released the last issued batches (their
@@ -363,11 +386,7 @@ template <int MAXK, int kStages, int NC>
 __device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages> &sm) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
-#ifdef CS_PRODUCER_TMA
-      mbar_init(&sm.full[s], 1);
-#else
-      mbar_init(&sm.full[s], 32);   // one cp.async arrival per producer lane
-#endif
+      mbar_init(&sm.full[s], 64);   // per producer lane: its cp.async completion + its line stores
       mbar_init(&sm.empty[s], NC);
       sm.vis[s] = 0u;
     }
@@ -387,14 +406,15 @@ struct FwdPixel {
 
 // One candidate at one pixel: evaluate, and blend iff (T >= floor if floor >
 // 0) and alpha >= cutoff (rasterize.py:194-204).  Returns whether it blended.
+// (dqx, dqy): the pixel centre relative to the tile's re-basing point.
 template <int NL, int MAXK, bool STATS>
-__device__ __forceinline__ bool fwd_candidate(const float4 *rec, float qx, float qy, float cutoff, float floor_,
+__device__ __forceinline__ bool fwd_candidate(const float4 *rec, float dqx, float dqy, float cutoff, float floor_,
                                               bool use_floor, int pos, FwdPixel &P, unsigned &n_lines) {
   const float4 h0 = rec[0], h2 = rec[2];
   LineSet<NL, MAXK> L;
   L.load(rec, __float_as_int(h2.z));
   float z[LineSet<NL, MAXK>::kN];
-  const Eval e = eval_field<NL, MAXK>(L, h0.z, h0.w, qx - h0.x, qy - h0.y, z);
+  const Eval e = eval_field<NL, MAXK>(L, h0.z, h0.w, dqx, dqy, z);
   if (STATS) n_lines += L.nl;
   if (!(e.alpha >= cutoff)) return false;
   const float4 h1 = rec[1];
@@ -433,19 +453,18 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
   unsigned n_eval = 0, n_lines = 0, n_blend = 0, n_warp_evals = 0;
   if (warp == NC) {
 #ifndef CS_NO_BLOCK_CULL
-    const BlockCull bc{(float)(tx * kTile) + 0.5f, (float)(ty * kTile) + 0.5f, a.cutoff};
     // (a counting run evaluates every candidate: its work counts are the
     // algorithmic E_fwd of the roofline accounting)
     const bool cull = !STATS && NC == 8 && a.cutoff > 0.f;
 #else
-    const BlockCull bc{0.f, 0.f, 0.f};
     const bool cull = false;
 #endif
-    pipe_produce<MAXK, kStages, NC>(sm, a.records, a.pair_ids, nbatch,
+    const TileLines tl{(double)(tx * kTile + kRebase), (double)(ty * kTile + kRebase), a.cutoff};
+    pipe_produce<MAXK, kStages, NC>(sm, a.records, a.lines, a.pair_ids, nbatch,
                        [&](int b, uint32_t &first, uint32_t &count) {
                          first = range.x + (uint32_t)b * kStageCands;
                          count = min((uint32_t)kStageCands, range.y - first);
-                       }, true, a.visible, cull ? &bc : nullptr);
+                       }, true, a.visible, tl, cull);
   } else {
     int lx, ly;
     tile_pixel(threadIdx.x, lx, ly);
@@ -453,7 +472,7 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2) + half * 8;
     const bool inside = px < a.width && py < a.height;
-    const float qx = px + 0.5f, qy = py + 0.5f;
+    const float qx = (float)(lx - kRebase) + 0.5f, qy = (float)(ly - kRebase) + 0.5f;   // relative to T
     int32_t *rec_dst = nullptr;
     if (REC && inside) rec_dst = a.rec_pos + a.rec_off[(size_t)py * a.width + px];
     FwdPixel P;
@@ -585,7 +604,7 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
   L.load(rec, __float_as_int(h2.z));
   constexpr int N = LineSet<NL, MAXK>::kN;
   float z[N];
-  const float dx = qx - h0.x, dy = qy - h0.y;
+  const float dx = qx, dy = qy;   // relative to the tile's re-basing point
   const float o = h0.w, sig = h0.z, dls = h2.y, inv_dls = h2.w;
   const Eval e = eval_field<NL, MAXK, true>(L, sig, o, dx, dy, z);
   if (STATS) n_lines += L.nl;
@@ -666,8 +685,8 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
 #pragma unroll
   for (int h = 0; h < PPL; h++) {
     const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3) + 4 * h;
-    qx[h] = px + 0.5f;
-    qy[h] = py + 0.5f;
+    qx[h] = (float)(px - tx * kTile - kRebase) + 0.5f;   // relative to the tile's re-basing point
+    qy[h] = (float)(py - ty * kTile - kRebase) + 0.5f;
     P[h].T = 1.f; P[h].g0 = P[h].g1 = P[h].g2 = P[h].S0 = P[h].S1 = P[h].S2 = 0.f;
     P[h].last = -1;
     if (warp < NC && px < a.width && py < a.height) {
@@ -702,7 +721,8 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
   };
   unsigned n_eval = 0, n_lines = 0, n_warp_evals = 0, n_bblend = 0;
   if (warp == NC) {
-    pipe_produce<MAXK, kStages, NC>(sm, a.records, a.pair_ids, nbatch, batch, false, nullptr);
+    const TileLines tl{(double)(tx * kTile + kRebase), (double)(ty * kTile + kRebase), 0.f};
+    pipe_produce<MAXK, kStages, NC>(sm, a.records, a.lines, a.pair_ids, nbatch, batch, false, nullptr, tl, false);
   } else {
     for (int b = 0; b < nbatch; b++) {
       const int s = b % kStages;
@@ -775,6 +795,17 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
 #undef CS_BWD2_PX
           if (STATS) n_warp_evals += __any_sync(0xffffffffu, any_act) ? 1u : 0u;
           if (__any_sync(0xffffffffu, contrib)) {
+            // the line sums are kept relative to the record's anchor a (the
+            // chain's frame): sum dL (q - a) = sum dL (q - T) + (T - a) sum dL
+            {
+              const float2 an = *reinterpret_cast<const float2 *>(rec);
+              const float ox = (float)(tx * kTile + kRebase) - an.x, oy = (float)(ty * kTile + kRebase) - an.y;
+#pragma unroll
+              for (int l = 0; l < MAXK; l++) {
+                v[A_LINES + 3 * l] = fmaf(ox, v[A_LINES + 3 * l + 2], v[A_LINES + 3 * l]);
+                v[A_LINES + 3 * l + 1] = fmaf(oy, v[A_LINES + 3 * l + 2], v[A_LINES + 3 * l + 1]);
+              }
+            }
             AccT *dst = a.accum + (size_t)sm.id[s][j] * AF;
 #pragma unroll
             for (int gi = 0; gi < NG; gi++) {
@@ -801,6 +832,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
 static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const cs_layout &L, char *ws) {
   BlendArgs a;
   a.records = reinterpret_cast<const float *>(ws + L.records);
+  a.lines = reinterpret_cast<const double *>(ws + L.lines);
   a.pair_ids = reinterpret_cast<const uint32_t *>(ws + L.pair_ids);
   a.ranges = reinterpret_cast<const uint2 *>(ws + L.tile_ranges);
   a.tile_order = L.tiles_x * L.tiles_y <= kMaxTileOrder ? reinterpret_cast<const uint32_t *>(ws + L.scratch) : nullptr;

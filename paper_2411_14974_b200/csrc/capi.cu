@@ -47,7 +47,7 @@ int cs_workspace_layout(const cs_camera *cam, const cs_settings *set, int64_t n,
   cs_layout L;
   std::memset(&L, 0, sizeof(L));
   L.max_k = k <= 8 ? 8 : 16;
-  L.rec_floats = cs::R_HEADER + 3 * L.max_k;
+  L.rec_floats = cs::R_HEADER;
   L.acc_floats = cs::A_LINES + 3 * L.max_k;
   L.tiles_x = (cam->width + cs::kTile - 1) / cs::kTile;
   L.tiles_y = (cam->height + cs::kTile - 1) / cs::kTile;
@@ -60,6 +60,7 @@ int cs_workspace_layout(const cs_camera *cam, const cs_settings *set, int64_t n,
   auto take = [&](size_t bytes) { size_t o = off; off = cs::align_up(off + bytes, 256); return o; };
   L.counters = take(sizeof(uint32_t) * cs::C_COUNT);
   L.records = take(sizeof(float) * un * L.rec_floats);
+  L.lines = take(sizeof(double) * un * 4 * L.max_k);
   L.hull = take(un * L.max_k);
   L.bbox = take(sizeof(int32_t) * 4 * un);
   L.depth_keys = take(sizeof(uint64_t) * un);

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
   __shared__ G s_dx[MAXK][kChainThreads], s_dy[MAXK][kChainThreads];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t i = (int64_t)blockIdx.x * kChainThreads + t;
-  constexpr int RF = Rec<MAXK>::kFloats;
+  constexpr int RF = Rec<MAXK>::kGlobal;
   constexpr int AF = Acc<MAXK>::kFloats;
   constexpr int kShRow = kShCoeffs * 3;
   // SH rows: one 192-byte bulk copy per prepared convex, issued first so it

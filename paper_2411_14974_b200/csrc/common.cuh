@@ -20,22 +20,36 @@ constexpr uint64_t kCulledKey = ~0ull;
 constexpr int kMaxTileOrder = 1 << 17;
 
 // ---------------------------------------------------------------------------
-// Per-convex blend record (float32), written by the preprocess kernel and
-// read by both blend kernels.  Line j evaluates, in log2 units,
-//   z2_j(q) = A_j*(qx-ax) + B_j*(qy-ay) + C_j = delta_s*log2(e)*L_j(q)
-// where L_j = n_j.q + off_j is the reference's signed line distance
-// (projection.py:131-133) and (ax, ay) an integer anchor inside the bbox
-// (keeps fp32 cancellation out of 1080p coordinates).
-//   float4 0: ax ay sigma_s o | 1: r g b depth | 2: 1-o dls nl 1/dls
-//   float4 3: bbox x0 x1 y0 y1 (int32 bits, half-open) | 4..: lines (A,B,C)
+// Per-convex blend record, written by the preprocess kernel:
+//   header (float32, 16 floats, global `records`):
+//     float4 0: ax ay sigma_s o | 1: r g b depth | 2: 1-o dls nl 1/dls
+//     float4 3: bbox x0 x1 y0 y1 (int32 bits, half-open)
+//   lines (float64, global `lines`, [MAXK][4] = (A, B, C, 0) per line, one
+//   256-bit store / load each):
+//     z2_j(q) = A_j*(qx-ax) + B_j*(qy-ay) + C_j = delta_s*log2(e)*L_j(q)
+//   where L_j = n_j.q + off_j is the reference's signed line distance
+//   (projection.py:131-133) and (ax, ay) an integer anchor (the pixel at hull
+//   vertex 0).
+// The blend kernels' producer warp re-bases every line of a candidate onto
+// the tile it streams it to -- C'_j = z2_j at the tile's centre point
+// (tx*16+8, ty*16+8), formed in float64 -- and stages float32 (A, B, C') in
+// shared memory next to the header: the per-pixel float32 evaluation then
+// only sees |dx|, |dy| <= 8 and |C'| = |z| near the tile, instead of
+// cancelling offsets of the size of the convex (a 300-pixel convex at
+// delta_s*log2(e) ~ 7 carried ~1e-4 of absolute error in z2 with one anchor).
+// Stage record in shared memory: header (16 floats) | A[MAXK] | B[MAXK] | C'[MAXK].
 enum RecField {
   R_AX = 0, R_AY = 1, R_SIGMA = 2, R_OPACITY = 3, R_R = 4, R_G = 5, R_B = 6, R_DEPTH = 7,
   R_ONE_MINUS_O = 8, R_DLS = 9, R_NLINES = 10, R_INV_DLS = 11, R_BBOX = 12, R_HEADER = 16
 };
 template <int MAXK> struct Rec {
-  static constexpr int kFloats = R_HEADER + 3 * MAXK;   // 40 for MAXK=8, multiple of 4
-  static_assert(kFloats % 4 == 0, "record must be float4 aligned");
+  static constexpr int kGlobal = R_HEADER;               // floats per convex in `records`
+  static constexpr int kFloats = R_HEADER + 3 * MAXK;   // stage record: 40 for MAXK=8, multiple of 4
+  static constexpr int kLines64 = 4 * MAXK;             // doubles per convex in `lines`
+  static_assert(kFloats % 4 == 0 && MAXK % 4 == 0, "record planes must be float4 aligned");
 };
+// Tile re-basing point: pixel (tx*16 + kRebase, ty*16 + kRebase).
+constexpr int kRebase = 8;
 
 // Screen-space gradient accumulators per convex (backward.py:102-108):
 //   d_color(3), d_opacity_eff, d_sigma_s, d_delta_s, pad(2), then per line
@@ -88,6 +102,14 @@ __device__ __forceinline__ uint64_t orderable_bits(double d) {
   if (d == 0.0) d = 0.0;  // -0.0 ties +0.0 as in Python's sort
   uint64_t b = (uint64_t)__double_as_longlong(d);
   return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// 256-bit global accesses (sm_100): four doubles at a 32-byte aligned address.
+__device__ __forceinline__ void st_global_v4d(double *p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void ld_global_nc_v4d(const double *p, double &a, double &b, double &c, double &d) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
 __device__ __forceinline__ float ex2(float x) {

@@ -26,6 +26,7 @@ struct PreArgs {
   double cutoff;
   const float *points, *raw_delta, *raw_sigma, *raw_opacity, *raw_mask, *sh;
   float *records;
+  double *lines;
   uint8_t *hull;
   int4 *bbox;
   uint64_t *depth_keys;
@@ -405,8 +406,9 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   const int v0 = hull.get(0);
   const double axd = floor(X[v0 * kPreThreads]), ayd = floor(Y[v0 * kPreThreads]);
   const double dls = delta_s * 1.4426950408889634;  // delta_s * log2(e)
-  constexpr int RF = Rec<MAXK>::kFloats;
+  constexpr int RF = Rec<MAXK>::kGlobal;
   float4 *dst = reinterpret_cast<float4 *>(a.records + i * RF);
+  double *lines = a.lines + i * Rec<MAXK>::kLines64;   // (A, B, C, 0) per line
   // line of edge j (projection.py:116-128): from vertex hull[j] to hull[j+1]
   auto line = [&](int j, double &nx, double &ny, double &off) {
     const int u = hull.get(j), v = hull.get(j + 1 < h ? j + 1 : 0);
@@ -424,17 +426,14 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
     line(h - 1, pnx, pny, poff);
   }
   double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
-  float buf[4];
 #pragma unroll
   for (int j = 0; j < MAXK; j++) {
-    float e3[3] = {0.f, 0.f, -INFINITY};   // padding line: 2^z = 0
     if (j < h) {
       double nx, ny, off;
       line(j, nx, ny, off);
-      // blend coefficients, anchor-relative offset formed in float64
-      e3[0] = (float)(dls * nx);
-      e3[1] = (float)(dls * ny);
-      e3[2] = (float)(dls * (off + nx * axd + ny * ayd));
+      // blend coefficients in float64, anchor-relative offset (the blends'
+      // producer re-bases them per tile)
+      st_global_v4d(lines + 4 * j, dls * nx, dls * ny, dls * (off + nx * axd + ny * ayd), 0.0);
       if (!full_frame) {  // projection.py:167-169, vertex j
         const int u = hull.get(j);
         double den = 1.0 + (pnx * nx + pny * ny);
@@ -446,12 +445,6 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
       }
       pnx = nx;
       pny = ny;
-    }
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-      const int f = 3 * j + c;
-      buf[f & 3] = e3[c];
-      if ((f & 3) == 3) dst[R_HEADER / 4 + f / 4] = make_float4(buf[0], buf[1], buf[2], buf[3]);
     }
   }
   // projection.py:170-177
@@ -602,6 +595,7 @@ int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_par
   a.points = p.points; a.raw_delta = p.raw_delta; a.raw_sigma = p.raw_sigma;
   a.raw_opacity = p.raw_opacity; a.raw_mask = p.raw_mask; a.sh = p.sh;
   a.records = reinterpret_cast<float *>(ws + L.records);
+  a.lines = reinterpret_cast<double *>(ws + L.lines);
   a.hull = reinterpret_cast<uint8_t *>(ws + L.hull);
   a.bbox = reinterpret_cast<int4 *>(ws + L.bbox);
   a.depth_keys = reinterpret_cast<uint64_t *>(ws + L.depth_keys);

@@ -58,8 +58,8 @@ def test_workspace_layout_regions_are_disjoint_and_aligned(lib):
     assert lib.cs_workspace_layout(ctypes.byref(cam), ctypes.byref(st), 1_000_000, 6, 8_000_000,
                                    ctypes.byref(L)) == 0
     assert (L.tiles_x, L.tiles_y) == (120, 68)
-    assert L.max_k == 8 and L.rec_floats == 40 and L.acc_floats == 32
-    names = ["counters", "records", "hull", "bbox", "depth_keys", "order", "tiles_touched", "pair_offsets",
+    assert L.max_k == 8 and L.rec_floats == 16 and L.acc_floats == 32
+    names = ["counters", "records", "lines", "hull", "bbox", "depth_keys", "order", "tiles_touched", "pair_offsets",
              "pair_tiles", "pair_ids", "tile_ranges", "pixel_last", "pixel_T", "pixel_clamp", "grad_accum",
              "scratch"]
     offs = [getattr(L, n) for n in names]

@@ -150,5 +150,7 @@ def test_sharded_step_gradients_equal_sum_of_view_backwards():
     for k in ref:
         a, b = step.flat.views[k].cpu().numpy().ravel(), ref[k].cpu().numpy().ravel()
         den = np.maximum(np.abs(a), np.abs(b))
-        rel = np.abs(a - b) / np.maximum(den, max(1e-4 * den.max(), 1e-12))
+        # the fused loss adjoint is float32 (the reference formulation here
+        # float64): the floor of tests/test_gpu_parity.py GRAD_FLOOR
+        rel = np.abs(a - b) / np.maximum(den, max(2e-4 * den.max(), 1e-12))
         assert rel.max() < 1e-3, (k, rel.max())

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.txt 2>&1
+tail -2 gpurun_out/smoke.txt
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -s > gpurun_out/pytest_gpu_full.log 2>&1
+grep -E "grad rel err|passed|failed|Error" gpurun_out/pytest_gpu_full.log | grep -v drop-in | cut -c1-330 | tail -40
+bash tools/ab_bench.sh base > gpurun_out/ab3.txt 2>&1; cat gpurun_out/ab3.txt
