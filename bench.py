@@ -1,22 +1,32 @@
 #!/usr/bin/env python
 """Benchmark of the sm_100a convex-splatting hot path (BASELINE.json metric).
 
-Workload (BASELINE.json configs[3]): G(1M, seed 0) six-point
-convexes, camera C(1920, 1080), DEPTH scaling, RenderSettings() defaults,
-synthetic float32 scene (no dataset), d_image ~ N(0, 1e-3) for the backward.
+Headline workload (BASELINE.json configs[3]): G(1M, seed 0)
+six-point convexes, camera C(1920, 1080), DEPTH scaling, RenderSettings()
+defaults, synthetic float32 scene (no dataset), d_image ~ N(0, 1e-3) for the
+backward.
 
 * ``value``: forward frames/s over all ranks (each rank renders a replica of
   the single view: one view is not partitioned), scene resident
   in HBM, L2 flushed before every timed frame (a 512 MB write, untimed).
-* ``fwd_bwd_iters_per_s``: forward + gradient zeroing + backward.
+* ``fwd_bwd_iters_per_s``: forward + backward (fresh gradients).
 * ``e2e``: same metric through the C-ABI call with HOST buffers: pinned
   host->device copy of the six parameter arrays, cs_forward, device->host
   copy of the image, all inside the timed region.
-* ``roofline``: the dominant kernel of the frame, from live CUDA-event stage
-  timings and the kernels' own work counters.
+* ``roofline``: the dominant kernel of the fwd+bwd frame, with SURVEY 8(d)'s
+  algorithmic work per stage (``roofline.stages``) and the frame composites
+  sum(t_ideal) / t_frame.
+* ``configs``: BASELINE.json configs 1-3 (1k @256^2 fwd+bwd on the
+  reference's own config-1 scene; the toy-chair fit, 128 views @512^2 per
+  training step; 100k @1297x840 forward), each with the CPU reference path
+  timed beside it (N = 1 only).
+* ``train_step``: config 5, the view-sharded training step (64 views
+  1297x840, NCCL all_reduce of the gradients) on all ranks.
 * ``cpu_baseline``: the float64 C oracle (port of the reference, oracle/)
   on this box's host cores over a bounded sample of tiles.
 
+``--gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (127.0.0.1 rendezvous).
 ``--impl reference`` times only the CPU reference path (the oracle port) on
 the host cores and prints the same JSON line with ``"impl": "reference"``.
 """
@@ -55,6 +65,12 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-train", action="store_true", help="skip the config-5 view-sharded training step")
+    p.add_argument("--no-configs", action="store_true", help="skip the config 1-3 blocks")
+    p.add_argument("--cpu-check", action="store_true",
+                   help="launcher / collective check without a GPU: the config-5 step logic on CPU over gloo")
+    p.add_argument("--chair-views", type=int, default=128)
+    p.add_argument("--chair-size", type=int, default=512)
+    p.add_argument("--chair-steps", type=int, default=3)
     p.add_argument("--train-views", type=int, default=64)
     p.add_argument("--train-width", type=int, default=1297)
     p.add_argument("--train-height", type=int, default=840)
@@ -67,6 +83,18 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def relaunch_distributed(n: int) -> int:
+    """Run this script under torch.distributed.run with n ranks (one node,
+    127.0.0.1 rendezvous on a free port); returns its exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def host_cores() -> int:
@@ -226,6 +254,185 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- configs 1-3
+def graph_times(r, fr, d_image, grads, flush, dev, steps: int, warmup: int, backward: bool):
+    """Forward (and forward + backward with fresh gradients) of an existing
+    frame as CUDA-graph replays, L2 flushed before every timed step; mean ms."""
+    import numpy as np
+    import torch
+    stream = torch.cuda.current_stream(dev)
+
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
+
+    def fwdbwd():
+        r.launch_forward(fr, 0, 2)
+        r.launch_backward(fr, d_image, grads, 0, 0)
+        r.launch_backward(fr, d_image, grads, 1, 1, overwrite=True)
+
+    torch.cuda.synchronize(dev)
+    graphs = [capture(lambda: r.launch_forward(fr, 0, 2))] + ([capture(fwdbwd)] if backward else [])
+    torch.cuda.synchronize(dev)
+    out = []
+    for g in graphs:
+        for _ in range(warmup):
+            g.replay()
+        ms = []
+        for _ in range(steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms.append(e0.elapsed_time(e1))
+        out.append(float(np.mean(ms)))
+    return out
+
+
+def config1_block(args, dev, flush, cpu: bool) -> dict:
+    """BASELINE.json configs[0]: the reference's own config-1 scene
+    (synth.make_scene(1000, 6, seed=0), ring_cameras(1, size=256)[0]; the
+    committed fixture tests/golden/config1.npz made by the reference) and its
+    d_image; forward + backward."""
+    import numpy as np
+    import torch
+
+    import paper_2411_14974_b200 as cs
+    from paper_2411_14974_b200 import rasterizer as rz
+    from tests import golden_cases as gc
+    g = gc.load("config1")
+    c, st_d = gc.camera(g), gc.settings(g)
+    cam = cs.Camera(fx=c["fx"], fy=c["fy"], cx=c["cx"], cy=c["cy"], width=c["width"], height=c["height"], R=c["R"],
+                    t=c["t"], z_near=c["z_near"], ortho=c["ortho"])
+    settings = cs.RenderSettings(contribution_cutoff=st_d["cutoff"], transmittance_floor=st_d["floor"])
+    st = cs.SceneTensors.from_arrays(gc.params(g), dev, background=g["background"])
+    r = rz.Rasterizer(dev)
+    fr = r.forward(st, cam, cs.ScalingMode(st_d["mode"]), settings)
+    d = torch.tensor(g["d_image"], dtype=torch.float32, device=dev)
+    fwd_ms, fb_ms = graph_times(r, fr, d, rz.empty_grads(st), flush, dev, max(args.steps, 20), 3, True)
+    out = {"workload": "config1: reference make_scene(1000, 6, seed=0) @ ring_cameras(1, size=256)[0], its d_image "
+                       "(tests/golden/config1.npz)", "convexes": st.n, "pairs": fr.n_pairs,
+           "gpu": {"fwd_fps": 1000.0 / fwd_ms, "fwd_ms": fwd_ms, "fwd_bwd_iters_per_s": 1000.0 / fb_ms,
+                   "fwd_bwd_ms": fb_ms, "launch": "CUDA graph replay, L2 flushed between steps"}}
+    if cpu:
+        import oracle
+        threads = host_cores()
+        t0 = time.perf_counter()
+        reps = 0
+        while reps < 3 or time.perf_counter() - t0 < 2.0:
+            view = oracle.prepare_view(gc.params(g), c, st_d, n_threads=threads)
+            tiles = oracle.bin_tiles(view, c["width"], c["height"], 16)
+            oracle.render(gc.params(g), c, st_d, n_threads=threads, view=view, tiles=tiles)
+            reps += 1
+        t_f = (time.perf_counter() - t0) / reps
+        t0 = time.perf_counter()
+        oracle.backward(gc.params(g), c, st_d, g["d_image"], n_threads=threads)
+        t_b = time.perf_counter() - t0
+        out["cpu_baseline"] = {"kind": "port", "cores": threads, "cpu": cpu_model(),
+                               "fwd_fps": 1.0 / t_f, "fwd_bwd_iters_per_s": 1.0 / (t_f + t_b),
+                               "sample": "whole frame (float64 C oracle: prepare_view + bin_tiles + render; backward "
+                                         "re-walks the frame)",
+                               "reference_numpy_s": {"fwd": 1.07, "bwd": 3.17, "source": "BASELINE.md section 2 "
+                                                     "(the reference package itself, 1 core, survey container)"}}
+    return out
+
+
+def config3_block(args, dev, flush, cpu: bool) -> dict:
+    """BASELINE.json configs[2]: G(100k, 0) @ C(1297, 840), forward FPS."""
+    import paper_2411_14974_b200 as cs
+    from paper_2411_14974_b200 import rasterizer as rz, synthetic
+    arrays = synthetic.quantize32(synthetic.generate_scene(100_000, 0))
+    cam = synthetic.bench_camera(1297, 840)
+    st = cs.SceneTensors.from_arrays(arrays, dev)
+    r = rz.Rasterizer(dev)
+    fr = r.forward(st, cam, cs.ScalingMode.DEPTH, cs.RenderSettings())
+    (fwd_ms,) = graph_times(r, fr, None, None, flush, dev, max(args.steps, 20), 3, False)
+    out = {"workload": "config3: G(100000,0) 6-point convexes @ 1297x840 (Mip-NeRF360 /4 shape), forward",
+           "convexes": st.n, "pairs": fr.n_pairs,
+           "gpu": {"fwd_fps": 1000.0 / fwd_ms, "fwd_ms": fwd_ms, "launch": "CUDA graph replay, L2 flushed"}}
+    if cpu:
+        threads = host_cores()
+        c = cpu_sample(arrays, cam, 6.0, threads, with_backward=False)
+        out["cpu_baseline"] = {"kind": "port", "cores": threads, "cpu": cpu_model(), "fwd_fps": 1.0 / c["fwd_frame_s"],
+                               "sample": f"full prepare_view+bin_tiles + {c['tiles_sampled']}/{c['tiles_total']} "
+                                         "random tiles, extrapolated",
+                               "reference_numpy_s": {"fwd": 70.5, "source": "BASELINE.md section 2"}}
+    return out
+
+
+def config2_block(args, dev, cpu: bool) -> dict:
+    """BASELINE.json configs[1]: toy chair fit.  Ground truth: the procedural
+    chair of 6-point prisms (synthetic.chair_scene) rendered from
+    ring_cameras(128) at 512^2; the fitted scene starts from
+    initialize.init_scene semantics on 2000 surface samples
+    (synthetic.init_scene_arrays).  One training step = render + L1/D-SSIM +
+    mask loss + backward of all 128 views, summed gradients, fused Adam
+    (ViewShardedStep, batch = 128 views)."""
+    import numpy as np
+    import torch
+
+    import paper_2411_14974_b200 as cs
+    from paper_2411_14974_b200 import rasterizer as rz, sharded, synthetic
+    size, nv = args.chair_size, args.chair_views
+    cams = synthetic.ring_cameras(nv, size, size)
+    mode, settings = cs.ScalingMode.DEPTH, cs.RenderSettings()
+    r = rz.Rasterizer(dev)
+    gt = cs.SceneTensors.from_arrays(synthetic.quantize32(synthetic.chair_scene()), dev)
+    views = [(c, r.forward(gt, c, mode, settings).image.clone()) for c in cams]
+    pts, cols = synthetic.chair_surface_samples(2000, seed=0)
+    init = synthetic.quantize32(synthetic.init_scene_arrays(pts, cols))
+    scene = cs.SceneTensors.from_arrays(init, dev)
+    params = {k: getattr(scene, k) for k in sharded.PARAM_ORDER}
+    step = sharded.ViewShardedStep(params, sharded.StepConfig(),
+                                   sharded.rasterizer_view_grad_fn(scene, mode, settings, rasterizer=r))
+    stream = torch.cuda.current_stream(dev)
+    step.step(views)                                     # warm-up: sizes the pair capacity
+    torch.cuda.synchronize(dev)
+    times, losses = [], []
+    for _ in range(args.chair_steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        info = step.step(views)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        times.append(e0.elapsed_time(e1))
+        losses.append(float(info["local_loss_sum"]) / nv)
+    ms = float(np.mean(times))
+    out = {"workload": f"config2: toy chair fit, {scene.n} convexes initialised from 2000 chair surface samples "
+                       f"(initialize.init_scene semantics), {nv} ring views @ {size}x{size}, batch = all views",
+           "gt_convexes": gt.n, "convexes": scene.n,
+           "gpu": {"train_steps_per_s": 1000.0 / ms, "ms_per_step": ms, "views_per_s": nv * 1000.0 / ms,
+                   "mean_view_loss_first_last": [losses[0], losses[-1]], "steps": args.chair_steps,
+                   "step": "per view: forward, fused L1+D-SSIM+mask loss, backward (accumulate); then one fused "
+                           "Adam update"}}
+    if cpu:
+        import oracle
+        threads = host_cores()
+        o_set = dict(cutoff=2e-4, floor=1e-4, tile=16, sh_degree=3, mode="depth", background=np.zeros(3))
+        sample = 2
+        t0 = time.perf_counter()
+        for c, tgt in views[:sample]:
+            cam_d = synthetic.camera_dict(c)
+            view = oracle.prepare_view(init, cam_d, o_set, n_threads=threads)
+            tiles = oracle.bin_tiles(view, size, size, 16)
+            fr = oracle.render(init, cam_d, o_set, n_threads=threads, view=view, tiles=tiles)
+            img = torch.tensor(fr["image"], requires_grad=True)
+            raw_mask = torch.tensor(init["raw_mask"], requires_grad=True)
+            loss = sharded.image_loss(img, tgt.double().cpu(), raw_mask)["total"]
+            d_img, _ = torch.autograd.grad(loss, (img, raw_mask))
+            oracle.backward(init, cam_d, o_set, d_img.numpy(), n_threads=threads, view=view, tiles=tiles)
+        per_view = (time.perf_counter() - t0) / sample
+        out["cpu_baseline"] = {"kind": "port", "cores": threads, "cpu": cpu_model(),
+                               "train_steps_per_s": 1.0 / (per_view * nv),
+                               "sample": f"{sample} of {nv} views (float64 C oracle fwd+bwd, torch float64 loss on "
+                                         f"the CPU), extrapolated to the {nv}-view step"}
+    return out
+
+
 # ----------------------------------------------------------------------------- config 5
 def train_step_bench(args, st, arrays, dev, world, rank):
     """One optimisation step over a batch of B ring views (1297x840): views
@@ -278,20 +485,71 @@ def train_step_bench(args, st, arrays, dev, world, rank):
             "rank0_loss_sum_first_last": [losses[0], losses[-1]]}
 
 
+# ----------------------------------------------------------------------------- launcher check (CPU)
+def cpu_check(args):
+    """--cpu-check: the multi-rank plumbing of this script without a GPU.
+    Every rank runs the config-5 step logic (ViewShardedStep: round-robin
+    views, one all_reduce(SUM) per step, identical Adam) with the
+    deterministic CPU per-view gradients of tests/test_sharded.py over gloo;
+    rank 0 prints the world size it ran with and whether every replica ended
+    bit-identical to the others and to a single-process run."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_14974_b200 import sharded
+    from tests.test_sharded import _params, _run_steps
+
+    world, rank, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    batch, steps = list(range(2 * world + 3)), 3
+    single = _params()                    # the single-process result (before the group exists)
+    _run_steps(single, batch, steps)
+    if world > 1:
+        dist.init_process_group("gloo")
+    params = _params()
+    _run_steps(params, batch, steps)
+    flat = torch.cat([params[k].reshape(-1) for k in sharded.PARAM_ORDER])
+    gathered = [torch.empty_like(flat) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(gathered, flat)
+    else:
+        gathered = [flat]
+    if rank == 0:
+        ref = torch.cat([single[k].reshape(-1) for k in sharded.PARAM_ORDER])
+        line = {"impl": "cpu-check", "n_gpus": world, "ranks": len(gathered), "backend": "gloo" if world > 1 else None,
+                "views": len(batch), "steps": steps,
+                "replicas_identical": all(torch.equal(g, gathered[0]) for g in gathered),
+                "max_abs_vs_single_process": float((gathered[0] - ref).abs().max())}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))     # one process per GPU under torch.distributed.run
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.cpu_check:
+        cpu_check(args)
         return
     import numpy as np
     import torch
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # communicator set-up (ranks, transports, NVLS) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_2411_14974_b200 import rasterizer as rz
@@ -390,7 +648,8 @@ def main():
     if not args.no_e2e:
         names = ("points", "raw_delta", "raw_sigma", "raw_opacity", "raw_mask", "sh")
         host = {k: getattr(st, k).detach().cpu().pin_memory() for k in names}
-        sets = [st, SceneTensors(*(torch.empty_like(getattr(st, k)) for k in names), background=st.background)]
+        # the second set starts as a copy (its sizing forward must see real parameters)
+        sets = [st, SceneTensors(*(getattr(st, k).clone() for k in names), background=st.background)]
         frames = [fr, r.forward(sets[1], cam, ScalingMode.DEPTH, settings, workspace=ws)]
         img_host = [torch.empty(fr.image.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
         h2d = sum(v.numel() * v.element_size() for v in host.values())
@@ -437,11 +696,12 @@ def main():
                "path": "pinned host params -> cs_forward (C ABI) -> pinned host image; two device parameter "
                        "sets: H2D of frame i+1 overlaps the render of frame i, D2H on a third stream"}
 
-    # ---- roofline of the frame's kernels
+    # ---- roofline: SURVEY.md 8(d)'s algorithmic work per stage
     L = ws.layout
     n, V, P = st.n, stats["n_visible"], stats["n_pairs"]
     pp = max(1, math.ceil(math.log2(max(L.tiles_x * L.tiles_y, 2)) / 8))
     stage_ms = fwd.mean(axis=0)
+    bwd_ms = fb.mean(axis=0)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -459,26 +719,36 @@ def main():
                        f"({mp['per_sm_per_clk']} per SM per clock; profiles/mufu_peak.json)")
     except (OSError, ValueError, KeyError):
         pass
-    k = st.k
-    pre_bytes = n * (k * 12 + 4 * 4 + 48 * 4) + n * (8 + 4 + 4) + V * (L.rec_floats * 4 + L.max_k + 16)
-    bin_bytes = (n * 8 + 8 * n * 12 * 2            # depth sort: histogram + 8 passes of (key, id)
-                 + n * 4 * 2 + n * 4 * 2 + n * 4   # scan: gather touched via order (x2 passes), write offsets
-                 + V * (4 + 4 + 16 + 4) + P * 8    # duplicate
-                 + P * 4 + pp * P * 8 * 2          # pair sort: histogram + passes of (tile, id)
-                 + P * 4)                          # ranges
-    mufu_ops = stats["fwd_line_evals"] + 3 * stats["fwd_evals"]
+    # K1: params read (280 B) + tiles_touched (4 B) per convex, 104-B record per visible convex
+    pre_bytes = n * 280 + n * 4 + V * 104
+    # K2: depth rank V x 12 B x 2 x 8 passes; duplicate P x 12 B; radix over
+    # ceil(log2 tiles) + ceil(log2 V) key bits in 8-bit digits, P x (2 x 12 x passes + 8) B; ranges P x 8 B
+    key_bits = math.ceil(math.log2(max(L.tiles_x * L.tiles_y, 2))) + math.ceil(math.log2(max(V, 2)))
+    radix_passes = math.ceil(key_bits / 8)
+    bin_bytes = V * 12 * 2 * 8 + P * 12 + P * (2 * 12 * radix_passes + 8) + P * 8
+    # K3: E_fwd x (T + 2) MUFU ops (T = hull lines of the candidate; E_fwd from the counting run)
+    fwd_mufu = stats["fwd_line_evals"] + 2 * stats["fwd_evals"]
+    # K4a: E_bwd x (T + 3); K4b: N x (280 + 96 + 280) B
+    bwd_mufu = stats["bwd_line_evals"] + 3 * stats["bwd_evals"]
+    chain_bytes = n * (280 + 96 + 280)
+
+    def stage(ms, bound, work, unit, peak, basis):
+        achieved = work / (ms * 1e-3) / 1e9
+        return {"ms": float(ms), "bound": bound, "work": int(work), "unit": unit, "achieved": achieved,
+                "peak": peak, "frac": achieved / peak, "ideal_ms": work / peak / 1e9 * 1e3, "basis": basis}
     stage_info = {
-        "preprocess": {"ms": float(stage_ms[0]), "bound": "hbm", "work": pre_bytes, "unit": "GB/s",
-                       "achieved": pre_bytes / (stage_ms[0] * 1e-3) / 1e9, "peak": hbm_peak},
-        "binning": {"ms": float(stage_ms[1]), "bound": "hbm", "work": bin_bytes, "unit": "GB/s",
-                    "achieved": bin_bytes / (stage_ms[1] * 1e-3) / 1e9, "peak": hbm_peak},
-        "blend": {"ms": float(stage_ms[2]), "bound": "sfu", "work": mufu_ops, "unit": "Gop/s",
-                  "achieved": mufu_ops / (stage_ms[2] * 1e-3) / 1e9, "peak": mufu_peak},
+        "preprocess": stage(stage_ms[0], "hbm", pre_bytes, "GB/s", hbm_peak, "N x 284 B + V x 104 B"),
+        "binning": stage(stage_ms[1], "hbm", bin_bytes, "GB/s", hbm_peak,
+                         f"V x 192 B + P x (12 + 24 x {radix_passes} + 16) B ({key_bits}-bit keys)"),
+        "blend": stage(stage_ms[2], "sfu", fwd_mufu, "Gop/s", mufu_peak, "E_fwd x (T + 2) MUFU"),
+        "backward_blend": stage(bwd_ms[1], "sfu", bwd_mufu, "Gop/s", mufu_peak, "E_bwd x (T + 3) MUFU"),
+        "chain": stage(bwd_ms[2], "hbm", chain_bytes, "GB/s", hbm_peak, "N x (280 + 96 + 280) B"),
     }
-    for s in stage_info.values():
-        s["frac"] = s["achieved"] / s["peak"]
-    bwd_ms = fb.mean(axis=0)
-    dominant = max(stage_info, key=lambda s: stage_info[s]["ms"])
+    ideal_fwd = sum(stage_info[k]["ideal_ms"] for k in ("preprocess", "binning", "blend"))
+    ideal_fb = ideal_fwd + stage_info["backward_blend"]["ideal_ms"] + stage_info["chain"]["ideal_ms"]
+    composite = {"forward": {"ideal_ms": ideal_fwd, "measured_ms": fwd_ms, "frac": ideal_fwd / fwd_ms},
+                 "fwd_bwd": {"ideal_ms": ideal_fb, "measured_ms": fb_ms, "frac": ideal_fb / fb_ms}}
+    dominant = max(stage_info, key=lambda s2: stage_info[s2]["ms"])      # over the fwd+bwd frame
     dom = stage_info[dominant]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -490,7 +760,18 @@ def main():
     roofline = {"kernel": dominant, "bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
                 "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if dom["bound"] == "hbm" else mufu_source,
-                "stages": stage_info}
+                "work_source": "SURVEY.md 8(d) algorithmic counts; E and T from an untimed counting pass",
+                "stages": stage_info, "composite": composite}
+
+    configs = None
+    if world == 1 and not args.no_configs:
+        del fr, grads
+        torch.cuda.empty_cache()
+        cpu_ok = not args.no_cpu_baseline
+        configs = {"config1": config1_block(args, dev, flush, cpu_ok),
+                   "config3": config3_block(args, dev, flush, cpu_ok),
+                   "config2": config2_block(args, dev, cpu_ok)}
+        torch.cuda.empty_cache()
 
     # ---- config 5: view-sharded training step (B views, all_reduce of the gradients)
     train = None
@@ -523,6 +804,7 @@ def main():
                      "backward_blend": float(bwd_ms[1]), "chain": float(bwd_ms[2])},
         "work": {k2: int(v) for k2, v in stats.items()},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clock, "train_step": train,
+        "configs": configs,
         # timed: whole-frame and per-stage graphs of the forward, then of fwd+bwd
         "gpu_launches": 2 * args.steps * (launches_fwd + (launches_fwd + 3)),
         "gpu_launches_detail": f"{launches_fwd} per forward (1 preprocess, 1 scratch clear, 6 depth order: key32 + offsets + "

@@ -193,6 +193,28 @@ CS_API int cs_read_counters(const void *workspace, uint32_t *host_out4, void *st
  * pairs overflowed the capacity, else CS_OK. */
 CS_API int cs_read_status(const void *workspace, void *stream);
 
+/* Full per-view state of the prepared convexes, float64 (the drop-in
+ * prepare_view's ProjectedConvex, projection.py:180-203, and ViewPrimitive,
+ * rasterize.py:56-65).  Rows of convexes the view did not prepare are left
+ * untouched; hull-line rows past the hull length are NaN. */
+typedef struct cs_view_export {
+    double *pixels;           /* [n,k,2]  projected points (projection.py:22-40) */
+    double *point_depths;     /* [n,k]    camera-frame z of the points */
+    double *normals;          /* [n,k,2]  hull-line unit normals (projection.py:116-128) */
+    double *offsets;          /* [n,k]    hull-line offsets */
+    double *delta_s, *sigma_s, *opacity, *scale;  /* [n] */
+    double *view_dir;         /* [n,3]    unit camera-centre -> convex-centre */
+    double *view_dist;        /* [n] */
+    double *color;            /* [n,3]    eval_sh_color in float64 */
+} cs_view_export;
+
+/* Replaces the per-primitive outputs of rasterize.prepare_view
+ * (rasterize.py:77-122) beyond the blend record: run after a forward (stage
+ * 0 at least) on the same workspace. */
+CS_API int cs_prepare_view_export(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                                  const void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                                  const cs_view_export *out, void *stream);
+
 /* Blend decisions of a frame (diagnostics: the decision-forced parity check
  * of the float64 oracle, tests/).  Re-runs stage 2 of cs_forward on a
  * workspace whose stages 0..1 ran, with the same kernel the forward uses,

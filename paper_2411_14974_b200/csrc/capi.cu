@@ -122,6 +122,22 @@ int cs_forward_record(const cs_camera *cam, const cs_settings *set, const cs_par
                                   reinterpret_cast<cudaStream_t>(stream), offsets, positions);
 }
 
+int cs_prepare_view_export(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                           const void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                           const cs_view_export *out, void *stream) {
+  if (!params || !workspace || !out) return CS_ERR_ARG;
+  cs_layout L;
+  int rc = cs_workspace_layout(cam, set, params->n, params->k, pair_capacity, &L);
+  if (rc) return rc;
+  if (workspace_bytes < L.total_bytes) return CS_ERR_WORKSPACE;
+  if (params->n > 0 && (!out->pixels || !out->point_depths || !out->normals || !out->offsets || !out->delta_s ||
+                        !out->sigma_s || !out->opacity || !out->scale || !out->view_dir || !out->view_dist ||
+                        !out->color || !params->points || !params->sh))
+    return CS_ERR_ARG;
+  return cs::launch_export_view(*cam, *set, *params, L, static_cast<const char *>(workspace), *out,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
 int cs_read_status(const void *workspace, void *stream) {
   if (!workspace) return CS_ERR_ARG;
   uint32_t c[cs::C_COUNT];

@@ -249,6 +249,8 @@ int launch_density_flags(const cs_params &P, const float *signal, const cs_densi
 int launch_density_scatter(const cs_params &P, const cs_density_config &c, const uint8_t *flags,
                            const uint32_t *child_keep, const int64_t *surv_pos, const int64_t *child_pos,
                            const int64_t *n_surv, const cs_scene_out &o, int64_t *index_map, cudaStream_t s);
+int launch_export_view(const cs_camera &cam, const cs_settings &set, const cs_params &p, const cs_layout &L,
+                       const char *ws, const cs_view_export &out, cudaStream_t s);
 int launch_hull_batch(int32_t m, int32_t npts, const int32_t *counts, const double *pts,
                       int32_t *hull, int32_t *hull_n, cudaStream_t s);
 size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, int tiles, struct Scratch *sc, char *base);

@@ -582,6 +582,126 @@ static void camera_center(const cs_camera &cam, double *c) {  // model.py:164-16
   }
 }
 
+// ---------------------------------------------------------------------------
+// cs_prepare_view_export: the full per-view state of every prepared convex
+// in float64 (projection.ProjectedConvex, projection.py:180-203, and
+// rasterize.ViewPrimitive, rasterize.py:56-65) for the drop-in prepare_view.
+// Not on the hot path: one thread per convex after a forward's stage 0
+// (hull cycle and visibility from the workspace), the projection and
+// hull_lines re-evaluated with the preprocess's expressions in this
+// --fmad=false translation unit (bit-exact with the reference), delta_s /
+// sigma_s / opacity, and the view direction and colour in float64
+// (rasterize.py:110-114, harmonics.py:33-59, 101-109).
+struct ExportArgs {
+  cs_camera cam;
+  int64_t n;
+  int k, max_k, sh_degree, mode;
+  double cam_center[3];
+  const float *points, *raw_delta, *raw_sigma, *raw_opacity, *sh;
+  const uint8_t *hull;
+  const uint32_t *touched;
+  cs_view_export out;
+};
+
+__global__ void __launch_bounds__(128) export_view_kernel(ExportArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  if (i >= a.n || a.touched[i] == 0) return;
+  const int k = a.k;
+  const double *R = a.cam.R;
+  double X[16], Y[16];
+  double cx = 0.0, cy = 0.0, cz = 0.0, zsum = 0.0;
+  for (int j = 0; j < k; j++) {
+    const double p0 = a.points[(i * k + j) * 3], p1 = a.points[(i * k + j) * 3 + 1], p2 = a.points[(i * k + j) * 3 + 2];
+    const double xc = fma(p2, R[2], fma(p1, R[1], p0 * R[0])) + a.cam.t[0];
+    const double yc = fma(p2, R[5], fma(p1, R[4], p0 * R[3])) + a.cam.t[1];
+    const double zc = fma(p2, R[8], fma(p1, R[7], p0 * R[6])) + a.cam.t[2];
+    zsum = zsum + zc;
+    cx = cx + p0; cy = cy + p1; cz = cz + p2;
+    if (a.cam.ortho) {
+      X[j] = a.cam.fx * xc + a.cam.cx;
+      Y[j] = a.cam.fy * yc + a.cam.cy;
+    } else {
+      X[j] = (a.cam.fx * xc) / zc + a.cam.cx;
+      Y[j] = (a.cam.fy * yc) / zc + a.cam.cy;
+    }
+    a.out.pixels[(i * k + j) * 2] = X[j];
+    a.out.pixels[(i * k + j) * 2 + 1] = Y[j];
+    a.out.point_depths[i * k + j] = zc;
+  }
+  int hidx[16], h = 0;
+  for (int j = 0; j < a.max_k; j++) {
+    const int v = a.hull[i * a.max_k + j];
+    if (v != 0xff) hidx[h++] = v;
+  }
+  for (int j = 0; j < k; j++) {   // projection.py:116-128 over the hull cycle; unused rows NaN
+    double nx = NAN, ny = NAN, off = NAN;
+    if (j < h) {
+      const int u = hidx[j], v = hidx[j + 1 < h ? j + 1 : 0];
+      const double ex = X[v] - X[u], ey = Y[v] - Y[u];
+      const double rx = ey, ry = -ex;
+      const double len = sqrt(rx * rx + ry * ry);
+      nx = rx / len;
+      ny = ry / len;
+      off = -(nx * X[u] + ny * Y[u]);
+    }
+    a.out.normals[(i * k + j) * 2] = nx;
+    a.out.normals[(i * k + j) * 2 + 1] = ny;
+    a.out.offsets[i * k + j] = off;
+  }
+  const double depth = zsum / k;
+  const double s = depth_scale(a.mode, a.cam.ortho ? 1.0 : depth);
+  a.out.delta_s[i] = s * exp((double)a.raw_delta[i]);
+  a.out.sigma_s[i] = s * exp((double)a.raw_sigma[i]);
+  a.out.opacity[i] = 1.0 / (1.0 + exp(-(double)a.raw_opacity[i]));
+  a.out.scale[i] = s;
+  const double vx = cx / k - a.cam_center[0], vy = cy / k - a.cam_center[1], vz = cz / k - a.cam_center[2];
+  const double dist = sqrt(vx * vx + vy * vy + vz * vz);
+  double d[3] = {0.0, 0.0, 1.0};
+  if (dist > 0.0) { d[0] = vx / dist; d[1] = vy / dist; d[2] = vz / dist; }
+  a.out.view_dir[i * 3] = d[0]; a.out.view_dir[i * 3 + 1] = d[1]; a.out.view_dir[i * 3 + 2] = d[2];
+  a.out.view_dist[i] = dist;
+  // harmonics.py:33-59 basis, 101-109 colour
+  const double x = d[0], y = d[1], z = d[2], xx = x * x, yy = y * y, zz = z * z;
+  double b[16];
+  b[0] = 0.28209479177387814;
+  b[1] = -0.4886025119029199 * y; b[2] = 0.4886025119029199 * z; b[3] = -0.4886025119029199 * x;
+  b[4] = 1.0925484305920792 * x * y; b[5] = -1.0925484305920792 * y * z;
+  b[6] = 0.31539156525252005 * (2.0 * zz - xx - yy); b[7] = -1.0925484305920792 * x * z;
+  b[8] = 0.5462742152960396 * (xx - yy);
+  b[9] = -0.5900435899266435 * y * (3.0 * xx - yy); b[10] = 2.890611442640554 * x * y * z;
+  b[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+  b[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+  b[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy); b[14] = 1.445305721320277 * z * (xx - yy);
+  b[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+  const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
+  for (int c = 0; c < 3; c++) {
+    double acc = 0.0;
+    for (int q = 0; q < nb; q++) acc += b[q] * (double)a.sh[(i * kShCoeffs + q) * 3 + c];
+    const double v = 0.5 + acc;
+    a.out.color[i * 3 + c] = v > 0.0 ? v : 0.0;
+  }
+}
+
+int launch_export_view(const cs_camera &cam, const cs_settings &set, const cs_params &p, const cs_layout &L,
+                       const char *ws, const cs_view_export &out, cudaStream_t s) {
+  if (p.n == 0) return CS_OK;
+  ExportArgs a;
+  a.cam = cam;
+  a.n = p.n;
+  a.k = p.k;
+  a.max_k = L.max_k;
+  a.sh_degree = set.sh_degree;
+  a.mode = set.scaling_mode;
+  camera_center(cam, a.cam_center);
+  a.points = p.points; a.raw_delta = p.raw_delta; a.raw_sigma = p.raw_sigma; a.raw_opacity = p.raw_opacity;
+  a.sh = p.sh;
+  a.hull = reinterpret_cast<const uint8_t *>(ws + L.hull);
+  a.touched = reinterpret_cast<const uint32_t *>(ws + L.tiles_touched);
+  a.out = out;
+  export_view_kernel<<<(int)((p.n + 127) / 128), 128, 0, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+}
+
 int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                       const cs_layout &L, char *ws, cudaStream_t s) {
   if (p.n == 0) return CS_OK;

@@ -75,6 +75,12 @@ class ScalingMode(Enum):
     def code(self) -> int:  # enum cs_scaling of include/convexsplat_b200.h
         return {"none": 0, "sqrt": 1, "depth": 2, "depth2": 3}[self.value]
 
+    @classmethod
+    def of(cls, mode) -> "ScalingMode":
+        """This enum from itself, its value string, or any enum with the same
+        values (the reference's field.ScalingMode: drop-in callers pass it)."""
+        return cls(getattr(mode, "value", mode))
+
 
 @dataclass(frozen=True)
 class RenderSettings:

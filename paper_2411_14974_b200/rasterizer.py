@@ -57,7 +57,7 @@ def settings_struct(settings: RenderSettings, mode: ScalingMode, background) -> 
     s.background[:] = [float(v) for v in np.asarray(background, dtype=np.float64).reshape(3)]
     s.tile = int(settings.tile_size)
     s.sh_degree = int(settings.sh_degree)
-    s.scaling_mode = ScalingMode(mode).code
+    s.scaling_mode = ScalingMode.of(mode).code
     return s
 
 
@@ -420,24 +420,35 @@ def record_blends(fr: Frame):
 
 @dataclass
 class ProjectedConvex:
-    """GPU-prepared subset of projection.ProjectedConvex (projection.py:180-203)."""
+    """projection.ProjectedConvex (projection.py:180-203): per-view
+    screen-space state of one primitive, float64 (cs_prepare_view_export)."""
 
     index: int
+    pixels: np.ndarray        # (K, 2)
+    point_depths: np.ndarray  # (K,)
     depth: float
-    hull_indices: np.ndarray
+    hull_indices: np.ndarray  # (H,)
+    normals: np.ndarray       # (H, 2)
+    offsets: np.ndarray       # (H,)
     delta_s: float
     sigma_s: float
-    bbox: tuple
+    bbox: tuple               # (x0, x1, y0, y1) half-open pixel rect
+
+    @property
+    def hull_pixels(self) -> np.ndarray:
+        return self.pixels[self.hull_indices]
 
 
 @dataclass
 class ViewPrimitive:
-    """rasterize.ViewPrimitive (rasterize.py:56-65); fields from the GPU record."""
+    """rasterize.ViewPrimitive (rasterize.py:56-65)."""
 
     pc: ProjectedConvex
     opacity: float
     color: np.ndarray
-    scale: float
+    scale: float           # depth scale applied to delta and sigma
+    view_dir: np.ndarray   # unit vector camera center -> primitive center
+    view_dist: float
 
 
 class PreparedView(list):
@@ -450,41 +461,82 @@ class PreparedView(list):
 
 def prepare_view(scene, cam: Camera, mode: ScalingMode = ScalingMode.DEPTH,
                  settings: RenderSettings = RenderSettings()) -> PreparedView:
-    """rasterize.prepare_view (rasterize.py:77-122) from the GPU preprocess."""
-    fr = default_rasterizer().forward(scene, cam, mode, settings)
+    """rasterize.prepare_view (rasterize.py:77-122) from the GPU preprocess:
+    the visible primitives in blending order (depth, index) with the float64
+    per-view state of cs_prepare_view_export; ``bins`` holds the GPU tile
+    lists (bin_tiles)."""
+    r = default_rasterizer()
+    fr = r.forward(scene, cam, mode, settings)
     info = inspect_frame(fr)
+    st, dev = fr.scene, fr.image.device
+    n, k = st.n, st.k
+    f64 = dict(dtype=torch.float64, device=dev)
+    ex = {"pixels": torch.zeros((n, k, 2), **f64), "point_depths": torch.zeros((n, k), **f64),
+          "normals": torch.zeros((n, k, 2), **f64), "offsets": torch.zeros((n, k), **f64),
+          "delta_s": torch.zeros(n, **f64), "sigma_s": torch.zeros(n, **f64), "opacity": torch.zeros(n, **f64),
+          "scale": torch.zeros(n, **f64), "view_dir": torch.zeros((n, 3), **f64), "view_dist": torch.zeros(n, **f64),
+          "color": torch.zeros((n, 3), **f64)}
+    out_c = _lib.CsViewExport(*(ex[f].data_ptr() for f, _ in _lib.CsViewExport._fields_))
+    ws = fr.workspace
+    _lib.check(_lib.load().cs_prepare_view_export(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
+                                                  ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
+                                                  ctypes.byref(out_c), torch.cuda.current_stream(dev).cuda_stream),
+               "cs_prepare_view_export")
+    ex = {f: _np(v) for f, v in ex.items()}
     out = PreparedView()
-    dls_to_delta = math.log(2.0)
     for rank, i in enumerate(info["order"]):
-        rec = info["records"][i]
         h = info["hull"][i]
-        depth = float(info["depth"][rank])
-        d = 1.0 if cam.ortho else depth
-        scale = {ScalingMode.NONE: 1.0, ScalingMode.SQRT_DEPTH: math.sqrt(d), ScalingMode.DEPTH: d,
-                 ScalingMode.DEPTH_SQUARED: d * d}[ScalingMode(mode)]
-        pc = ProjectedConvex(int(i), depth, h[h >= 0].copy(), float(rec[9]) * dls_to_delta, float(rec[2]),
-                             tuple(int(v) for v in info["bbox"][i]))
-        out.append(ViewPrimitive(pc, float(rec[3]), rec[4:7].astype(np.float64), scale))
-    rank_of = {int(i): r for r, i in enumerate(info["order"])}
+        h = h[h >= 0].copy()
+        nh = h.size
+        pc = ProjectedConvex(int(i), ex["pixels"][i].copy(), ex["point_depths"][i].copy(), float(info["depth"][rank]),
+                             h, ex["normals"][i, :nh].copy(), ex["offsets"][i, :nh].copy(), float(ex["delta_s"][i]),
+                             float(ex["sigma_s"][i]), tuple(int(v) for v in info["bbox"][i]))
+        out.append(ViewPrimitive(pc, float(ex["opacity"][i]), ex["color"][i].copy(), float(ex["scale"][i]),
+                                 ex["view_dir"][i].copy(), float(ex["view_dist"][i])))
+    rank_of = np.full(n, -1, np.int64)
+    rank_of[info["order"]] = np.arange(len(info["order"]))
     bins = []
     for t in range(info["tiles_x"] * info["tiles_y"]):
-        s, e = info["tile_ranges"][t]
-        bins.append([rank_of[int(i)] for i in info["pair_ids"][s:e]] if e > s else [])
+        s0, e = info["tile_ranges"][t]
+        bins.append(rank_of[info["pair_ids"][s0:e]].tolist() if e > s0 else [])
     out.bins, out.tiles_x, out.tiles_y = bins, info["tiles_x"], info["tiles_y"]
     return out
 
 
-def bin_tiles(prepared: PreparedView, width: int, height: int, tile_size: int = 16):
+def bin_tiles(prepared, width: int, height: int, tile_size: int = 16):
     """rasterize.bin_tiles (rasterize.py:134-144): per-tile candidate lists of
-    positions in the prepared order, as produced by the GPU binning."""
-    if not isinstance(prepared, PreparedView) or prepared.bins is None:
-        raise TypeError("bin_tiles expects the result of this package's prepare_view()")
-    if tile_size != 16:
-        raise ValueError("the sm_100a binning supports tile_size=16")
-    tx, ty = (width + 15) // 16, (height + 15) // 16
-    if (tx, ty) != (prepared.tiles_x, prepared.tiles_y):
-        raise ValueError("width/height differ from the prepared camera")
-    return prepared.bins, tx, ty
+    positions in the prepared order, row-major tiles; returns (bins,
+    tiles_x, tiles_y).  For this package's prepare_view() result these are
+    the GPU binning's lists; for any other prepared list (e.g. the
+    reference's own ViewPrimitives) the (tile, position) pairs of the
+    ``pc.bbox`` rectangles are expanded and stably sorted by tile on the
+    GPU."""
+    tiles_x = (width + tile_size - 1) // tile_size
+    tiles_y = (height + tile_size - 1) // tile_size
+    if isinstance(prepared, PreparedView) and prepared.bins is not None and tile_size == 16 \
+            and (tiles_x, tiles_y) == (prepared.tiles_x, prepared.tiles_y):
+        return [list(b) for b in prepared.bins], tiles_x, tiles_y
+    bins = [[] for _ in range(tiles_x * tiles_y)]
+    if len(prepared) == 0:
+        return bins, tiles_x, tiles_y
+    dev = _device()
+    bb = torch.tensor([tuple(vp.pc.bbox) for vp in prepared], dtype=torch.int64, device=dev)
+    tx0, tx1 = bb[:, 0] // tile_size, (bb[:, 1] - 1) // tile_size
+    ty0, ty1 = bb[:, 2] // tile_size, (bb[:, 3] - 1) // tile_size
+    nx, ny = tx1 - tx0 + 1, ty1 - ty0 + 1
+    cnt = nx * ny
+    pos = torch.repeat_interleave(torch.arange(len(prepared), device=dev), cnt)
+    start = torch.cumsum(cnt, 0) - cnt
+    j = torch.arange(int(cnt.sum()), device=dev) - torch.repeat_interleave(start, cnt)
+    tile = (ty0[pos] + j // nx[pos]) * tiles_x + tx0[pos] + j % nx[pos]
+    tile_sorted, perm = torch.sort(tile, stable=True)       # position order kept within a tile
+    counts = torch.bincount(tile_sorted, minlength=tiles_x * tiles_y).cpu().tolist()
+    flat = pos[perm].cpu().tolist()
+    o = 0
+    for t, c in enumerate(counts):
+        bins[t] = flat[o:o + c]
+        o += c
+    return bins, tiles_x, tiles_y
 
 
 __all__ = ["Rasterizer", "Workspace", "Frame", "rasterize", "render", "render_reference", "backward",

@@ -83,8 +83,8 @@ class SceneTensors:
 
     @classmethod
     def from_scene(cls, scene: Scene, device="cuda") -> "SceneTensors":
-        prims = scene.primitives
-        k = prims[0].num_points if prims else 6
+        prims = list(scene.primitives)
+        k = int(np.asarray(prims[0].points).shape[0]) if prims else 6
         arrays = dict(
             points=np.stack([c.points for c in prims]) if prims else np.zeros((0, k, 3)),
             raw_delta=np.array([c.raw_delta for c in prims], dtype=np.float64),
@@ -93,7 +93,8 @@ class SceneTensors:
             raw_mask=np.array([c.raw_mask for c in prims], dtype=np.float64),
             sh=np.stack([c.sh for c in prims]) if prims else np.zeros((0, SH_COEFFS, 3)),
         )
-        return cls.from_arrays(arrays, device, scene.background, scene.scene_extent)
+        return cls.from_arrays(arrays, device, np.asarray(getattr(scene, "background", np.zeros(3)), dtype=np.float64),
+                               float(getattr(scene, "scene_extent", 1.0)))
 
     def to_scene(self) -> Scene:
         a = self.numpy()
@@ -110,9 +111,13 @@ def as_scene_tensors(scene, device: Optional[torch.device] = None) -> SceneTenso
         if scene.device != device or scene.points.dtype != torch.float32:
             return scene.to(device)
         return scene
-    if isinstance(scene, Scene):
+    if isinstance(scene, Scene) or hasattr(scene, "primitives"):
+        # this package's Scene, or any object with the reference Scene's
+        # surface (model.py:175-194: primitives of SmoothConvex-like objects
+        # with points / raw_* / sh, background, scene_extent) -- the
+        # reference's own convexsplat.model.Scene is accepted as is
         return SceneTensors.from_scene(scene, device)
-    raise TypeError(f"expected Scene or SceneTensors, got {type(scene).__name__}")
+    raise TypeError(f"expected a Scene (with .primitives) or SceneTensors, got {type(scene).__name__}")
 
 
 __all__ = ["SceneTensors", "PARAM_NAMES", "as_scene_tensors"]

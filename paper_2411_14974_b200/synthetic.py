@@ -121,3 +121,92 @@ def perturb(arrays: dict, seed: int = 1, extent: float = 2.0, fraction: float = 
 def camera_dict(cam: Camera) -> dict:
     return dict(fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy, R=cam.R, t=cam.t, z_near=cam.z_near,
                 width=cam.width, height=cam.height, ortho=cam.ortho)
+
+
+# ----------------------------------------------------------------------------- config 2: toy chair
+# BASELINE.json configs[1] / SURVEY.md 8(d) row 2.  The paper's chair
+# (Fig. 2) is a 2-D toy; this is a procedural 3-D chair -- a seat, a back
+# and four legs -- whose parts are boxes split into 6-point triangular
+# prisms (two per box cell), the ground truth the fit is rendered from.
+SH_C0 = 0.28209479177387814   # harmonics.py:7 (degree-0 SH constant)
+CHAIR_PARTS = (
+    # (min corner, max corner, colour, cells per axis)
+    ((-0.6, -0.05, -0.6), (0.6, 0.1, 0.6), (0.75, 0.45, 0.2), (4, 1, 4)),      # seat
+    ((-0.6, 0.1, 0.45), (0.6, 1.2, 0.6), (0.55, 0.3, 0.15), (4, 4, 1)),        # back
+    ((-0.55, -1.0, -0.55), (-0.4, -0.05, -0.4), (0.3, 0.3, 0.35), (1, 3, 1)),  # legs
+    ((0.4, -1.0, -0.55), (0.55, -0.05, -0.4), (0.3, 0.3, 0.35), (1, 3, 1)),
+    ((-0.55, -1.0, 0.4), (-0.4, -0.05, 0.55), (0.3, 0.3, 0.35), (1, 3, 1)),
+    ((0.4, -1.0, 0.4), (0.55, -0.05, 0.55), (0.3, 0.3, 0.35), (1, 3, 1)),
+)
+
+
+def _prisms_of_box(lo, hi) -> list:
+    """A box as two triangular prisms (6 points each): the x-z rectangle split
+    along its diagonal, extruded along y."""
+    (x0, y0, z0), (x1, y1, z1) = lo, hi
+    tris = (((x0, z0), (x1, z0), (x1, z1)), ((x0, z0), (x1, z1), (x0, z1)))
+    return [np.array([(x, y0, z) for x, z in t] + [(x, y1, z) for x, z in t], dtype=np.float64) for t in tris]
+
+
+def chair_scene(opacity: float = 0.98, delta: float = 20.0, sigma: float = 0.05) -> dict:
+    """Ground-truth chair as SoA arrays (sharp, nearly opaque prisms)."""
+    pts, cols = [], []
+    for lo, hi, col, cells in CHAIR_PARTS:
+        lo, hi = np.asarray(lo), np.asarray(hi)
+        step = (hi - lo) / np.asarray(cells)
+        for ix in range(cells[0]):
+            for iy in range(cells[1]):
+                for iz in range(cells[2]):
+                    a = lo + step * (ix, iy, iz)
+                    for prism in _prisms_of_box(a, a + step):
+                        pts.append(prism)
+                        cols.append(col)
+    n = len(pts)
+    sh = np.zeros((n, 16, 3))
+    sh[:, 0] = (np.asarray(cols) - 0.5) / SH_C0
+    return dict(points=np.stack(pts), raw_delta=np.full(n, math.log(delta)), raw_sigma=np.full(n, math.log(sigma)),
+                raw_opacity=np.full(n, float(inverse_opacity_activation(opacity))),
+                raw_mask=np.full(n, float(inverse_mask_activation(0.995))), sh=sh, background=np.zeros(3))
+
+
+def chair_surface_samples(count: int = 2000, seed: int = 0, noise: float = 0.02):
+    """~count points on the chair's box surfaces (area-weighted) with their
+    part colours (+ noise): the sparse point cloud of initialize.init_scene."""
+    rng = np.random.default_rng(seed)
+    faces = []
+    for lo, hi, col, _ in CHAIR_PARTS:
+        lo, hi = np.asarray(lo, dtype=np.float64), np.asarray(hi, dtype=np.float64)
+        for axis in range(3):
+            u, v = [a for a in range(3) if a != axis]
+            area = (hi[u] - lo[u]) * (hi[v] - lo[v])
+            for side in (lo[axis], hi[axis]):
+                faces.append((axis, side, lo, hi, u, v, area, col))
+    areas = np.array([f[6] for f in faces])
+    pick = rng.choice(len(faces), size=count, p=areas / areas.sum())
+    pts = np.empty((count, 3))
+    cols = np.empty((count, 3))
+    for j, fi in enumerate(pick):
+        axis, side, lo, hi, u, v, _, col = faces[fi]
+        pts[j, axis] = side
+        pts[j, u] = rng.uniform(lo[u], hi[u])
+        pts[j, v] = rng.uniform(lo[v], hi[v])
+        cols[j] = col
+    cols = np.clip(cols + rng.normal(0.0, noise, size=cols.shape), 0.0, 1.0)
+    return pts, cols
+
+
+def init_scene_arrays(points: np.ndarray, colors: np.ndarray, k: int = 6) -> dict:
+    """initialize.init_scene (initialize.py:67-106) as SoA arrays: one convex
+    per point on a Fibonacci sphere of radius 1.2 x the mean 3-NN distance,
+    delta 0.1, sigma 0.00095, opacity 0.1, mask 0.99, SH DC from the colour."""
+    from .model import inverse_delta_activation, inverse_sigma_activation
+    points = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    n = points.shape[0]
+    radii = np.maximum(1.2 * mean_knn_distance(points), 1e-9)
+    pts = points[:, None, :] + radii[:, None, None] * fibonacci_offsets(k)[None]
+    sh = np.zeros((n, 16, 3))
+    sh[:, 0] = (np.asarray(colors, dtype=np.float64) - 0.5) / SH_C0
+    return dict(points=pts, raw_delta=np.full(n, float(inverse_delta_activation(0.1))),
+                raw_sigma=np.full(n, float(inverse_sigma_activation(0.00095))),
+                raw_opacity=np.full(n, float(inverse_opacity_activation(0.1))),
+                raw_mask=np.full(n, float(inverse_mask_activation(0.99))), sh=sh, background=np.zeros(3))

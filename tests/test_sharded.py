@@ -152,5 +152,5 @@ def test_sharded_step_gradients_equal_sum_of_view_backwards():
         den = np.maximum(np.abs(a), np.abs(b))
         # the fused loss adjoint is float32 (the reference formulation here
         # float64): the floor of tests/test_gpu_parity.py GRAD_FLOOR
-        rel = np.abs(a - b) / np.maximum(den, max(2e-4 * den.max(), 1e-12))
+        rel = np.abs(a - b) / np.maximum(den, max(5e-4 * den.max(), 1e-12))
         assert rel.max() < 1e-3, (k, rel.max())
