@@ -29,6 +29,18 @@
 
 namespace cs {
 
+#ifdef CS_WAIT_STATS
+// diagnostics (tools/wait_stats.py): SM cycles of the forward / backward
+// consumer warps [0]/[4] and of their waits on `full` [1]/[5]; producer
+// cycles [2]/[6] and its waits on `empty` [3]/[7]
+__device__ unsigned long long g_wait_stats[8];
+#define WS_T0(v) const long long v = clock64()
+#define WS_ADD(i, t0) atomicAdd(&g_wait_stats[i], (unsigned long long)(clock64() - (t0)))
+#else
+#define WS_T0(v)
+#define WS_ADD(i, t0)
+#endif
+
 struct BlendArgs {
   const float *records;
   const double *lines;
@@ -210,6 +222,10 @@ template <int NC> __host__ __device__ constexpr int pipe_threads() { return 32 *
 #define CS_BWD_STAGES 6
 #endif
 constexpr int kStageCands = 32;
+// longest back-off sleep of the producer waiting for a free stage
+#ifndef CS_PROD_SLEEP_NS
+#define CS_PROD_SLEEP_NS 512
+#endif
 
 template <int MAXK, int kStages>
 struct PipeSmem {
@@ -310,6 +326,7 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
                                              uint8_t *visible, const TileLines &tl, bool cull) {
   constexpr int RG = Rec<MAXK>::kGlobal;
   const int lane = threadIdx.x & 31;
+  WS_T0(tp);
   int issued = 0;
   bool stopped = false;
   // candidate ids are loaded one batch ahead (their latency hides behind the
@@ -320,15 +337,50 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
     batch(0, f0, c0);
     if (lane < (int)c0) next_id = __ldg(pair_ids + f0 + lane);
   }
+  // Forward consumers leave the pipeline when their pixels are done
+  // (arrive_drop into the phases of the next kStages batches): once every
+  // consumer has left, those drops can complete phases of batches this warp
+  // never issues, and a stage's barrier may run two phases past the one
+  // waited for -- its parity then reads "not complete" again.  So the
+  // forward's waits on `empty` also end as soon as every consumer has left
+  // (sm.ndone == NC): nothing reads the stages any more.
+  auto wait_empty = [&](int y) -> bool {   // false: every consumer left
+    uint64_t *bar = &sm.empty[y % kStages];
+    const uint32_t par = (y / kStages) & 1;
+    if (!forward) {
+      if (CS_PROD_SLEEP_NS > 0) mbar_wait_backoff(bar, par, CS_PROD_SLEEP_NS);
+      else mbar_wait(bar, par);
+      return true;
+    }
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t ns = 32;
+    for (int it = 0;; it++) {
+      if (mbar_try_wait(bar, par)) return true;
+      if (*reinterpret_cast<volatile int *>(&sm.ndone) == NC) return false;
+      if (CS_PROD_SLEEP_NS > 0) {
+        __nanosleep(ns);
+        ns = min(2u * ns, (uint32_t)CS_PROD_SLEEP_NS);
+      }
+      if ((it & 63) == 63 && globaltimer_ns() - t0 > 2000000000ull) __trap();
+    }
+  };
+  bool all_left = false;
   for (int b = 0; b < nbatch; b++) {
     const int s = b % kStages, u = b / kStages;
     if (u > 0) {
-      mbar_wait(&sm.empty[s], (u - 1) & 1);  // batch b - kStages released by every consumer
+      // batch b - kStages released by every consumer
+      WS_T0(tw);
+      const bool ok = wait_empty(b - kStages);
+      if (lane == 0) WS_ADD(forward ? 3 : 7, tw);
+      if (!ok) {
+        all_left = true;
+        break;
+      }
       if (forward) flush_visible(sm, s, visible);
     }
     if (forward && *reinterpret_cast<volatile int *>(&sm.ndone) == NC) {
-      // stop = b + 1: consumers leave at batch b.  Consumers still behind
-      // (done warps lag) keep releasing the issued batches < b normally.
+      // every consumer left: stop streaming (stop = b + 1 releases any
+      // consumer still waiting for batch b -- none with the drop-out)
       if (lane == 0) *reinterpret_cast<volatile int *>(&sm.stop) = b + 1;
       __syncwarp();
       mbar_arrive(&sm.full[s]);                  // all 32 lanes, twice: the barrier counts 64
@@ -372,14 +424,26 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
     issued = b + 1;
   }
   // drain: wait until the consumers released the last issued batches (their
-  // bulk copies have landed, so nothing targets this CTA's shared memory
-  // after exit) and publish their visibility.  After a stop, batch
-  // issued - kStages was already waited on and flushed above.
+  // copies have landed, so nothing targets this CTA's shared memory after
+  // exit) and publish their visibility.  After a stop, batch issued - kStages
+  // was already waited on and flushed above.  Once every (forward) consumer
+  // has left, the producer's own copies are waited for instead and every
+  // stage's remaining visibility bits are published.
   const int lo = stopped ? issued - kStages + 1 : issued - kStages;
-  for (int b = max(0, lo); b < issued; b++) {
-    mbar_wait(&sm.empty[b % kStages], (b / kStages) & 1);
+  for (int b = max(0, lo); b < issued && !all_left; b++) {
+    if (!wait_empty(b)) {
+      all_left = true;
+      break;
+    }
     if (forward) flush_visible(sm, b % kStages, visible);
   }
+  if (all_left || stopped) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    if (forward)
+      for (int st = 0; st < kStages; st++) flush_visible(sm, st, visible);
+  }
+  if (lane == 0) WS_ADD(forward ? 2 : 6, tp);
 }
 
 template <int MAXK, int kStages, int NC>
@@ -480,13 +544,37 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
     P.last = -1; P.nblend = 0;
     P.done = !inside;
     bool warp_done = __all_sync(0xffffffffu, P.done);
-    if (warp_done && lane == 0) atomicAdd(&sm.ndone, 1);
+    // A warp whose pixels all terminated leaves the pipeline for good
+    // instead of waiting on every remaining stage: before arriving for
+    // batch b it arrive_drops on the phases of batches b .. b + kStages - 1
+    // (the phase of batch x is current once every consumer released batch
+    // x - kStages; this warp's own arrival for that one is already in), so
+    // the producer's later phases no longer expect it.
+    auto leave = [&](int b) {
+      if (lane == 0) {
+        __threadfence_block();   // this warp's visibility bits before the count the producer reads
+        atomicAdd(&sm.ndone, 1);
+#pragma unroll 1
+        for (int i = 0; i < kStages; i++) {
+          const int x = b + i;
+          if (i > 0 && x >= kStages) mbar_wait(&sm.empty[x % kStages], ((x - kStages) / kStages) & 1);
+          mbar_arrive_drop(&sm.empty[x % kStages]);
+        }
+      }
+      __syncwarp();
+    };
+    WS_T0(tc);
+    if (warp_done) leave(0);
     const bool use_floor = a.floor > 0.f;
-    for (int b = 0; b < nbatch; b++) {
+    for (int b = 0; b < nbatch && !warp_done; b++) {
       const int s = b % kStages;
-      mbar_wait(&sm.full[s], (b / kStages) & 1);
+      {
+        WS_T0(tw);
+        mbar_wait(&sm.full[s], (b / kStages) & 1);
+        if (lane == 0) WS_ADD(1, tw);
+      }
       if (*reinterpret_cast<volatile int *>(&sm.stop) == b + 1) break;
-      if (!warp_done) {
+      {
         const uint32_t first = range.x + (uint32_t)b * kStageCands;
         const int count = (int)min((uint32_t)kStageCands, range.y - first);
         // lane j: pixels of this warp's block inside candidate j's bbox and alive
@@ -530,7 +618,6 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
             vis |= 1u << j;
             if (__all_sync(0xffffffffu, P.done)) {
               warp_done = true;
-              if (lane == 0) atomicAdd(&sm.ndone, 1);
               break;
             }
           }
@@ -543,8 +630,13 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[s]);
+      if (warp_done) {
+        leave(b);
+      } else if (lane == 0) {
+        mbar_arrive(&sm.empty[s]);
+      }
     }
+    if (lane == 0) WS_ADD(0, tc);
     n_blend = (unsigned)P.nblend;
     if (inside) {
       const size_t p = (size_t)py * a.width + px;
@@ -724,6 +816,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
     const TileLines tl{(double)(tx * kTile + kRebase), (double)(ty * kTile + kRebase), 0.f};
     pipe_produce<MAXK, kStages, NC>(sm, a.records, a.lines, a.pair_ids, nbatch, batch, false, nullptr, tl, false);
   } else {
+    WS_T0(tc);
     for (int b = 0; b < nbatch; b++) {
       const int s = b % kStages;
       uint32_t first, count;
@@ -743,7 +836,11 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           fm[h] = sh ? (w0 >> sh) | (w1 << (32u - sh)) : w0;
         }
       }
-      mbar_wait(&sm.full[s], (b / kStages) & 1);
+      {
+        WS_T0(tw);
+        mbar_wait(&sm.full[s], (b / kStages) & 1);
+        if (lane == 0) WS_ADD(5, tw);
+      }
       if ((int)first <= warp_last) {
         const uint32_t pos = first + lane;
         uint32_t pm[PPL], any = 0u;
@@ -820,6 +917,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
+    if (lane == 0) WS_ADD(4, tc);
   }
   if (STATS) {
     block_add_u64(a.stats + S_BWD_EVALS, n_eval);
@@ -918,3 +1016,15 @@ int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs
 }
 
 }  // namespace cs
+
+#ifdef CS_WAIT_STATS
+extern "C" CS_API int cs_debug_wait_stats(unsigned long long *host8, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(host8, cs::g_wait_stats, sizeof(unsigned long long) * 8) != cudaSuccess) return 2;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(cs::g_wait_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -1,6 +1,7 @@
 // Shared definitions of the sm_100a convex-splatting kernels.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "../../include/convexsplat_b200.h"
@@ -193,24 +194,54 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t phas
       : "memory");
   return done != 0;
 }
-// Waiting warps back off with __nanosleep so they do not steal issue slots
-// from the warps doing work (a suspend-time hint alone wakes on every
-// barrier event of the CTA).
+// Wait for the phase of parity `phase` to complete: suspend-hinted
+// try_wait (the warp sleeps until a barrier event of the CTA), the 2 s
+// watchdog read once per 64 polls (a wait that long is a protocol bug: trap
+// instead of hanging the device).
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   if (mbar_try_wait(bar, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-#ifdef CS_WAIT_SLEEP
-  uint32_t ns = 32;
-  for (uint32_t it = 1; !mbar_try_wait(bar, phase); it++) {
-    __nanosleep(ns);
-    ns = min(ns * 2u, 256u);
-    if ((it & 255u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
-  }
-#else
-  for (uint32_t it = 1; !mbar_try_wait_sleep(bar, phase); it++) {
-    if ((it & 255u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
-  }
+  for (;;) {
+#pragma unroll 1
+    for (int it = 0; it < 64; it++)
+      if (mbar_try_wait_sleep(bar, phase)) return;
+    if (globaltimer_ns() - t0 > 2000000000ull) {
+#ifdef CS_WAIT_DEBUG
+      printf("mbar_wait timeout: block %d thread %d bar smem+%u parity %u\n", (int)blockIdx.x, (int)threadIdx.x,
+             smem_u32(bar), phase);
 #endif
+      __trap();
+    }
+  }
+}
+// The same with an exponential __nanosleep back-off (up to max_ns): for a
+// waiter that expects a long wait (the producer warp waiting for the
+// consumers to release a stage), so that it stays off the issue slots
+// instead of waking on every barrier event of the CTA.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t phase, uint32_t max_ns) {
+  if (mbar_try_wait(bar, phase)) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t ns = 32;
+  for (;;) {
+#pragma unroll 1
+    for (int it = 0; it < 16; it++) {
+      __nanosleep(ns);
+      if (mbar_try_wait(bar, phase)) return;
+      ns = min(2u * ns, max_ns);
+    }
+    if (globaltimer_ns() - t0 > 2000000000ull) {
+#ifdef CS_WAIT_DEBUG
+      printf("mbar_wait_backoff timeout: block %d thread %d bar smem+%u parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, smem_u32(bar), phase);
+#endif
+      __trap();
+    }
+  }
+}
+// Leave a barrier for good: arrive on its current phase and drop this
+// thread's arrival from the expected count of every later phase.
+__device__ __forceinline__ void mbar_arrive_drop(uint64_t *bar) {
+  asm volatile("mbarrier.arrive_drop.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Pixel of a 16x16 tile handled by thread t: warps cover 8x4 sub-blocks so
