@@ -284,6 +284,7 @@ __device__ __forceinline__ uint32_t stage_lines(const float *rec_g, const double
   float lb[8];
 #pragma unroll
   for (int q = 0; q < 8; q++) lb[q] = -INFINITY;
+  float mag = 0.f;   // largest |C'| + 8 |A| + 8 |B|: the float32 evaluation error of z is ~2^-23 of it
 #pragma unroll
   for (int l = 0; l < MAXK; l++) {
     if (l < nl) {
@@ -294,6 +295,7 @@ __device__ __forceinline__ uint32_t stage_lines(const float *rec_g, const double
       Bs[l] = Bf;
       Cs[l] = Cf;
       if (cull) {
+        mag = fmaxf(mag, fabsf(Cf) + 8.f * (fabsf(Af) + fabsf(Bf)));
 #pragma unroll
         for (int q = 0; q < 8; q++) {
           const float xl = d0 + (float)((q & 1) * 8), yl = d0 + (float)((q >> 1) * 4);
@@ -308,7 +310,7 @@ __device__ __forceinline__ uint32_t stage_lines(const float *rec_g, const double
 #pragma unroll
     for (int q = 0; q < 8; q++) {
       const float v = h0.z * lb[q];
-      if (v - thr > 1e-3f * (1.f + fabsf(thr) + fabsf(v))) m &= ~(1u << q);
+      if (v - thr > 1e-3f * (1.f + fabsf(thr) + fabsf(v)) + h0.z * mag * 0x1p-18f) m &= ~(1u << q);
     }
   }
   return m;
@@ -794,10 +796,15 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
       P[h].S2 = P[h].T * a.bg[2];
     }
   }
-  int lmax = P[0].last;
+  // last blended position of each of the warp's 8x4 blocks (the forward
+  // wrote a blend-mask word for every batch up to it) and of the warp
+  int sub_last[PPL];
 #pragma unroll
-  for (int h = 1; h < PPL; h++) lmax = max(lmax, P[h].last);
-  const int warp_last = __reduce_max_sync(0xffffffffu, lmax);
+  for (int h = 0; h < PPL; h++) sub_last[h] = __reduce_max_sync(0xffffffffu, P[h].last);
+  int lmax = sub_last[0];
+#pragma unroll
+  for (int h = 1; h < PPL; h++) lmax = max(lmax, sub_last[h]);
+  const int warp_last = lmax;
   if (warp < NC && lane == 0) s_last[warp] = warp_last;
   pipe_init<MAXK, kStages, NC>(sm);
   int block_last = s_last[0];
@@ -832,7 +839,10 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           const uint32_t rel = first - range.x;   // forward batch rel / 32, bit rel % 32
           const uint32_t *mk = a.blend_mask + (size_t)sub * a.mask_words + (range.x >> 5) + tile + (rel >> 5);
           const uint32_t sh = rel & 31u;
-          const uint32_t w0 = __ldg(mk), w1 = sh ? __ldg(mk + 1) : 0u;
+          // only words of forward batches that hold a position <= the
+          // block's last were written (and can matter)
+          const uint32_t w0 = (int)first <= sub_last[h] ? __ldg(mk) : 0u;
+          const uint32_t w1 = sh && (int)(first + 32u - sh) <= sub_last[h] ? __ldg(mk + 1) : 0u;
           fm[h] = sh ? (w0 >> sh) | (w1 << (32u - sh)) : w0;
         }
       }

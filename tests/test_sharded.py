@@ -154,3 +154,54 @@ def test_sharded_step_gradients_equal_sum_of_view_backwards():
         # float64): the floor of tests/test_gpu_parity.py GRAD_FLOOR
         rel = np.abs(a - b) / np.maximum(den, max(5e-4 * den.max(), 1e-12))
         assert rel.max() < 1e-3, (k, rel.max())
+
+
+@pytest.mark.gpu
+def test_sharded_step_overflow_redo_equals_roomy_run():
+    """rasterizer_view_grad_fn reuses one pair capacity across views without
+    host syncs and redoes the step when a view overflowed it
+    (check_overflow).  A step whose first view sees nothing (capacity sized
+    from it, then forced small) and whose later views overflow must end with
+    the same flat gradients, sigma signal and view counts as a step that had
+    room from the start: the discarded attempt leaves no trace."""
+    import paper_2411_14974_b200 as cs
+    from paper_2411_14974_b200 import rasterizer as rz, synthetic
+    arrays = synthetic.quantize32(synthetic.generate_scene(3000, seed=4))
+    st = cs.SceneTensors.from_arrays(arrays, "cuda")
+    tgt = cs.SceneTensors.from_arrays(synthetic.quantize32(synthetic.perturb(arrays, seed=6)), "cuda")
+    W, H = 160, 120
+    R, t = synthetic.look_at((0.0, 1.4, -4.0), target=(0.0, 1.4, -8.0))     # facing away: nothing visible
+    away = cs.Camera(fx=100.0, fy=100.0, cx=W / 2, cy=H / 2, width=W, height=H, R=R, t=t)
+    cams = [away] + synthetic.ring_cameras(3, W, H)
+    views = [(c, cs.render(tgt, c).image) for c in cams]
+    views = [(c, torch.tensor(im, dtype=torch.float32, device="cuda")) for c, im in views]
+    mode, settings = cs.ScalingMode.DEPTH, cs.RenderSettings()
+
+    def run(tight: bool):
+        params = {k: getattr(st, k).clone() for k in sharded.PARAM_ORDER}
+        scene = cs.SceneTensors(**{k: params[k] for k in ("points", "raw_delta", "raw_sigma", "raw_opacity",
+                                                          "raw_mask", "sh")}, background=st.background)
+        r = rz.Rasterizer("cuda")
+        if tight:
+            r._cap_hint[(scene.n, W, H)] = 1024          # the first (empty) view keeps the capacity tiny
+        fn = sharded.rasterizer_view_grad_fn(scene, mode, settings, rasterizer=r)
+        step = sharded.ViewShardedStep(params, sharded.StepConfig(), fn)
+        calls = {"n": 0}
+        inner = fn.check_overflow
+
+        def counting():
+            ovf = inner()
+            calls["n"] += int(ovf)
+            return ovf
+        fn.check_overflow = counting
+        step.step(views)
+        return {k: v.clone() for k, v in step.flat.views.items()}, calls["n"]
+
+    tight, redos = run(True)
+    roomy, redos0 = run(False)
+    assert redos >= 1 and redos0 == 0, (redos, redos0)
+    torch.testing.assert_close(tight["sigma_views"], roomy["sigma_views"], rtol=0, atol=0)
+    for k in list(sharded.PARAM_ORDER) + ["sigma_signal"]:
+        a, b = tight[k].cpu().numpy().ravel(), roomy[k].cpu().numpy().ravel()
+        scale = max(float(np.abs(b).max()), 1e-30)
+        assert float(np.abs(a - b).max()) <= 1e-5 * scale, k     # float atomics: summation order only
