@@ -20,13 +20,14 @@ fr = r.forward(st, cam, cs.ScalingMode.DEPTH, cs.RenderSettings())
 d = torch.randn(h, w, 3, device="cuda") * 1e-3
 grads = rz.zero_grads(st)
 L = _lib.load()
-buf = (ctypes.c_ulonglong * 8)()
+buf = (ctypes.c_ulonglong * 12)()
 L.cs_debug_wait_stats(buf, 1)
 r.launch_forward(fr, 2, 2)
 r.launch_backward(fr, d, grads, 0, 0)
 L.cs_debug_wait_stats(buf, 0)
 v = list(buf)
 print(f"forward : consumers wait on full {100 * v[1] / max(v[0], 1):.1f}% of their cycles; "
-      f"producer waits on empty {100 * v[3] / max(v[2], 1):.1f}% of its cycles")
+      f"producer waits on empty {100 * v[3] / max(v[2], 1):.1f}% of its cycles; "
+      f"first-batch waits {100 * v[8] / max(v[0], 1):.1f}%")
 print(f"backward: consumers wait on full {100 * v[5] / max(v[4], 1):.1f}% of their cycles; "
       f"producer waits on empty {100 * v[7] / max(v[6], 1):.1f}% of its cycles")
