@@ -67,7 +67,6 @@ struct BlendArgs {
   // skips the others
   uint32_t *blend_mask;
   uint32_t mask_words;
-  uint32_t *tile_counter;   // persistent forward: tiles handed out so far beyond gridDim.x
   // decision record (forward, REC instantiation only): pixel p's blended
   // pair indices, in blend order, at rec_pos[rec_off[p] ...]
   const int64_t *rec_off;
@@ -227,9 +226,7 @@ constexpr int kStageCands = 32;
 #ifndef CS_PROD_SLEEP_NS
 #define CS_PROD_SLEEP_NS 512
 #endif
-#ifndef CS_FWD_PROD_SLEEP_NS
-#define CS_FWD_PROD_SLEEP_NS 128
-#endif
+
 
 template <int MAXK, int kStages>
 struct PipeSmem {
@@ -242,12 +239,6 @@ struct PipeSmem {
   uint64_t empty[kStages];
   int ndone;
   int stop;
-  // persistent forward: what each stage holds -- the block's tile sequence
-  // number (-1: end of stream), tile id, first pair index, candidate count,
-  // batch index within the tile; and the number of (consumer warp, tile)
-  // completions so far
-  int mseq[kStages], mtile[kStages], mfirst[kStages], mcount[kStages], mbatch[kStages];
-  int done_count;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -468,7 +459,6 @@ __device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages> &sm) {
     }
     sm.ndone = 0;
     sm.stop = 0;
-    sm.done_count = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -667,269 +657,6 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
       a.pixel_clamp[p] = (uint8_t)((v0 >= 0.f && v0 <= 1.f) | ((v1 >= 0.f && v1 <= 1.f) << 1) |
                                    ((v2 >= 0.f && v2 <= 1.f) << 2));
     }
-  }
-  if (STATS) {
-    block_add_u64(a.stats + S_FWD_EVALS, n_eval);
-    block_add_u64(a.stats + S_FWD_LINES, n_lines);
-    block_add_u64(a.stats + S_FWD_BLENDS, n_blend);
-    block_add_u64(a.stats + S_FWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent forward blend: gridDim.x blocks (one wave: SMs x resident
-// blocks) each take tiles u = blockIdx.x, blockIdx.x + G, ... of the
-// heaviest-first tile order.  The producer streams the batches of tile after
-// tile through the same ring -- a stage carries its tile in mseq/mtile and
-// the consumers switch tiles when the stream does -- so a block's next tile
-// starts while its consumers finish the current one instead of every block
-// paying the latency of its first batch (12% of the consumers' cycles with
-// one block per tile, tools/wait_stats.py).  The producer loads the next
-// tile's range and first candidate ids during the current tile and prefetches
-// their records into L2.  It abandons a tile once every consumer warp is done
-// with it (done_count); a final stage with mseq = -1 ends the stream.
-template <int MAXK, int kStages, int NC>
-__device__ __forceinline__ void fwd_produce_persistent(PipeSmem<MAXK, kStages> &sm, const BlendArgs &a, int tiles,
-                                                       bool cull) {
-  constexpr int RG = Rec<MAXK>::kGlobal;
-  const int lane = threadIdx.x & 31;
-  // tiles are handed out dynamically (heaviest first): the first gridDim.x by
-  // block index, then one per atomicAdd on the workspace's tile counter
-  auto next_u = [&]() {
-    int v = 0;
-    if (lane == 0) v = (int)gridDim.x + (int)atomicAdd(a.tile_counter, 1u);
-    return __shfl_sync(0xffffffffu, v, 0);
-  };
-  auto tile_of = [&](int u) { return u < tiles ? (a.tile_order ? (int)__ldg(a.tile_order + u) : u) : -1; };
-  auto wait_stage = [&](int g) {   // batch g - kStages released by every consumer
-    if (g < kStages) return;
-    const int s = g % kStages;
-    const uint32_t par = ((g - kStages) / kStages) & 1;
-    if (CS_FWD_PROD_SLEEP_NS > 0) mbar_wait_backoff(&sm.empty[s], par, CS_FWD_PROD_SLEEP_NS);
-    else mbar_wait(&sm.empty[s], par);
-    flush_visible(sm, s, a.visible);
-  };
-  int g = 0;
-  int u = blockIdx.x;
-  int tile = tile_of(u);
-  uint2 range = tile >= 0 ? __ldg(a.ranges + tile) : make_uint2(0u, 0u);
-  uint32_t next_id = (tile >= 0 && range.x + lane < range.y) ? __ldg(a.pair_ids + range.x + lane) : 0u;
-  for (int i = 0; tile >= 0; i++) {
-    const int nb = max(1, (int)((range.y - range.x + kStageCands - 1) / kStageCands));
-    const TileLines tl{(double)((tile % a.tiles_x) * kTile + kRebase), (double)((tile / a.tiles_x) * kTile + kRebase),
-                       a.cutoff};
-    // the next tile, one dependent step per issued batch (their latencies
-    // overlap with this tile's streaming): its queue position, its id, its
-    // range, its first candidate ids (+ an L2 prefetch of their records)
-    int un = 0, ntile = -1, step = 0;
-    uint2 nrange = make_uint2(0u, 0u);
-    uint32_t nids = 0u;
-    auto look_ahead = [&]() {
-      if (step == 0) un = next_u();
-      else if (step == 1) ntile = tile_of(un);
-      else if (step == 2) { if (ntile >= 0) nrange = __ldg(a.ranges + ntile); }
-      else if (step == 3) { if (ntile >= 0) nids = nrange.x + lane < nrange.y ? __ldg(a.pair_ids + nrange.x + lane) : 0u; }
-      else if (step == 4 && ntile >= 0 && nrange.x + lane < nrange.y) {
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.records + (size_t)nids * RG) : "memory");
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.lines + (size_t)nids * Rec<MAXK>::kLines64) : "memory");
-      }
-      step++;
-    };
-    for (int b = 0; b < nb; b++) {
-      if (b > 0 && *reinterpret_cast<volatile int *>(&sm.done_count) >= NC * (i + 1)) break;   // all done with it
-      const int s = g % kStages;
-      wait_stage(g);
-      const uint32_t first = range.x + (uint32_t)b * kStageCands;
-      const uint32_t count = range.y > first ? min((uint32_t)kStageCands, range.y - first) : 0u;
-      const uint32_t id = next_id;
-      if (b + 1 < nb) next_id = first + kStageCands + lane < range.y ? __ldg(a.pair_ids + first + kStageCands + lane) : 0u;
-      if (lane == 0) {
-        sm.mseq[s] = i; sm.mtile[s] = tile; sm.mfirst[s] = (int)first; sm.mcount[s] = (int)count; sm.mbatch[s] = b;
-      }
-      if (lane < (int)count) sm.id[s][lane] = id;
-      {
-        constexpr int CPR = R_HEADER / 4, RPR = 32 / CPR;
-        const int r_in = lane / CPR, c = lane % CPR;
-        for (int r0 = 0; r0 < (int)count; r0 += RPR) {
-          const int r = r0 + r_in;
-          const uint32_t rid = __shfl_sync(0xffffffffu, id, min(r, 31));
-          if (r < (int)count) {
-            const float4 *src = reinterpret_cast<const float4 *>(a.records + (size_t)rid * RG) + c;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sm.rec[s][r][c])), "l"(src)
-                         : "memory");
-          }
-        }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
-      }
-      uint32_t bm = 0xffu;
-      if (lane < (int)count)
-        bm = stage_lines<MAXK>(a.records + (size_t)id * RG, a.lines + (size_t)id * Rec<MAXK>::kLines64,
-                               sm.rec[s][lane], TileLines{tl.tx, tl.ty, cull ? tl.cutoff : 0.f});
-      sm.bmask[s][lane] = (uint8_t)bm;
-      mbar_arrive(&sm.full[s]);   // release: this lane's shared stores
-      g++;
-      look_ahead();
-    }
-    while (step < 4) look_ahead();
-    u = un;
-    tile = ntile;
-    range = nrange;
-    next_id = nids;
-  }
-  // end of the stream: a stage with mseq = -1 (the consumers do not release it)
-  {
-    const int s = g % kStages;
-    wait_stage(g);
-    if (lane == 0) sm.mseq[s] = -1;
-    __syncwarp();
-    mbar_arrive(&sm.full[s]);   // all 32 lanes, twice: the barrier counts 64
-    mbar_arrive(&sm.full[s]);
-    g++;
-  }
-  // drain the batches before it
-  for (int y = max(0, g - 1 - kStages + 1); y < g - 1; y++) {
-    mbar_wait(&sm.empty[y % kStages], (y / kStages) & 1);
-    flush_visible(sm, y % kStages, a.visible);
-  }
-}
-
-template <int MAXK, bool STATS, bool REC = false>
-__global__ void __launch_bounds__(pipe_threads<8>(), CS_FWD_MINB) forward_persistent_kernel(BlendArgs a) {
-  constexpr int kStages = CS_FWD_STAGES;
-  constexpr int NC = 8;
-  extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
-  PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
-  const int tiles = a.tiles_x * ((a.height + kTile - 1) / kTile);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pipe_init<MAXK, kStages, NC>(sm);
-  unsigned n_eval = 0, n_lines = 0, n_blend = 0, n_warp_evals = 0;
-  if (warp == NC) {
-#ifndef CS_NO_BLOCK_CULL
-    const bool cull = !STATS && a.cutoff > 0.f;   // (a counting run evaluates every candidate)
-#else
-    const bool cull = false;
-#endif
-    fwd_produce_persistent<MAXK, kStages, NC>(sm, a, tiles, cull);
-  } else {
-    int lx, ly;
-    tile_pixel(threadIdx.x, lx, ly);
-    const float qx = (float)(lx - kRebase) + 0.5f, qy = (float)(ly - kRebase) + 0.5f;   // relative to T
-    const bool use_floor = a.floor > 0.f;
-    int cur = -1, tile = 0, px = 0, py = 0, rx0 = 0, ry0 = 0;
-    bool inside = false, warp_done = true, finalized = true;
-    int32_t *rec_dst = nullptr;
-    FwdPixel P;
-    auto finalize = [&]() {
-      n_blend += (unsigned)P.nblend;
-      if (inside) {
-        const size_t p = (size_t)py * a.width + px;
-        const float v0 = fmaf(P.T, a.bg[0], P.C0), v1 = fmaf(P.T, a.bg[1], P.C1), v2 = fmaf(P.T, a.bg[2], P.C2);
-        a.image[3 * p] = fminf(fmaxf(v0, 0.f), 1.f);
-        a.image[3 * p + 1] = fminf(fmaxf(v1, 0.f), 1.f);
-        a.image[3 * p + 2] = fminf(fmaxf(v2, 0.f), 1.f);
-        a.final_T[p] = P.T;
-        a.pixel_T[p] = P.T;
-        a.weight_sum[p] = P.W;
-        a.count[p] = P.nblend;
-        if (a.depth) a.depth[p] = P.D;
-        a.pixel_last[p] = P.last;
-        a.pixel_clamp[p] = (uint8_t)((v0 >= 0.f && v0 <= 1.f) | ((v1 >= 0.f && v1 <= 1.f) << 1) |
-                                     ((v2 >= 0.f && v2 <= 1.f) << 2));
-      }
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();   // this warp's visibility bits before the count the producer reads
-        atomicAdd(&sm.done_count, 1);
-      }
-      finalized = true;
-      warp_done = true;
-    };
-    for (int g = 0;; g++) {
-      const int s = g % kStages;
-      {
-        WS_T0(tw);
-        mbar_wait(&sm.full[s], (g / kStages) & 1);
-        if (lane == 0) WS_ADD(1, tw);
-      }
-      const int seq = *reinterpret_cast<volatile int *>(&sm.mseq[s]);
-      if (seq < 0) break;   // end of the stream (not released)
-      if (seq != cur) {     // the stream moved on to the next tile
-        if (!finalized) finalize();
-        cur = seq;
-        tile = *reinterpret_cast<volatile int *>(&sm.mtile[s]);
-        const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-        px = tx * kTile + lx;
-        py = ty * kTile + ly;
-        rx0 = tx * kTile + ((warp & 1) << 3);
-        ry0 = ty * kTile + ((warp >> 1) << 2);
-        inside = px < a.width && py < a.height;
-        if (REC && inside) rec_dst = a.rec_pos + a.rec_off[(size_t)py * a.width + px];
-        P.T = 1.f; P.C0 = P.C1 = P.C2 = P.W = P.D = 0.f;
-        P.last = -1; P.nblend = 0;
-        P.done = !inside;
-        finalized = false;
-        warp_done = __all_sync(0xffffffffu, P.done);
-        if (warp_done) finalize();
-      }
-      if (!warp_done) {
-        const uint32_t first = (uint32_t)*reinterpret_cast<volatile int *>(&sm.mfirst[s]);
-        const int count = *reinterpret_cast<volatile int *>(&sm.mcount[s]);
-        const int bidx = *reinterpret_cast<volatile int *>(&sm.mbatch[s]);
-        const uint32_t alive = __ballot_sync(0xffffffffu, !P.done);
-#ifndef CS_NO_BLOCK_CULL
-        const bool may = STATS || !(a.cutoff > 0.f) || ((sm.bmask[s][lane] >> warp) & 1u);
-#else
-        const bool may = true;
-#endif
-        const uint32_t pm = lane < count && may ? block_mask(rec_bbox(sm.rec[s][lane]), rx0, ry0) & alive : 0u;
-        uint32_t m = __ballot_sync(0xffffffffu, pm != 0u);
-        uint32_t vis = 0;
-        bool now_done = false;
-        while (m) {
-          const int j = __ffs(m) - 1;
-          m &= m - 1;
-          const float4 *rec = sm.rec[s][j];
-          bool blended = false;
-          const uint32_t pj = __shfl_sync(0xffffffffu, pm, j);
-          const bool act = !P.done && ((pj >> lane) & 1u);
-          if (!__any_sync(0xffffffffu, act)) continue;   // its pixels died earlier in this stage
-          if (STATS) n_warp_evals++;
-          if (act) {
-            if (STATS) n_eval++;
-            const int pos = (int)first + j;
-            if (MAXK == 8) {
-              const int nl = __float_as_int(rec[2].z);   // warp-uniform line count (an if chain: a switch became a jump table)
-              if (nl == 5) blended = fwd_candidate<5, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
-              else if (nl == 6) blended = fwd_candidate<6, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
-              else if (nl == 4) blended = fwd_candidate<4, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
-              else blended = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
-            } else {
-              blended = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, use_floor, pos, P, n_lines);
-            }
-            if (REC && blended) rec_dst[P.nblend - 1] = pos;
-          }
-          if (__any_sync(0xffffffffu, blended)) {
-            vis |= 1u << j;
-            if (__all_sync(0xffffffffu, P.done)) {
-              now_done = true;
-              break;
-            }
-          }
-        }
-        if (lane == 0) {
-          if (vis) atomicOr(&sm.vis[s], vis);
-          // word (range.x / 32 + tile + batch) of this block's mask: unique
-          // per (tile, batch), written for every batch the warp processed
-          // (an empty tile's single batch has count 0 and range (0, 0): no word)
-          const uint32_t rx = first - (uint32_t)bidx * kStageCands;
-          if (count > 0) a.blend_mask[(size_t)warp * a.mask_words + (rx >> 5) + tile + bidx] = vis;
-        }
-        if (now_done) finalize();
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[s]);
-    }
-    if (!finalized) finalize();
   }
   if (STATS) {
     block_add_u64(a.stats + S_FWD_EVALS, n_eval);
@@ -1257,7 +984,6 @@ static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const c
   a.d_image = nullptr;
   a.rec_off = nullptr;
   a.rec_pos = nullptr;
-  a.tile_counter = reinterpret_cast<uint32_t *>(ws + L.counters) + C_TILE_NEXT;
   return a;
 }
 
@@ -1276,29 +1002,6 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
   a.visible = f.visible;
   if (f.visible && p.n > 0) cudaMemsetAsync(f.visible, 0, (size_t)p.n, s);
   const int tiles = L.tiles_x * L.tiles_y;
-#ifdef CS_FWD_PERSIST
-  // persistent: one wave of blocks looping over the tiles (measured slower:
-  // 0.387 vs 0.363 ms at 1M @1080p)
-  cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t), s);
-  auto launch = [&](auto k, size_t smem) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pipe_threads<8>(), smem);
-    const int grid = std::max(1, std::min(tiles, sms * std::max(per_sm, 1)));
-    k<<<grid, pipe_threads<8>(), smem, s>>>(a);
-  };
-  if (L.max_k == 8) {
-    launch(rec ? forward_persistent_kernel<8, false, true> : stats ? forward_persistent_kernel<8, true>
-                                                                   : forward_persistent_kernel<8, false>,
-           sizeof(PipeSmem<8, CS_FWD_STAGES>));
-  } else {
-    launch(rec ? forward_persistent_kernel<16, false, true> : stats ? forward_persistent_kernel<16, true>
-                                                                    : forward_persistent_kernel<16, false>,
-           sizeof(PipeSmem<16, CS_FWD_STAGES>));
-  }
-#else
   if (L.max_k == 8) {
     auto k = rec ? forward_kernel<8, false, true> : stats ? forward_kernel<8, true> : forward_kernel<8, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
@@ -1308,7 +1011,6 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_FWD_STAGES>));
     k<<<tiles * (8 / CS_FWD_NC), pipe_threads<CS_FWD_NC>(), sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
   }
-#endif
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }
 

@@ -73,7 +73,7 @@ typedef float AccT;
 // depth-sort keys.
 enum Counter {
   C_NVISIBLE = 0, C_NPAIRS = 1, C_OVERFLOW = 2, C_NSORT = 3, C_CHUNK0 = 4, C_STATS = 16, C_KMINC = 32, C_KMAX = 34,
-  C_NONFINITE = 36, C_TILE_NEXT = 37, C_COUNT = 40
+  C_NONFINITE = 36, C_COUNT = 40
 };
 // uint64 work statistics at word C_STATS (roofline accounting, read by the benchmark)
 enum Stat {
