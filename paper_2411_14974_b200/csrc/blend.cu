@@ -683,8 +683,11 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
 }
 
 // Per-pixel backward state (backward.py:133-205).
+// GS = g . S, the upstream gradient dotted with the colour composited
+// behind (backward.py:163-205 keeps S per channel; only g . S enters
+// d alpha, and g is constant per pixel): one running scalar instead of three.
 struct BwdPixel {
-  float T, g0, g1, g2, S0, S1, S2;
+  float T, g0, g1, g2, GS;
   int last;
 };
 
@@ -718,7 +721,8 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
   v[A_DC] += P.g0 * w;
   v[A_DC + 1] += P.g1 * w;
   v[A_DC + 2] += P.g2 * w;
-  float dA = P.g0 * (Tp * c0 - P.S0 * rom) + P.g1 * (Tp * c1 - P.S1 * rom) + P.g2 * (Tp * c2 - P.S2 * rom);
+  const float gc = fmaf(P.g0, c0, fmaf(P.g1, c1, P.g2 * c2));   // g . c
+  float dA = fmaf(Tp, gc, -P.GS * rom);                            // g . (T_prev c - S / (1 - alpha))
   if (!(e.alpha_raw < (float)kAlphaMaxD)) dA = 0.f;
   v[A_DOEFF] += dA * e.I;
   const float dI = dA * o;
@@ -739,9 +743,7 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
     }
   }
   v[A_DDEL] += dphi * wz * inv_dls;               // dphi * sum_l w_l L_l
-  P.S0 = fmaf(w, c0, P.S0);
-  P.S1 = fmaf(w, c1, P.S1);
-  P.S2 = fmaf(w, c2, P.S2);
+  P.GS = fmaf(w, gc, P.GS);
   P.T = Tp;
   return true;
 }
@@ -788,7 +790,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
     const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3) + 4 * h;
     qx[h] = (float)(px - tx * kTile - kRebase) + 0.5f;   // relative to the tile's re-basing point
     qy[h] = (float)(py - ty * kTile - kRebase) + 0.5f;
-    P[h].T = 1.f; P[h].g0 = P[h].g1 = P[h].g2 = P[h].S0 = P[h].S1 = P[h].S2 = 0.f;
+    P[h].T = 1.f; P[h].g0 = P[h].g1 = P[h].g2 = P[h].GS = 0.f;
     P[h].last = -1;
     if (warp < NC && px < a.width && py < a.height) {
       const size_t p = (size_t)py * a.width + px;
@@ -798,9 +800,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
       P[h].g0 = (cm & 1) ? a.d_image[3 * p] : 0.f;
       P[h].g1 = (cm & 2) ? a.d_image[3 * p + 1] : 0.f;
       P[h].g2 = (cm & 4) ? a.d_image[3 * p + 2] : 0.f;
-      P[h].S0 = P[h].T * a.bg[0];
-      P[h].S1 = P[h].T * a.bg[1];
-      P[h].S2 = P[h].T * a.bg[2];
+      P[h].GS = P[h].T * fmaf(P[h].g0, a.bg[0], fmaf(P[h].g1, a.bg[1], P[h].g2 * a.bg[2]));   // S = T_final bg
     }
   }
   // last blended position of each of the warp's 8x4 blocks (the forward
