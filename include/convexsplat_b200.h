@@ -269,6 +269,17 @@ CS_API int cs_backward_ex(const cs_camera *cam, const cs_settings *set, const cs
                           const float *d_image, const cs_grads *grads, const cs_view_signal *signal,
                           uint32_t flags, int32_t first_stage, int32_t last_stage, void *stream);
 
+/* The chain stage (stage 1) of cs_backward_ex over the convexes
+ * [first, last) only: the gradient rows of a convex range are final as soon
+ * as its launch completes, so a view-sharded step can all-reduce them
+ * (bucketed by convex range) while the chain of the next range runs
+ * (SURVEY 8(e)).  Needs stage 0 of the same backward first; flags:
+ * CS_GRADS_OVERWRITE only. */
+CS_API int cs_backward_chain_range(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                                   void *workspace, size_t workspace_bytes, int64_t pair_capacity,
+                                   const cs_grads *grads, const cs_view_signal *signal, uint32_t flags,
+                                   int64_t first, int64_t last, void *stream);
+
 /* Scratch bytes cs_image_loss needs for an H x W image. Host-only. */
 CS_API int cs_image_loss_workspace(int32_t height, int32_t width, size_t *bytes);
 

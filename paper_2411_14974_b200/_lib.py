@@ -15,7 +15,7 @@ EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forwa
            "cs_forward_stages", "cs_forward_ex", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
            "cs_backward_signal", "cs_backward_ex", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step",
            "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags", "cs_density_scatter",
-           "cs_read_status", "cs_forward_record", "cs_prepare_view_export")
+           "cs_read_status", "cs_forward_record", "cs_prepare_view_export", "cs_backward_chain_range")
 ABI_VERSION = 7
 ERR_WORKSPACE = 3     # CS_ERR_WORKSPACE
 ERR_NONFINITE = 4     # CS_ERR_NONFINITE
@@ -124,6 +124,10 @@ def load(path: str = None):
     L.cs_read_counters.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), _vp]
     L.cs_read_status.argtypes = [_vp, _vp]
     L.cs_forward_record.argtypes = L.cs_forward.argtypes[:-1] + [_vp, _vp, _vp]
+    L.cs_backward_chain_range.argtypes = [ctypes.POINTER(CsCamera), ctypes.POINTER(CsSettings),
+                                          ctypes.POINTER(CsParams), _vp, ctypes.c_size_t, ctypes.c_int64,
+                                          ctypes.POINTER(CsGrads), ctypes.POINTER(CsViewSignal), ctypes.c_uint32,
+                                          ctypes.c_int64, ctypes.c_int64, _vp]
     L.cs_prepare_view_export.argtypes = [ctypes.POINTER(CsCamera), ctypes.POINTER(CsSettings),
                                          ctypes.POINTER(CsParams), _vp, ctypes.c_size_t, ctypes.c_int64,
                                          ctypes.POINTER(CsViewExport), _vp]
@@ -149,7 +153,8 @@ def load(path: str = None):
                "cs_read_counters", "cs_graham_scan_batch", "cs_backward_signal", "cs_backward_ex",
                "cs_image_loss_workspace",
                "cs_image_loss", "cs_adam_step", "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags",
-               "cs_density_scatter", "cs_read_status", "cs_forward_record", "cs_prepare_view_export"):
+               "cs_density_scatter", "cs_read_status", "cs_forward_record", "cs_prepare_view_export",
+               "cs_backward_chain_range"):
         getattr(L, fn).restype = ctypes.c_int
     if L.cs_abi_version() != ABI_VERSION:
         raise CsError(f"ABI mismatch: library {L.cs_abi_version()} != {ABI_VERSION}")

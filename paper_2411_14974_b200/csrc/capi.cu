@@ -188,6 +188,24 @@ static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_
   return CS_OK;
 }
 
+int cs_backward_chain_range(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                            size_t workspace_bytes, int64_t pair_capacity, const cs_grads *grads,
+                            const cs_view_signal *signal, uint32_t flags, int64_t first, int64_t last, void *stream) {
+  if (!params || !grads || !workspace) return CS_ERR_ARG;
+  if (flags & ~(uint32_t)CS_GRADS_OVERWRITE) return CS_ERR_ARG;
+  if (signal && (!signal->sigma_signal || !signal->sigma_views || !signal->visible)) return CS_ERR_ARG;
+  if (first < 0 || last < first || last > params->n) return CS_ERR_ARG;
+  cs_layout L;
+  int rc = cs_workspace_layout(cam, set, params->n, params->k, pair_capacity, &L);
+  if (rc) return rc;
+  if (workspace_bytes < L.total_bytes) return CS_ERR_WORKSPACE;
+  if (params->n > 0 && (!grads->d_points || !grads->d_raw_delta || !grads->d_raw_sigma || !grads->d_raw_opacity ||
+                        !grads->d_raw_mask || !grads->d_sh))
+    return CS_ERR_ARG;
+  return cs::launch_chain(*cam, *set, *params, L, static_cast<char *>(workspace), *grads, signal,
+                          (flags & CS_GRADS_OVERWRITE) != 0, reinterpret_cast<cudaStream_t>(stream), first, last);
+}
+
 int cs_backward_stages(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
                        size_t workspace_bytes, int64_t pair_capacity, const float *d_image, const cs_grads *grads,
                        int32_t first_stage, int32_t last_stage, void *stream) {

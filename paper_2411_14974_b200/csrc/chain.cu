@@ -37,6 +37,7 @@ struct ChainArgs {
   cs_grads g;
   cs_view_signal sig;   // sigma_signal == nullptr: no densification signal
   uint32_t *nonfinite;  // workspace counter C_NONFINITE: set when a gradient row is not finite
+  int64_t first;        // convexes [first, n) (a range: cs_backward_chain_range)
 };
 
 #ifdef CS_CHAIN_F64   // float64 geometry arrays: half the threads keep the static shared memory under 48 KB
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
   __shared__ G s_x[MAXK][kChainThreads], s_y[MAXK][kChainThreads];
   __shared__ G s_dx[MAXK][kChainThreads], s_dy[MAXK][kChainThreads];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int64_t i = (int64_t)blockIdx.x * kChainThreads + t;
+  const int64_t i = a.first + (int64_t)blockIdx.x * kChainThreads + t;
   constexpr int RF = Rec<MAXK>::kGlobal;
   constexpr int AF = Acc<MAXK>::kFloats;
   constexpr int kShRow = kShCoeffs * 3;
@@ -391,11 +392,14 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
 
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                  const cs_layout &L, char *ws, const cs_grads &g, const cs_view_signal *sig, bool overwrite,
-                 cudaStream_t s) {
-  if (p.n == 0) return CS_OK;
+                 cudaStream_t s, int64_t first, int64_t last) {
+  if (last < 0 || last > p.n) last = p.n;
+  if (first < 0) first = 0;
+  if (last <= first) return CS_OK;
   ChainArgs a;
   a.cam = cam;
-  a.n = p.n;
+  a.n = last;
+  a.first = first;
   a.k = p.k;
   a.sh_degree = set.sh_degree;
   a.mode = set.scaling_mode;
@@ -414,11 +418,11 @@ int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &
   a.sig = sig ? *sig : cs_view_signal{nullptr, nullptr, nullptr};
   a.nonfinite = reinterpret_cast<uint32_t *>(ws + L.counters) + C_NONFINITE;
   if (L.max_k == 8) {
-    if (overwrite) chain_kernel<8, true><<<(int)((p.n + chain_threads<8>() - 1) / chain_threads<8>()), chain_threads<8>(), 0, s>>>(a);
-    else chain_kernel<8, false><<<(int)((p.n + chain_threads<8>() - 1) / chain_threads<8>()), chain_threads<8>(), 0, s>>>(a);
+    if (overwrite) chain_kernel<8, true><<<(int)((last - first + chain_threads<8>() - 1) / chain_threads<8>()), chain_threads<8>(), 0, s>>>(a);
+    else chain_kernel<8, false><<<(int)((last - first + chain_threads<8>() - 1) / chain_threads<8>()), chain_threads<8>(), 0, s>>>(a);
   } else {
-    if (overwrite) chain_kernel<16, true><<<(int)((p.n + chain_threads<16>() - 1) / chain_threads<16>()), chain_threads<16>(), 0, s>>>(a);
-    else chain_kernel<16, false><<<(int)((p.n + chain_threads<16>() - 1) / chain_threads<16>()), chain_threads<16>(), 0, s>>>(a);
+    if (overwrite) chain_kernel<16, true><<<(int)((last - first + chain_threads<16>() - 1) / chain_threads<16>()), chain_threads<16>(), 0, s>>>(a);
+    else chain_kernel<16, false><<<(int)((last - first + chain_threads<16>() - 1) / chain_threads<16>()), chain_threads<16>(), 0, s>>>(a);
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }

@@ -267,7 +267,7 @@ int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs
                           const cs_layout &L, char *ws, const float *d_image, bool stats, cudaStream_t s);
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                  const cs_layout &L, char *ws, const cs_grads &g, const cs_view_signal *sig, bool overwrite,
-                 cudaStream_t s);
+                 cudaStream_t s, int64_t first = 0, int64_t last = -1);
 int launch_image_loss(int H, int W, const float *img, const float *tgt, const float *raw_mask, int64_t n,
                       double lam, double beta, float *d_image, float *d_raw_mask, double *stats, void *ws,
                       cudaStream_t s);

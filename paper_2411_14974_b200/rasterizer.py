@@ -226,6 +226,23 @@ class Rasterizer:
                                               (_lib.WORK_COUNTERS if work_counters else 0), first_stage, last_stage,
                                               stream), "cs_backward_ex")
 
+    def launch_chain_range(self, fr: Frame, grads: dict, first: int, last: int, signal=None):
+        """Stage 1 (the per-convex chain) of a backward whose stage 0 ran,
+        over convexes [first, last) only, accumulating (+=) into ``grads``
+        (cs_backward_chain_range): the bucketed all-reduce of the
+        view-sharded step starts on a range as soon as its chain is done."""
+        g = _lib.CsGrads(grads["points"].data_ptr(), grads["raw_delta"].data_ptr(), grads["raw_sigma"].data_ptr(),
+                         grads["raw_opacity"].data_ptr(), grads["raw_mask"].data_ptr(), grads["sh"].data_ptr())
+        ws = fr.workspace
+        sig = None
+        if signal is not None:
+            sig = _lib.CsViewSignal(signal[0].data_ptr(), signal[1].data_ptr(), signal[2].data_ptr())
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(_lib.load().cs_backward_chain_range(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
+                                                       ctypes.byref(fr.params_c), ws.ptr, ws.nbytes, fr.capacity,
+                                                       ctypes.byref(g), ctypes.byref(sig) if sig is not None else None,
+                                                       0, int(first), int(last), stream), "cs_backward_chain_range")
+
     @staticmethod
     def read_stats(fr: Frame) -> dict:
         """Work counters of the last forward/backward on this workspace (syncs);

@@ -174,7 +174,7 @@ class ViewShardedStep:
     """
 
     def __init__(self, params: dict, config: StepConfig = StepConfig(), view_grad_fn: Callable = None,
-                 group=None):
+                 group=None, buckets: int = 4):
         self.params = params
         self.config = config
         self.group = group
@@ -191,6 +191,11 @@ class ViewShardedStep:
             self.adam = Adam(params)
         self.view_grad_fn = view_grad_fn
         self.iteration = 0
+        # bucketed all-reduce: the rank's last view runs its
+        # chain per convex range and each range's rows are all-reduced
+        # (async) while the next range's chain runs; `buckets` ranges
+        self.buckets = max(1, int(buckets))
+        self._pending = []
 
     def lrs(self, iteration: int) -> dict:
         c = self.config
@@ -209,8 +214,14 @@ class ViewShardedStep:
         own = getattr(self.view_grad_fn, "handles_signal", False)
         sigma_prev = None if own else torch.empty_like(grads["raw_sigma"])
         losses = []
-        for view in shard_views(batch, self.rank, self.world):
-            if own:
+        self._pending = []
+        mine = shard_views(batch, self.rank, self.world)
+        bucketed = self.world > 1 and getattr(self.view_grad_fn, "supports_buckets", False)
+        for vi, view in enumerate(mine):
+            if own and bucketed and vi == len(mine) - 1:
+                loss = self.view_grad_fn(view, grads, signal, ranges=self.bucket_ranges(),
+                                         on_range=self._reduce_range)
+            elif own:
                 loss = self.view_grad_fn(view, grads, signal)
             else:
                 sigma_prev.copy_(grads["raw_sigma"])
@@ -223,17 +234,41 @@ class ViewShardedStep:
         total = torch.stack(losses).sum() if losses else torch.zeros((), device=self.flat.buffer.device)
         return {"local_views": len(losses), "local_loss_sum": total}
 
+    def bucket_ranges(self) -> list:
+        n = self.flat.views["raw_delta"].shape[0]
+        step = -(-n // self.buckets) if n else 1
+        return [(i, min(i + step, n)) for i in range(0, n, step)]
+
+    def _reduce_range(self, first: int, last: int):
+        """All-reduce (async, SUM) of the rows [first, last) of every flat
+        tensor: issued on NCCL's stream after the chain of that range, so it
+        overlaps the chain of the next range."""
+        for k in self.flat.views:
+            self._pending.append(dist.all_reduce(self.flat.views[k][first:last], op=dist.ReduceOp.SUM,
+                                                 group=self.group, async_op=True))
+
     def reduce(self, batch_size: int):
-        """The single collective: sum of everyone's gradients (the 1/B of the
-        batch mean is applied inside the optimiser step)."""
-        if self.world > 1:
+        """The collective: sum of everyone's gradients (the 1/B of the batch
+        mean is applied inside the optimiser step) -- the bucketed
+        all-reduces issued during the last view, or one all-reduce of the
+        whole flat buffer."""
+        if self.world <= 1:
+            return
+        if self._pending:
+            for w in self._pending:
+                w.wait()
+            self._pending = []
+        else:
             dist.all_reduce(self.flat.buffer, op=dist.ReduceOp.SUM, group=self.group)
 
     def step(self, batch: list) -> dict:
         self.iteration += 1
         info = self.accumulate(batch)
         check = getattr(self.view_grad_fn, "check_overflow", None)
-        while check is not None and check():   # a view overflowed its pair capacity: redo with more room
+        while check is not None and check(self.group if self.world > 1 else None):
+            # a view of some rank overflowed its pair capacity: every rank redoes the step with more room
+            for w in self._pending:
+                w.wait()
             info = self.accumulate(batch)
         diverged = getattr(self.view_grad_fn, "diverged", None)
         if diverged is not None and diverged():   # trainer.py:172-173 (read with the overflow check)
@@ -290,7 +325,7 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
     # device maxima over the step's views: (pairs, overflow, non-finite)
     state = {"cap": None, "max": torch.zeros(3, dtype=torch.int32, device=scene.device), "bad": False}
 
-    def fn(view, grads: dict, signal: dict):
+    def fn(view, grads: dict, signal: dict, ranges=None, on_range=None):
         cam, target = view
         if state["cap"] is None:      # first view ever: size the capacity with a checked forward
             fr = r.forward(scene, cam, mode, settings, workspace=ws)
@@ -300,16 +335,26 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
         torch.maximum(state["max"][0:2], ws.counters()[1:3], out=state["max"][0:2])   # (pairs, overflow)
         loss = cuda_image_loss(fr.image, target, scene.raw_mask, config.lambda_dssim, config.beta_mask,
                                d_raw_mask=grads["raw_mask"], workspace=lw)
-        r.launch_backward(fr, loss["d_image"], grads,
-                          signal=(signal["sigma_signal"], signal["sigma_views"], fr.visible))
+        sig = (signal["sigma_signal"], signal["sigma_views"], fr.visible)
+        if ranges is None:
+            r.launch_backward(fr, loss["d_image"], grads, signal=sig)
+        else:   # the chain per convex range, each range handed on as soon as it is final
+            r.launch_backward(fr, loss["d_image"], grads, 0, 0)
+            for first, last in ranges:
+                r.launch_chain_range(fr, grads, first, last, signal=sig)
+                on_range(first, last)
         # non-finite loss (trainer.py:172) or gradient row (the chain's C_NONFINITE flag)
         bad = (~torch.isfinite(loss["total"])).to(torch.int32).reshape(1)
         torch.maximum(state["max"][2:3], torch.maximum(bad, ws.counters()[36:37]), out=state["max"][2:3])
         return loss["total"]
 
-    def check_overflow() -> bool:
+    def check_overflow(group=None) -> bool:
         """One host read per step: True (and a larger capacity) if any view
-        overflowed its pair capacity since the last check."""
+        overflowed its pair capacity since the last check -- on any rank of
+        ``group`` (the maxima are all-reduced first), so that every rank
+        redoes the step together."""
+        if group is not None or (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+            dist.all_reduce(state["max"], op=dist.ReduceOp.MAX, group=group)
         pairs, ovf, bad = (int(v) for v in state["max"].cpu())
         state["max"].zero_()
         state["bad"] = bool(bad) and not ovf
@@ -321,6 +366,7 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
         return False
 
     fn.handles_signal = True
+    fn.supports_buckets = True
     fn.check_overflow = check_overflow
     fn.diverged = lambda: state["bad"]
     return fn

@@ -205,3 +205,65 @@ def test_sharded_step_overflow_redo_equals_roomy_run():
         a, b = tight[k].cpu().numpy().ravel(), roomy[k].cpu().numpy().ravel()
         scale = max(float(np.abs(b).max()), 1e-30)
         assert float(np.abs(a - b).max()) <= 1e-5 * scale, k     # float atomics: summation order only
+
+
+def _mock_signal_fn(params, bucket_log=None):
+    """A per-view function with the GPU function's interface (accumulates its
+    own sigma signal; with ``ranges`` it hands every convex range on as soon
+    as the range's rows are final, as the chain-per-range backward does)."""
+    def fn(view, grads, signal, ranges=None, on_range=None):
+        v = float(view)
+        for name, g in grads.items():
+            g.add_(torch.sin(params[name] * (1.0 + 0.1 * v) + v))
+        n = params["points"].shape[0]
+        vis = ((torch.arange(n) % (int(view) + 2)) != 0).to(grads["raw_sigma"].dtype)
+        signal["sigma_signal"].add_(torch.cos(params["raw_sigma"] + v).abs() * vis)
+        signal["sigma_views"].add_(vis)
+        if ranges is not None:
+            for first, last in ranges:
+                if bucket_log is not None:
+                    bucket_log.append((first, last))
+                on_range(first, last)
+        return torch.tensor(v)
+    fn.handles_signal = True
+    fn.supports_buckets = True
+    return fn
+
+
+def _bucket_worker(rank, world, port, out_path, buckets):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        params = _params()
+        log = []
+        step = sharded.ViewShardedStep(params, sharded.StepConfig(total_iterations=100),
+                                       _mock_signal_fn(params, log), buckets=buckets)
+        for _ in range(3):
+            step.step(list(range(7)))
+        torch.save({"params": params, "sigma": step.sigma_sum.clone(), "log": log}, f"{out_path}.{rank}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bucketed_all_reduce_equals_one_all_reduce():
+    """the rank's last view hands its convex ranges to async
+    all-reduces as their rows become final (overlapping the chain of the
+    next range); the step ends bit-identical to one all-reduce of the whole
+    buffer and to a single process."""
+    results = {}
+    for buckets in (1, 3):
+        with tempfile.TemporaryDirectory() as tmp:
+            out = os.path.join(tmp, "res")
+            mp.spawn(_bucket_worker, args=(2, _free_port(), out, buckets), nprocs=2, join=True)
+            results[buckets] = [torch.load(f"{out}.{r}") for r in range(2)]
+    single = _params()
+    step = sharded.ViewShardedStep(single, sharded.StepConfig(total_iterations=100), _mock_signal_fn(single))
+    for _ in range(3):
+        step.step(list(range(7)))
+    r1, r3 = results[1], results[3]
+    assert len(r3[0]["log"]) == 3 * 3 and r1[0]["log"] == [(0, 37)] * 3     # 3 ranges per step, 3 steps
+    for name in single:
+        torch.testing.assert_close(r3[0]["params"][name], r3[1]["params"][name], rtol=0, atol=0)
+        torch.testing.assert_close(r3[0]["params"][name], r1[0]["params"][name], rtol=0, atol=0)
+        torch.testing.assert_close(r3[0]["params"][name], single[name], rtol=1e-10, atol=1e-12)
+    torch.testing.assert_close(r3[0]["sigma"], step.sigma_sum, rtol=1e-10, atol=1e-12)
