@@ -189,8 +189,8 @@ def test_sharded_step_overflow_redo_equals_roomy_run():
         calls = {"n": 0}
         inner = fn.check_overflow
 
-        def counting():
-            ovf = inner()
+        def counting(group=None):
+            ovf = inner(group)
             calls["n"] += int(ovf)
             return ovf
         fn.check_overflow = counting
