@@ -49,5 +49,6 @@ for rep in sys.argv[1:]:
             except ValueError:
                 pass
     tot = sum(s for s, _ in stalls) or 1.0
-    print("   top stall samples:", ", ".join(f"{k.split('stalled_')[1].split('.')[0]} {100 * s / tot:.0f}%"
+    if stalls:
+        print("   top stall samples:", ", ".join(f"{k.split('stalled_')[1].split('.')[0]} {100 * s / tot:.0f}%"
                                               for s, k in sorted(stalls, reverse=True)[:8]))
