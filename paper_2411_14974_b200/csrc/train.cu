@@ -232,7 +232,9 @@ __global__ void __launch_bounds__(kLossThreads) mask_term_kernel(const float *ra
   for (int64_t i = (int64_t)blockIdx.x * kLossThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kLossThreads) {
     const float m = 1.f / (1.f + __expf(-raw_mask[i]));
     s += m;
-    if (d_raw_mask) d_raw_mask[i] += beta * m * (1.f - m) / (float)n;
+    // a reduction, not a read-modify-write: the chain stages of other views
+    // (other streams) accumulate into the same gradient row concurrently
+    if (d_raw_mask) atomicAdd(d_raw_mask + i, beta * m * (1.f - m) / (float)n);
   }
   atomic_add_block_sum(stats + 2, s);
 }

@@ -216,6 +216,9 @@ class ViewShardedStep:
         losses = []
         self._pending = []
         mine = shard_views(batch, self.rank, self.world)
+        begin = getattr(self.view_grad_fn, "begin", None)
+        if begin is not None:
+            begin()
         bucketed = self.world > 1 and getattr(self.view_grad_fn, "supports_buckets", False)
         for vi, view in enumerate(mine):
             if own and bucketed and vi == len(mine) - 1:
@@ -230,7 +233,11 @@ class ViewShardedStep:
                 vis = visible.to(self.flat.buffer.dtype)
                 signal["sigma_signal"].add_((grads["raw_sigma"] - sigma_prev).abs_() * vis)
                 signal["sigma_views"].add_(vis)
-            losses.append(loss.detach().reshape(()).to(self.flat.buffer.dtype))
+            losses.append(loss.detach().reshape(()))
+        end = getattr(self.view_grad_fn, "end", None)
+        if end is not None:
+            end()
+        losses = [x.to(self.flat.buffer.dtype) for x in losses]
         total = torch.stack(losses).sum() if losses else torch.zeros((), device=self.flat.buffer.device)
         return {"local_views": len(losses), "local_loss_sum": total}
 
@@ -304,35 +311,65 @@ class ViewShardedStep:
         return new
 
 
-def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConfig(), rasterizer=None):
+def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConfig(), rasterizer=None,
+                            lanes: int = 2):
     """Default per-view function on the GPU: sm_100a render, fused CUDA loss
     (cs_image_loss; adds the mask-loss gradient, trainer.py:176), backward
     through the C ABI accumulating into the flat buffers together with the
     view's sigma signal (cs_backward_signal).  Returns the view's loss as a
     device scalar.
 
-    No host synchronisation per view: one workspace is reused by every view
-    (stream order serialises them) and the forwards run with the cached pair
+    Views alternate between ``lanes`` CUDA streams, each with its own
+    workspaces: the views of a step are independent until their gradients
+    are summed (the backward's accumulation is by atomic reductions), so
+    view v+1's forward overlaps view v's backward and the kernels' tails --
+    every stage is latency-bound below full occupancy.  ViewShardedStep
+    brackets a step's views with ``begin()`` / ``end()`` (fork from and join
+    into the caller's stream).
+
+    No host synchronisation per view: the forwards run with the cached pair
     capacity; each view's pair count and overflow flag are folded into a
-    device maximum that ``check_overflow`` reads once per step -- if any view
-    overflowed, the step is redone with a larger capacity (ViewShardedStep)."""
+    per-lane device maximum that ``check_overflow`` reads once per step -- if
+    any view overflowed, the step is redone with a larger capacity."""
     from .rasterizer import Workspace, default_rasterizer
     from .train_ops import LossWorkspace, image_loss as cuda_image_loss
 
     r = rasterizer or default_rasterizer(scene.device)
-    lw = LossWorkspace()
-    ws = Workspace(scene.device)
-    # device maxima over the step's views: (pairs, overflow, non-finite)
-    state = {"cap": None, "max": torch.zeros(3, dtype=torch.int32, device=scene.device), "bad": False}
+    dev = scene.device
+    n_lanes = max(1, int(lanes))
+    lane_state = [{"stream": torch.cuda.Stream(dev) if n_lanes > 1 else None, "ws": Workspace(dev),
+                   "lw": LossWorkspace(),
+                   # device maxima over the lane's views: (pairs, overflow, non-finite)
+                   "max": torch.zeros(3, dtype=torch.int32, device=dev)} for _ in range(n_lanes)]
+    state = {"cap": None, "bad": False, "next": 0, "forked": False}
 
-    def fn(view, grads: dict, signal: dict, ranges=None, on_range=None):
+    def begin():
+        """Fork: every lane stream waits for the caller's stream (the zeroed
+        flat buffer, the current parameters)."""
+        state["next"] = 0
+        if n_lanes > 1:
+            ev = torch.cuda.current_stream(dev).record_event()
+            for ln in lane_state:
+                ln["stream"].wait_event(ev)
+            state["forked"] = True
+
+    def end():
+        """Join: the caller's stream waits for every lane."""
+        if n_lanes > 1 and state["forked"]:
+            cur = torch.cuda.current_stream(dev)
+            for ln in lane_state:
+                cur.wait_stream(ln["stream"])
+            state["forked"] = False
+
+    def body(ln, view, grads, signal, ranges, on_range):
         cam, target = view
+        ws, lw = ln["ws"], ln["lw"]
         if state["cap"] is None:      # first view ever: size the capacity with a checked forward
             fr = r.forward(scene, cam, mode, settings, workspace=ws)
             state["cap"] = fr.capacity
         else:
             fr = r.forward(scene, cam, mode, settings, workspace=ws, capacity=state["cap"], check=False)
-        torch.maximum(state["max"][0:2], ws.counters()[1:3], out=state["max"][0:2])   # (pairs, overflow)
+        torch.maximum(ln["max"][0:2], ws.counters()[1:3], out=ln["max"][0:2])   # (pairs, overflow)
         loss = cuda_image_loss(fr.image, target, scene.raw_mask, config.lambda_dssim, config.beta_mask,
                                d_raw_mask=grads["raw_mask"], workspace=lw)
         sig = (signal["sigma_signal"], signal["sigma_views"], fr.visible)
@@ -345,18 +382,39 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
                 on_range(first, last)
         # non-finite loss (trainer.py:172) or gradient row (the chain's C_NONFINITE flag)
         bad = (~torch.isfinite(loss["total"])).to(torch.int32).reshape(1)
-        torch.maximum(state["max"][2:3], torch.maximum(bad, ws.counters()[36:37]), out=state["max"][2:3])
+        torch.maximum(ln["max"][2:3], torch.maximum(bad, ws.counters()[36:37]), out=ln["max"][2:3])
         return loss["total"]
+
+    def fn(view, grads: dict, signal: dict, ranges=None, on_range=None):
+        k = state["next"]
+        state["next"] = k + 1
+        ln = lane_state[k % n_lanes]
+        if ln["stream"] is None or not state["forked"]:
+            return body(ln, view, grads, signal, ranges, on_range)
+        if ranges is not None:
+            # the bucketed all-reduce reads rows the other lanes also add to:
+            # this (last) view's lane first waits for them
+            for other in lane_state:
+                if other is not ln:
+                    ln["stream"].wait_stream(other["stream"])
+        with torch.cuda.stream(ln["stream"]):
+            out = body(ln, view, grads, signal, ranges, on_range)
+        out.record_stream(torch.cuda.current_stream(dev))
+        return out
 
     def check_overflow(group=None) -> bool:
         """One host read per step: True (and a larger capacity) if any view
         overflowed its pair capacity since the last check -- on any rank of
         ``group`` (the maxima are all-reduced first), so that every rank
         redoes the step together."""
+        mx = lane_state[0]["max"]
+        for ln in lane_state[1:]:
+            torch.maximum(mx, ln["max"], out=mx)
         if group is not None or (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
-            dist.all_reduce(state["max"], op=dist.ReduceOp.MAX, group=group)
-        pairs, ovf, bad = (int(v) for v in state["max"].cpu())
-        state["max"].zero_()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+        pairs, ovf, bad = (int(v) for v in mx.cpu())
+        for ln in lane_state:
+            ln["max"].zero_()
         state["bad"] = bool(bad) and not ovf
         if ovf:
             state["cap"] = int(pairs * 1.25) + 1024
@@ -367,6 +425,7 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
 
     fn.handles_signal = True
     fn.supports_buckets = True
+    fn.begin, fn.end = begin, end
     fn.check_overflow = check_overflow
     fn.diverged = lambda: state["bad"]
     return fn
