@@ -312,7 +312,7 @@ class ViewShardedStep:
 
 
 def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConfig(), rasterizer=None,
-                            lanes: int = 2):
+                            lanes: int = 4):
     """Default per-view function on the GPU: sm_100a render, fused CUDA loss
     (cs_image_loss; adds the mask-loss gradient, trainer.py:176), backward
     through the C ABI accumulating into the flat buffers together with the
