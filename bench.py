@@ -407,8 +407,8 @@ def config2_block(args, dev, cpu: bool) -> dict:
            "gt_convexes": gt.n, "convexes": scene.n,
            "gpu": {"train_steps_per_s": 1000.0 / ms, "ms_per_step": ms, "views_per_s": nv * 1000.0 / ms,
                    "mean_view_loss_first_last": [losses[0], losses[-1]], "steps": args.chair_steps,
-                   "step": "per view: forward, fused L1+D-SSIM+mask loss, backward (accumulate); then one fused "
-                           "Adam update"}}
+                   "step": "per view: forward, fused L1+D-SSIM+mask loss, backward (accumulate); views alternate "
+                           "between 4 CUDA-stream lanes; then one fused Adam update"}}
     if cpu:
         import oracle
         threads = host_cores()
@@ -481,6 +481,7 @@ def train_step_bench(args, st, arrays, dev, world, rank):
             "views_per_s": args.train_views * 1000.0 / ms, "batch_views": args.train_views,
             "view_size": [args.train_width, args.train_height], "convexes": st.n, "ranks": world,
             "views_per_rank": len(mine), "steps": args.train_steps, "scaling": "strong (fixed batch of views)",
+            "lanes": "views alternate between 4 CUDA-stream lanes (own workspaces) on each rank",
             "collective": "one all_reduce(SUM) of %d float32 per step" % step.flat.buffer.numel(),
             "rank0_loss_sum_first_last": [losses[0], losses[-1]]}
 
