@@ -472,7 +472,7 @@ __device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages> &sm) {
 
 // Per-pixel forward state (rasterize.py:178-204).
 struct FwdPixel {
-  float T, C0, C1, C2, W, D;
+  float T, C0, C1, C2, D;
   int last, nblend;
   bool done;
 };
@@ -495,7 +495,6 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float dqx, floa
   P.C0 = fmaf(w, h1.x, P.C0);
   P.C1 = fmaf(w, h1.y, P.C1);
   P.C2 = fmaf(w, h1.z, P.C2);
-  P.W += w;
   P.D = fmaf(w, h1.w, P.D);
   P.T *= fmaxf(fmaf(h0.w, e.J, h2.x), 1e-6f);   // 1 - alpha = (1-o) + o (1-I)
   P.nblend++;
@@ -571,7 +570,7 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
     int32_t *rec_dst = nullptr;
     if (REC && inside) rec_dst = a.rec_pos + a.rec_off[(size_t)py * a.width + px];
     FwdPixel P;
-    P.T = 1.f; P.C0 = P.C1 = P.C2 = P.W = P.D = 0.f;
+    P.T = 1.f; P.C0 = P.C1 = P.C2 = P.D = 0.f;
     P.last = -1; P.nblend = 0;
     P.done = !inside;
     bool warp_done = __all_sync(0xffffffffu, P.done);
@@ -678,7 +677,9 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
       a.image[3 * p + 2] = fminf(fmaxf(v2, 0.f), 1.f);
       a.final_T[p] = P.T;
       a.pixel_T[p] = P.T;
-      a.weight_sum[p] = P.W;
+      // blend_weight_sum = sum T_prev alpha telescopes to 1 - T (rasterize.py:198-200;
+      // the compositing identity of test_rasterize.py:108-116): no running sum
+      a.weight_sum[p] = 1.f - P.T;
       a.count[p] = P.nblend;
       if (a.depth) a.depth[p] = P.D;
       a.pixel_last[p] = P.last;
