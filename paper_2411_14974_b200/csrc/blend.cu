@@ -470,11 +470,14 @@ __device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages> &sm) {
   __syncthreads();
 }
 
-// Per-pixel forward state (rasterize.py:178-204).
+#define P_T_LT(t, thr) ((t) < (thr))
+// Per-pixel forward state (rasterize.py:178-204).  A pixel is done when
+// T < thr: thr = the transmittance floor (or 0 without one), and pixels
+// outside the image start at T = -1 -- no separate flag.
 struct FwdPixel {
   float T, C0, C1, C2, D;
   int last, nblend;
-  bool done;
+  __device__ __forceinline__ bool done(float thr) const { return P_T_LT(T, thr); }
 };
 
 // One candidate at one pixel: evaluate, and blend iff (T >= floor if floor >
@@ -499,7 +502,6 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float dqx, floa
   P.T *= fmaxf(fmaf(h0.w, e.J, h2.x), 1e-6f);   // 1 - alpha = (1-o) + o (1-I)
   P.nblend++;
   P.last = pos;
-  if (use_floor && P.T < floor_) P.done = true;
   return true;
 }
 
@@ -565,15 +567,16 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
     ly += half * 8;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 2) + half * 8;
-    const bool inside = px < a.width && py < a.height;
+    bool inside = px < a.width && py < a.height;
     const float qx = (float)(lx - kRebase) + 0.5f, qy = (float)(ly - kRebase) + 0.5f;   // relative to T
     int32_t *rec_dst = nullptr;
     if (REC && inside) rec_dst = a.rec_pos + a.rec_off[(size_t)py * a.width + px];
     FwdPixel P;
     P.T = 1.f; P.C0 = P.C1 = P.C2 = P.D = 0.f;
     P.last = -1; P.nblend = 0;
-    P.done = !inside;
-    bool warp_done = __all_sync(0xffffffffu, P.done);
+    if (!inside) P.T = -1.f;
+    const float thr = a.floor > 0.f ? a.floor : 0.f;   // rasterize.py:194: alive while T >= floor
+    bool warp_done = __all_sync(0xffffffffu, P.done(thr));
     // A warp whose pixels all terminated leaves the pipeline for good
     // instead of waiting on every remaining stage: before arriving for
     // batch b it arrive_drops on the phases of batches b .. b + kStages - 1
@@ -609,7 +612,7 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
         const uint32_t first = range.x + (uint32_t)b * kStageCands;
         const int count = (int)min((uint32_t)kStageCands, range.y - first);
         // lane j: pixels of this warp's block inside candidate j's bbox and alive
-        const uint32_t alive = __ballot_sync(0xffffffffu, !P.done);
+        const uint32_t alive = __ballot_sync(0xffffffffu, !P.done(thr));
 #ifndef CS_NO_BLOCK_CULL
         const bool may = STATS || NC != 8 || !(a.cutoff > 0.f) || ((sm.bmask[s][lane] >> warp) & 1u);
 #else
@@ -624,7 +627,7 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
           const float4 *rec = sm.rec[s][j];
           bool blended = false;
           const uint32_t pj = __shfl_sync(0xffffffffu, pm, j);
-          const bool act = !P.done && ((pj >> lane) & 1u);
+          const bool act = !P.done(thr) && ((pj >> lane) & 1u);
           if (!__any_sync(0xffffffffu, act)) continue;   // its pixels died earlier in this stage
           if (STATS) n_warp_evals++;
 #ifdef CS_NO_EVAL
@@ -647,7 +650,7 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
           }
           if (__any_sync(0xffffffffu, blended)) {
             vis |= 1u << j;
-            if (__all_sync(0xffffffffu, P.done)) {
+            if (__all_sync(0xffffffffu, P.done(thr))) {
               warp_done = true;
               break;
             }
@@ -669,6 +672,7 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
     }
     if (lane == 0) WS_ADD(0, tc);
     n_blend = (unsigned)P.nblend;
+    inside = px < a.width && py < a.height;
     if (inside) {
       const size_t p = (size_t)py * a.width + px;
       const float v0 = fmaf(P.T, a.bg[0], P.C0), v1 = fmaf(P.T, a.bg[1], P.C1), v2 = fmaf(P.T, a.bg[2], P.C2);
