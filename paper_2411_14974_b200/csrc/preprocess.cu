@@ -213,6 +213,55 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
 #define GX(i) X[(i) * stride]
 #define GY(i) Y[(i) * stride]
   if (n < 3) return 0;
+  int ref = 0;
+  NL rest;
+#ifndef CS_NO_HULL_FAST
+  bool sorted = false;
+  // Fast sort for n <= 8.  When every pair of the other points has a cross
+  // product around ref (the comparator's own float64 expression) beyond
+  // both the 1e-9 tolerance and its rounding bound (4.5e-16 (|ax by| +
+  // |ay bx|), so its sign is the exact one), the comparator is the strict
+  // total order of the points' angles around ref: there are no duplicates
+  // (a duplicate pair gives 0), the dedupe is the identity, and any sort --
+  // CPython's binarysort included -- yields the one order, each point's
+  // position being the number of points before it.  The C(n-1, 2) products
+  // are independent, where binary insertion is a chain of dependent
+  // comparisons.  Otherwise fall through to the CPython-order sort.
+  if (n <= 8) {
+    for (int j = 1; j < n; j++)
+      if (GY(j) < GY(ref) || (GY(j) == GY(ref) && GX(j) < GX(ref))) ref = j;
+    const double rx = GX(ref), ry = GY(ref);
+    for (int j = 0; j < n; j++)
+      if (j != ref) rest.push(j);
+    const int m = n - 1;
+    uint32_t rank = 0;   // 4-bit position per rest entry
+    bool decisive = true;
+    for (int q = 1; q < m; q++) {
+      const int b = rest.get(q);
+      const double bx = GX(b) - rx, by = GY(b) - ry;
+#pragma unroll
+      for (int p = 0; p < 7; p++)
+        if (p < q) {
+          const int a = rest.get(p);
+          const double ax = GX(a) - rx, ay = GY(a) - ry;
+          const double s = ax * by, t = ay * bx, c = s - t;
+          decisive &= fabs(c) > fmax(kCrossTol, 1e-15 * (fabs(s) + fabs(t)));
+          rank += c > 0.0 ? (1u << (4 * q)) : (1u << (4 * p));   // a before b : b before a
+        }
+    }
+    if (decisive) {
+      NL order;
+      order.n = m;
+      for (int j = 0; j < m; j++) order.set((int)((rank >> (4 * j)) & 15u), rest.get(j));
+      rest = order;
+      sorted = true;
+    } else {
+      rest = NL();
+      ref = 0;
+    }
+  }
+  if (!sorted) {
+#endif
   NL uq;
   for (int i = 0; i < n; i++) {
     const double xi = GX(i), yi = GY(i);
@@ -224,7 +273,7 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
     if (!dup) uq.push(i);
   }
   if (uq.n < 3) return 0;
-  int ref = uq.get(0);
+  ref = uq.get(0);
   for (int j = 1; j < uq.n; j++) {
     const int u = uq.get(j);
     if (GY(u) < GY(ref) || (GY(u) == GY(ref) && GX(u) < GX(ref))) ref = u;
@@ -237,7 +286,6 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
     if (c < -kCrossTol) return false;
     return (ax * ax + ay * ay) < (bx * bx + by * by);
   };
-  NL rest;
   for (int j = 0; j < uq.n; j++)
     if (uq.get(j) != ref) rest.push(uq.get(j));
   const int m = rest.n;
@@ -264,12 +312,16 @@ __device__ int graham_scan_packed(int n, const double *X, const double *Y, int s
       rest.insert(l, pivot);
     }
   }
+#ifndef CS_NO_HULL_FAST
+  }
+#endif
+  const int nrest = rest.n;
   auto cross = [&](int o, int a, int b) -> double {  // projection.py:43-44
     return (GX(a) - GX(o)) * (GY(b) - GY(o)) - (GY(a) - GY(o)) * (GX(b) - GX(o));
   };
   NL st;
   st.push(ref);
-  for (int j = 0; j < m; j++) {
+  for (int j = 0; j < nrest; j++) {
     const int c = rest.get(j);
     while (st.n >= 2 && cross(st.get(st.n - 2), st.get(st.n - 1), c) <= kCrossTol) st.pop();
     st.push(c);
@@ -350,9 +402,20 @@ __device__ __forceinline__ void sh_colour(float x, float y, float z, int deg, co
 // kernel) in check.  Every value is computed by the same expression as in the
 // reference, so the discrete results are unchanged.  The anchor of the
 // anchor-relative line offsets is the integer pixel at hull vertex 0.
+#ifdef CS_PRE_PHASES
+// diagnostics: SM cycles per preprocess phase, summed over threads (tools/pre_phases.py)
+__device__ unsigned long long g_pre_phase[8];
+#define PH(n) do { const long long t_ = clock64(); atomicAdd(&g_pre_phase[n], (unsigned long long)(t_ - ph_t)); ph_t = t_; } while (0)
+#else
+#define PH(n) do {} while (0)
+#endif
+
 template <int MAXK>
 __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, double *X,
                                                double *Y) {
+#ifdef CS_PRE_PHASES
+  long long ph_t = clock64();
+#endif
   const int k = a.k;
   // the scalar parameters are loaded up front (their latency overlaps)
   const float r_mask = __ldg(a.raw_mask + i), r_delta = __ldg(a.raw_delta + i);
@@ -362,6 +425,7 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   // rasterize.py:89 mask gate (model.py:105-107, expit = 1/(1+exp(-x)))
   const double mask = 1.0 / (1.0 + exp(-(double)r_mask));
   if (mask <= kMaskGate) return false;
+  PH(0);
   // projection.py:22-40
   const double *R = a.cam.R;
   double zsum = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
@@ -385,9 +449,11 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
     }
   }
   if (culled) return false;
+  PH(1);
   NibbleListT<typename std::conditional<(MAXK <= 8), uint32_t, uint64_t>::type> hull;
   const int h = graham_scan_packed(k, X, Y, kPreThreads, hull);
   if (h == 0) return false;
+  PH(2);
   // rasterize.py:99-103
   const double depth = zsum / k;
   const double s = depth_scale(a.mode, a.cam.ortho ? 1.0 : depth);
@@ -447,6 +513,7 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
       pny = ny;
     }
   }
+  PH(3);
   // projection.py:170-177
   int x0, x1, y0, y1;
   if (full_frame) {
@@ -485,11 +552,13 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   float dx = 0.f, dy = 0.f, dz = 1.f;
   if (d2 > 0.f) { const float rs = rsqrtf(d2); dx = vx * rs; dy = vy * rs; dz = vz * rs; }
   float col[3];
+  PH(4);
   sh_colour(dx, dy, dz, a.sh_degree, a.sh + i * kShCoeffs * 3, col);
   dst[0] = make_float4((float)axd, (float)ayd, (float)sigma_s, (float)o);
   dst[1] = make_float4(col[0], col[1], col[2], (float)depth);
   dst[2] = make_float4(1.f / (1.f + __expf(ro)), (float)dls, __int_as_float(h), __frcp_rn((float)dls));
   dst[3] = make_float4(__int_as_float(x0), __int_as_float(x1), __int_as_float(y0), __int_as_float(y1));
+  PH(5);
   return true;
 }
 
@@ -681,6 +750,18 @@ __global__ void __launch_bounds__(128) export_view_kernel(ExportArgs a) {
     a.out.color[i * 3 + c] = v > 0.0 ? v : 0.0;
   }
 }
+
+#ifdef CS_PRE_PHASES
+extern "C" CS_API int cs_debug_pre_phases(unsigned long long *host8, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(host8, g_pre_phase, sizeof(unsigned long long) * 8) != cudaSuccess) return 2;
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_pre_phase, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 int launch_export_view(const cs_camera &cam, const cs_settings &set, const cs_params &p, const cs_layout &L,
                        const char *ws, const cs_view_export &out, cudaStream_t s) {
