@@ -378,7 +378,7 @@ __device__ __forceinline__ void sh_colour(float x, float y, float z, int deg, co
 #pragma unroll
   for (int q = 0; q < kShCoeffs * 3 / 4; q++) {  // 4 coefficients of 3 channels = 3 float4
     if (4 * q < 3 * nb) {
-      const float4 v = __ldg(sh4 + q);
+      const float4 v = sh4[q];
       const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int r = 0; r < 4; r++) {
@@ -410,9 +410,14 @@ __device__ unsigned long long g_pre_phase[8];
 #define PH(n) do {} while (0)
 #endif
 
+// What the colour pass (after the block's geometry) needs of a visible convex.
+struct ColourJob {
+  float dx, dy, dz, depth;
+};
+
 template <int MAXK>
 __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, const float *pts_s, double *X,
-                                               double *Y) {
+                                               double *Y, ColourJob &cj, uint64_t &key) {
 #ifdef CS_PRE_PHASES
   long long ph_t = clock64();
 #endif
@@ -540,7 +545,8 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   }
   a.bbox[i] = make_int4(x0, x1, y0, y1);
   a.touched[i] = (uint32_t)(((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1));
-  a.depth_keys[i] = orderable_bits(depth);
+  key = orderable_bits(depth);
+  a.depth_keys[i] = key;
   // rasterize.py:110-114 view direction; harmonics.py:101-109 colour (float32,
   // SH rows read straight from global: 12 x 16-byte loads per thread).  The
   // direction only feeds the continuous colour: centre offset in float64
@@ -551,11 +557,9 @@ __device__ __forceinline__ bool preprocess_one(const PreArgs &a, int64_t i, cons
   const float d2 = vx * vx + vy * vy + vz * vz;
   float dx = 0.f, dy = 0.f, dz = 1.f;
   if (d2 > 0.f) { const float rs = rsqrtf(d2); dx = vx * rs; dy = vy * rs; dz = vz * rs; }
-  float col[3];
+  cj.dx = dx; cj.dy = dy; cj.dz = dz; cj.depth = (float)depth;
   PH(4);
-  sh_colour(dx, dy, dz, a.sh_degree, a.sh + i * kShCoeffs * 3, col);
   dst[0] = make_float4((float)axd, (float)ayd, (float)sigma_s, (float)o);
-  dst[1] = make_float4(col[0], col[1], col[2], (float)depth);
   dst[2] = make_float4(1.f / (1.f + __expf(ro)), (float)dls, __int_as_float(h), __frcp_rn((float)dls));
   dst[3] = make_float4(__int_as_float(x0), __int_as_float(x1), __int_as_float(y0), __int_as_float(y1));
   PH(5);
@@ -595,7 +599,36 @@ __global__ void __launch_bounds__(kPreThreads, CS_PRE_BLOCKS) preprocess_kernel(
   }
   const int64_t i = base + threadIdx.x;
   bool vis = false;
-  if (i < a.n) vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, Xs + threadIdx.x, Ys + threadIdx.x);
+  ColourJob cj;
+  uint64_t key = 0ull;
+  if (i < a.n)
+    vis = preprocess_one<MAXK>(a, i, pts_smem + threadIdx.x * rowf, Xs + threadIdx.x, Ys + threadIdx.x, cj, key);
+  // Colour (harmonics.py:101-109) after the block's geometry: its SH rows
+  // (48 floats per convex, prefetched into L2 at the start) are copied by
+  // one bulk TMA into the smem the geometry no longer needs, so the
+  // per-thread 192-byte rows are not gathered from L2 by 12 strided loads
+  // per thread each waiting on its own round trip.
+  {
+    float *sh_smem = reinterpret_cast<float *>(pre_smem);
+    __syncthreads();   // every thread is done with X, Y and its points
+    if (full) {
+      if (threadIdx.x == 0) {
+        const uint32_t sbytes = kPreThreads * kShCoeffs * 3 * 4;
+        fence_proxy_async_smem();   // the generic reads above precede the async-proxy writes
+        mbar_expect_tx(&bars[0], sbytes);
+        tma_bulk_g2s(sh_smem, a.sh + base * kShCoeffs * 3, sbytes, &bars[0]);
+      }
+      mbar_wait(&bars[0], 1);
+    } else {
+      for (int q = threadIdx.x; q < nblk * kShCoeffs * 3; q += kPreThreads) sh_smem[q] = a.sh[base * kShCoeffs * 3 + q];
+      __syncthreads();
+    }
+    if (vis) {
+      float col[3];
+      sh_colour(cj.dx, cj.dy, cj.dz, a.sh_degree, sh_smem + threadIdx.x * kShCoeffs * 3, col);
+      reinterpret_cast<float4 *>(a.records + i * Rec<MAXK>::kGlobal)[1] = make_float4(col[0], col[1], col[2], cj.depth);
+    }
+  }
   unsigned b = __ballot_sync(0xffffffffu, vis);
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(&a.counters[C_NVISIBLE], (unsigned)__popc(b));
   // range of the visible depth keys (block reduce, one atomic pair per block)
@@ -604,7 +637,7 @@ __global__ void __launch_bounds__(kPreThreads, CS_PRE_BLOCKS) preprocess_kernel(
     if (threadIdx.x == 0) { s_kminc = 0ull; s_kmax = 0ull; }
     __syncthreads();
     unsigned long long kc = 0ull, kx = 0ull;
-    if (vis) { kx = a.depth_keys[i]; kc = ~kx; }
+    if (vis) { kx = key; kc = ~kx; }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       kc = max(kc, (unsigned long long)__shfl_xor_sync(0xffffffffu, kc, o));
@@ -804,7 +837,9 @@ int launch_preprocess(const cs_camera &cam, const cs_settings &set, const cs_par
   a.counters = reinterpret_cast<uint32_t *>(ws + L.counters);
   camera_center(cam, a.cam_center);
   const int blocks = (int)((p.n + kPreThreads - 1) / kPreThreads);
-  const size_t smem = (size_t)kPreThreads * (2 * L.max_k * sizeof(double) + p.k * 3 * sizeof(float));
+  // geometry staging (X, Y, points), later reused for the block's SH rows
+  const size_t smem = (size_t)kPreThreads * std::max(2 * L.max_k * sizeof(double) + p.k * 3 * sizeof(float),
+                                                     (size_t)kShCoeffs * 3 * sizeof(float));
   if (L.max_k == 8) {
     cudaFuncSetAttribute(preprocess_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     preprocess_kernel<8><<<blocks, kPreThreads, smem, s>>>(a);
