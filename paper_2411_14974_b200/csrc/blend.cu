@@ -492,6 +492,7 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float dqx, floa
   float z[LineSet<NL, MAXK>::kN];
   const Eval e = eval_field<NL, MAXK>(L, h0.z, h0.w, dqx, dqy, z);
   if (STATS) n_lines += L.nl;
+#ifdef CS_FWD_BRANCHY
   if (!(e.alpha >= cutoff)) return false;
   const float4 h1 = rec[1];
   const float w = P.T * e.alpha;
@@ -503,6 +504,21 @@ __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float dqx, floa
   P.nblend++;
   P.last = pos;
   return true;
+#else
+  // predicated (no divergent branch): a rejected candidate adds w = 0 and
+  // multiplies T by 1, which leaves the state bit-identical
+  const bool ok = e.alpha >= cutoff;
+  const float4 h1 = rec[1];
+  const float w = ok ? P.T * e.alpha : 0.f;
+  P.C0 = fmaf(w, h1.x, P.C0);
+  P.C1 = fmaf(w, h1.y, P.C1);
+  P.C2 = fmaf(w, h1.z, P.C2);
+  P.D = fmaf(w, h1.w, P.D);
+  P.T *= ok ? fmaxf(fmaf(h0.w, e.J, h2.x), 1e-6f) : 1.f;   // 1 - alpha = (1-o) + o (1-I)
+  P.nblend += ok ? 1 : 0;
+  P.last = ok ? pos : P.last;
+  return ok;
+#endif
 }
 
 // Forward blend (rasterize.py:178-209), one 16x16 tile per block.  REC:
@@ -817,12 +833,12 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
   const uint2 range = a.ranges[tile];
   const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + (warp >> 1) * 4 * PPL;
   BwdPixel P[PPL];
-  float qx[PPL], qy[PPL];
+  // pixel h of the lane, relative to the tile's re-basing point: (qx, qy0 + 4 h)
+  const float qx = (float)(rx0 + (lane & 7) - tx * kTile - kRebase) + 0.5f;
+  const float qy0 = (float)(ry0 + (lane >> 3) - ty * kTile - kRebase) + 0.5f;
 #pragma unroll
   for (int h = 0; h < PPL; h++) {
     const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3) + 4 * h;
-    qx[h] = (float)(px - tx * kTile - kRebase) + 0.5f;   // relative to the tile's re-basing point
-    qy[h] = (float)(py - ty * kTile - kRebase) + 0.5f;
     P[h].T = 1.f; P[h].g0 = P[h].g1 = P[h].g2 = P[h].GS = 0.f;
     P[h].last = -1;
     if (warp < NC && px < a.width && py < a.height) {
@@ -924,7 +940,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           bool contrib = false;
 #define CS_BWD2_PX(NLV, H)                                                                       \
   if (H < PPL && act[H % PPL]) {                                                                   \
-    const bool c_ = bwd_candidate<NLV, MAXK, STATS>(rec, qx[H % PPL], qy[H % PPL], a.cutoff, P[H % PPL], v, n_lines); \
+    const bool c_ = bwd_candidate<NLV, MAXK, STATS>(rec, qx, qy0 + (float)(4 * (H % PPL)), a.cutoff, P[H % PPL], v, n_lines); \
     contrib |= c_;                                                                                 \
     if (STATS) n_bblend += (unsigned)c_;                                                           \
   }
