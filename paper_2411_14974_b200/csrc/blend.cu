@@ -1,7 +1,8 @@
 // K3 forward blend and K4a backward blend over 16x16 tiles.
 //
-// Forward (rasterize.py:178-209, field.py:51-72, rasterize.py:147-153): one
-// thread per pixel, candidates staged in shared memory in batches; per
+// Forward (rasterize.py:178-209, field.py:51-72, rasterize.py:147-153): two
+// pixels per thread (forward2_kernel; forward_kernel, one pixel per thread,
+// with -DCS_FWD_PPL1), candidates staged in shared memory in batches; per
 // candidate whose bbox holds the pixel:
 //   z_j = delta_s L_j, phi = LSE(z), I = sigmoid(-sigma_s phi),
 //   alpha = min(o I, ALPHA_MAX); blend iff (T >= floor if floor > 0) and
@@ -715,6 +716,301 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
   }
 }
 
+// ---------------------------------------------------------------------------
+// Forward blend, two pixels per lane (8x8 pixels per warp, 4 consumer warps
+// per 16x16 tile).  Per candidate the warp-level work -- the loop step, the
+// record address, the line-count dispatch, the line loads and the votes --
+// is shared by two pixels (rows r and r + 4 of the lane's column), and the
+// two evaluations are independent chains the scheduler interleaves.  Every
+// pixel sees the same candidates in the same order with the same arithmetic
+// as in forward_kernel, so the outputs are bit-identical; the blend masks are
+// still per 8x4 block (a warp writes the words of its two blocks).
+// ---------------------------------------------------------------------------
+
+// 2^z summed over the lines at (dx, dy): eval_field's expression and order.
+template <int NL, int MAXK>
+__device__ __forceinline__ float line_sum(const LineSet<NL, MAXK> &L, float dx, float dy) {
+  constexpr int N = LineSet<NL, MAXK>::kN;
+  float ex[N];
+#pragma unroll
+  for (int l = 0; l < N; l++)
+    ex[l] = L.has(l) ? ex2(fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]))) : 0.f;
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int l = 0; l + w < N; l += 2 * w) ex[l] += ex[l + w];
+  return ex[0];
+}
+__device__ __forceinline__ bool lse_in_range(float s) { return s >= 0x1p-100f && s <= 0x1p100f; }
+// eval_field's max-shifted log-sum-exp (a sum outside [2^-100, 2^100]; rare):
+// the lines are re-read from the stage
+template <int NL, int MAXK>
+__device__ __noinline__ float lse_shifted(const float4 *rec, float dx, float dy) {
+  constexpr int N = LineSet<NL, MAXK>::kN;
+  LineSet<NL, MAXK> L;
+  L.load(rec, __float_as_int(rec[2].z));
+  float z[N];
+  float m = -INFINITY;
+#pragma unroll
+  for (int l = 0; l < N; l++)
+    if (L.has(l)) {
+      z[l] = fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]));
+      m = fmaxf(m, z[l]);
+    }
+  float s2 = 0.f;
+#pragma unroll
+  for (int l = 0; l < N; l++)
+    if (L.has(l)) s2 += ex2(z[l] - m);
+  return m + lg2(s2);
+}
+__device__ __forceinline__ Eval eval_finish(float phi2, float sig, float o) {
+  Eval e;
+  const float u = ex2(sig * phi2);
+  e.I = rcp(1.f + u);
+  e.J = u > 1.f ? 1.f - e.I : u * e.I;
+  e.alpha_raw = o * e.I;
+  e.alpha = fminf(e.alpha_raw, (float)kAlphaMaxD);
+  e.phi2 = phi2;
+  return e;
+}
+// the predicated blend update of fwd_candidate
+__device__ __forceinline__ void blend_update(FwdPixel &P, const Eval &e, bool ok, float4 h0, float4 h1, float4 h2,
+                                             int pos) {
+  const float w = ok ? P.T * e.alpha : 0.f;
+  P.C0 = fmaf(w, h1.x, P.C0);
+  P.C1 = fmaf(w, h1.y, P.C1);
+  P.C2 = fmaf(w, h1.z, P.C2);
+  P.D = fmaf(w, h1.w, P.D);
+  P.T *= ok ? fmaxf(fmaf(h0.w, e.J, h2.x), 1e-6f) : 1.f;
+  P.nblend += ok ? 1 : 0;
+  P.last = ok ? pos : P.last;
+}
+// One candidate at both pixels of the lane (act0 / act1: which of them to blend).
+template <int NL, int MAXK, bool STATS>
+__device__ __forceinline__ void fwd_pair(const float4 *rec, float qx, float qy0, bool act0, bool act1, float cutoff,
+                                         int pos, FwdPixel &P0, FwdPixel &P1, unsigned &n_lines, bool &bl0, bool &bl1) {
+  const float4 h0 = rec[0], h2 = rec[2];
+  float s0, s1;
+  {
+    LineSet<NL, MAXK> L;
+    L.load(rec, __float_as_int(h2.z));
+    s0 = line_sum(L, qx, qy0);
+    s1 = line_sum(L, qx, qy0 + 4.f);
+    if (STATS) n_lines += (unsigned)L.nl * ((act0 ? 1u : 0u) + (act1 ? 1u : 0u));
+  }
+  float phi0 = lg2(s0), phi1 = lg2(s1);
+  if (!(lse_in_range(s0) && lse_in_range(s1))) {
+    if (!lse_in_range(s0)) phi0 = lse_shifted<NL, MAXK>(rec, qx, qy0);
+    if (!lse_in_range(s1)) phi1 = lse_shifted<NL, MAXK>(rec, qx, qy0 + 4.f);
+  }
+  const Eval e0 = eval_finish(phi0, h0.z, h0.w), e1 = eval_finish(phi1, h0.z, h0.w);
+  const float4 h1 = rec[1];
+  bl0 = act0 && e0.alpha >= cutoff;
+  bl1 = act1 && e1.alpha >= cutoff;
+  blend_update(P0, e0, bl0, h0, h1, h2, pos);
+  blend_update(P1, e1, bl1, h0, h1, h2, pos);
+}
+
+#ifndef CS_FWD2_MINB
+#define CS_FWD2_MINB 5
+#endif
+template <int MAXK, bool STATS, bool REC = false>
+__global__ void __launch_bounds__(pipe_threads<4>(), CS_FWD2_MINB) forward2_kernel(BlendArgs a) {
+  constexpr int kStages = CS_FWD_STAGES;
+  constexpr int NC = 4;
+  extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
+  PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
+  const int unit = (int)blockIdx.x;
+  const int tile = a.tile_order ? (int)a.tile_order[unit] : unit;
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint2 range = a.ranges[tile];
+  const int nbatch = (int)((range.y - range.x + kStageCands - 1) / kStageCands);
+  pipe_init<MAXK, kStages, NC>(sm);
+  unsigned n_eval = 0, n_lines = 0, n_blend = 0, n_warp_evals = 0;
+  if (warp == NC) {
+#ifndef CS_NO_BLOCK_CULL
+    const bool cull = !STATS && a.cutoff > 0.f;
+#else
+    const bool cull = false;
+#endif
+    const TileLines tl{(double)(tx * kTile + kRebase), (double)(ty * kTile + kRebase), a.cutoff};
+    const int total = (int)gridDim.x;
+    int f_tile = -1;
+    uint2 f_range = make_uint2(0u, 0u);
+    uint32_t f_id = 0u;
+    auto look_ahead = [&](int step) {   // as in forward_kernel
+      const int fu = unit + a.ahead;
+      if (a.ahead <= 0 || fu >= total) return;
+      const int lane = threadIdx.x & 31;
+      if (step == 0) f_tile = a.tile_order ? (int)__ldg(a.tile_order + fu) : fu;
+      else if (step == 1) f_range = __ldg(a.ranges + f_tile);
+      else if (step == 2) f_id = f_range.x + lane < f_range.y ? __ldg(a.pair_ids + f_range.x + lane) : 0xffffffffu;
+      else if (step == 3 && f_id != 0xffffffffu) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.records + (size_t)f_id * Rec<MAXK>::kGlobal) : "memory");
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.lines + (size_t)f_id * Rec<MAXK>::kLines64) : "memory");
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.lines + (size_t)f_id * Rec<MAXK>::kLines64 + 16) : "memory");
+      }
+    };
+    pipe_produce<MAXK, kStages, NC>(sm, a.records, a.lines, a.pair_ids, nbatch,
+                       [&](int b, uint32_t &first, uint32_t &count) {
+                         first = range.x + (uint32_t)b * kStageCands;
+                         count = min((uint32_t)kStageCands, range.y - first);
+                       }, true, a.visible, tl, cull, look_ahead);
+  } else {
+    // warp: columns (warp & 1) * 8 + 0..7, rows (warp >> 1) * 8 + 0..7; lane:
+    // column lane & 7, rows lane >> 3 and (lane >> 3) + 4 (pixel h = 0, 1,
+    // in the 8x4 blocks q0 and q1 = q0 + 2)
+    const int lx = ((warp & 1) << 3) | (lane & 7), ly0 = ((warp >> 1) << 3) | (lane >> 3);
+    const int px = tx * kTile + lx, py0 = ty * kTile + ly0;
+    const int rx0 = tx * kTile + ((warp & 1) << 3), ry0 = ty * kTile + ((warp >> 1) << 3);
+    const int q0 = (warp & 1) | ((warp >> 1) << 2);
+    const float qx = (float)(lx - kRebase) + 0.5f, qy0 = (float)(ly0 - kRebase) + 0.5f;
+    FwdPixel P0, P1;
+    P0.T = P1.T = 1.f;
+    P0.C0 = P0.C1 = P0.C2 = P0.D = 0.f;
+    P1.C0 = P1.C1 = P1.C2 = P1.D = 0.f;
+    P0.last = P1.last = -1;
+    P0.nblend = P1.nblend = 0;
+    const bool in0 = px < a.width && py0 < a.height, in1 = px < a.width && py0 + 4 < a.height;
+    if (!in0) P0.T = -1.f;
+    if (!in1) P1.T = -1.f;
+    int32_t *rec0 = nullptr, *rec1 = nullptr;
+    if (REC && in0) rec0 = a.rec_pos + a.rec_off[(size_t)py0 * a.width + px];
+    if (REC && in1) rec1 = a.rec_pos + a.rec_off[(size_t)(py0 + 4) * a.width + px];
+    const float thr = a.floor > 0.f ? a.floor : 0.f;   // rasterize.py:194: alive while T >= floor
+    bool warp_done = __all_sync(0xffffffffu, P0.done(thr) && P1.done(thr));
+    auto leave = [&](int b) {   // as in forward_kernel
+      if (lane == 0) {
+        __threadfence_block();
+        atomicAdd(&sm.ndone, 1);
+#pragma unroll 1
+        for (int i = 0; i < kStages; i++) {
+          const int x = b + i;
+          if (i > 0 && x >= kStages) mbar_wait(&sm.empty[x % kStages], ((x - kStages) / kStages) & 1);
+          mbar_arrive_drop(&sm.empty[x % kStages]);
+        }
+      }
+      __syncwarp();
+    };
+    if (warp_done) leave(0);
+    const bool cull = !STATS && a.cutoff > 0.f;
+    for (int b = 0; b < nbatch && !warp_done; b++) {
+      const int s = b % kStages;
+      mbar_wait(&sm.full[s], (b / kStages) & 1);
+      if (*reinterpret_cast<volatile int *>(&sm.stop) == b + 1) break;
+      {
+        const uint32_t first = range.x + (uint32_t)b * kStageCands;
+        const int count = (int)min((uint32_t)kStageCands, range.y - first);
+        const uint32_t alive0 = __ballot_sync(0xffffffffu, !P0.done(thr));
+        const uint32_t alive1 = __ballot_sync(0xffffffffu, !P1.done(thr));
+        uint32_t pm0 = 0u, pm1 = 0u;
+        if (lane < count) {
+          const uint32_t bm = cull ? sm.bmask[s][lane] : 0xffu;
+          const int4 bb = rec_bbox(sm.rec[s][lane]);
+          if ((bm >> q0) & 1u) pm0 = block_mask(bb, rx0, ry0) & alive0;
+          if ((bm >> (q0 + 2)) & 1u) pm1 = block_mask(bb, rx0, ry0 + 4) & alive1;
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, (pm0 | pm1) != 0u);
+        uint32_t vis0 = 0, vis1 = 0;
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          const float4 *rec = sm.rec[s][j];
+          const uint32_t pj0 = __shfl_sync(0xffffffffu, pm0, j), pj1 = __shfl_sync(0xffffffffu, pm1, j);
+          const bool act0 = !P0.done(thr) && ((pj0 >> lane) & 1u);
+          const bool act1 = !P1.done(thr) && ((pj1 >> lane) & 1u);
+          const bool any0 = __any_sync(0xffffffffu, act0), any1 = __any_sync(0xffffffffu, act1);
+          if (!(any0 || any1)) continue;
+          if (STATS) {
+            n_warp_evals += (any0 ? 1u : 0u) + (any1 ? 1u : 0u);
+            n_eval += (act0 ? 1u : 0u) + (act1 ? 1u : 0u);
+          }
+          const int pos = (int)first + j;
+          bool bl0 = false, bl1 = false;
+          if (any0 && any1) {
+            if (MAXK == 8) {
+              const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
+              if (nl == 5) fwd_pair<5, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+              else if (nl == 6) fwd_pair<6, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+              else if (nl == 4) fwd_pair<4, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+              else fwd_pair<0, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+            } else {
+              fwd_pair<0, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+            }
+          } else {
+            // one of the two 8x4 blocks: the single-pixel evaluation
+            FwdPixel &P = any0 ? P0 : P1;
+            const bool act = any0 ? act0 : act1;
+            const float qy = any0 ? qy0 : qy0 + 4.f;
+            bool bl = false;
+            if (act) {
+              if (MAXK == 8) {
+                const int nl = __float_as_int(rec[2].z);
+                if (nl == 5) bl = fwd_candidate<5, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+                else if (nl == 6) bl = fwd_candidate<6, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+                else if (nl == 4) bl = fwd_candidate<4, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+                else bl = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+              } else {
+                bl = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+              }
+            }
+            if (any0) bl0 = bl; else bl1 = bl;
+          }
+          if (REC && bl0) rec0[P0.nblend - 1] = pos;
+          if (REC && bl1) rec1[P1.nblend - 1] = pos;
+          const bool b0 = __any_sync(0xffffffffu, bl0), b1 = __any_sync(0xffffffffu, bl1);
+          if (b0) vis0 |= 1u << j;
+          if (b1) vis1 |= 1u << j;
+          if ((b0 || b1) && __all_sync(0xffffffffu, P0.done(thr) && P1.done(thr))) {
+            warp_done = true;
+            break;
+          }
+        }
+        if (lane == 0) {
+          if (vis0 | vis1) atomicOr(&sm.vis[s], vis0 | vis1);
+          const size_t word = (size_t)(range.x >> 5) + tile + b;
+          a.blend_mask[(size_t)q0 * a.mask_words + word] = vis0;
+          a.blend_mask[(size_t)(q0 + 2) * a.mask_words + word] = vis1;
+        }
+      }
+      __syncwarp();
+      if (warp_done) {
+        leave(b);
+      } else if (lane == 0) {
+        mbar_arrive(&sm.empty[s]);
+      }
+    }
+    n_blend = (unsigned)(P0.nblend + P1.nblend);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const FwdPixel &P = h ? P1 : P0;
+      const int py = py0 + 4 * h;
+      if (px < a.width && py < a.height) {
+        const size_t p = (size_t)py * a.width + px;
+        const float v0 = fmaf(P.T, a.bg[0], P.C0), v1 = fmaf(P.T, a.bg[1], P.C1), v2 = fmaf(P.T, a.bg[2], P.C2);
+        a.image[3 * p] = fminf(fmaxf(v0, 0.f), 1.f);
+        a.image[3 * p + 1] = fminf(fmaxf(v1, 0.f), 1.f);
+        a.image[3 * p + 2] = fminf(fmaxf(v2, 0.f), 1.f);
+        a.final_T[p] = P.T;
+        a.pixel_T[p] = P.T;
+        a.weight_sum[p] = 1.f - P.T;
+        a.count[p] = P.nblend;
+        if (a.depth) a.depth[p] = P.D;
+        a.pixel_last[p] = P.last;
+        a.pixel_clamp[p] = (uint8_t)((v0 >= 0.f && v0 <= 1.f) | ((v1 >= 0.f && v1 <= 1.f) << 1) |
+                                     ((v2 >= 0.f && v2 <= 1.f) << 2));
+      }
+    }
+  }
+  if (STATS) {
+    block_add_u64(a.stats + S_FWD_EVALS, n_eval);
+    block_add_u64(a.stats + S_FWD_LINES, n_lines);
+    block_add_u64(a.stats + S_FWD_BLENDS, n_blend);
+    block_add_u64(a.stats + S_FWD_WARP_EVALS, lane == 0 ? n_warp_evals : 0u);
+  }
+}
+
 // 32 per-lane values -> lane L holds the warp sum of value L.
 __device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
   const int lane = threadIdx.x & 31;
@@ -1061,6 +1357,19 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
     a.ahead = 0;
 #endif
   }
+#ifndef CS_FWD_PPL1
+  a.ahead = a.ahead / CS_FWD_MINB * CS_FWD2_MINB;
+  if (L.max_k == 8) {
+    auto k = rec ? forward2_kernel<8, false, true> : stats ? forward2_kernel<8, true> : forward2_kernel<8, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
+    k<<<tiles, pipe_threads<4>(), sizeof(PipeSmem<8, CS_FWD_STAGES>), s>>>(a);
+  } else {
+    auto k = rec ? forward2_kernel<16, false, true> : stats ? forward2_kernel<16, true> : forward2_kernel<16, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_FWD_STAGES>));
+    k<<<tiles, pipe_threads<4>(), sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
+  }
+  return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+#endif
   if (L.max_k == 8) {
     auto k = rec ? forward_kernel<8, false, true> : stats ? forward_kernel<8, true> : forward_kernel<8, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
