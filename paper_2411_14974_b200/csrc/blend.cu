@@ -1093,6 +1093,123 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
   return true;
 }
 
+// The gradient terms of one pixel (bwd_candidate after its evaluation), with
+// the blend decision as a predicate: a pixel that did not blend adds exact
+// zeros (v never holds -0, so v + 0 == v) and keeps its state -- the same
+// sums, in the same order, as the branch in bwd_candidate.
+template <int NL, int MAXK, int VN>
+__device__ __forceinline__ void bwd_terms(const LineSet<NL, MAXK> &L, const float (&z)[LineSet<NL, MAXK>::kN],
+                                          const Eval &e, bool ok, float dx, float dy, float4 h0, float4 h1,
+                                          float4 h2, BwdPixel &P, float (&v)[VN]) {
+  constexpr int N = LineSet<NL, MAXK>::kN;
+  const float o = h0.w, sig = h0.z, dls = h2.y, inv_dls = h2.w;
+  const float om = fmaxf(fmaf(o, e.J, h2.x), 1e-6f);  // 1 - alpha
+#ifdef CS_EXACT_RECIP
+  const float rom = 1.f / om;
+#else
+  const float rom = rcp(om);
+#endif
+  const float Tp = P.T * rom;
+  const float w = ok ? Tp * e.alpha : 0.f;
+  v[A_DC] += P.g0 * w;
+  v[A_DC + 1] += P.g1 * w;
+  v[A_DC + 2] += P.g2 * w;
+  const float gc = fmaf(P.g0, h1.x, fmaf(P.g1, h1.y, P.g2 * h1.z));   // g . c
+  float dA = fmaf(Tp, gc, -P.GS * rom);
+  if (!ok || !(e.alpha_raw < (float)kAlphaMaxD)) dA = 0.f;
+  v[A_DOEFF] += dA * e.I;
+  const float dI = dA * o;
+  const float slope = e.I * e.J;
+  const float dphi = -sig * slope * dI;
+  v[A_DSIG] += ok ? -(e.phi2 * kLn2) * slope * dI : 0.f;
+  const float dscale = dphi * (dls * kLn2);
+  float wz = 0.f;
+#pragma unroll
+  for (int l = 0; l < N; l++) {
+    if (L.has(l)) {
+      const float wl = acc_ex2(z[l] - e.phi2);
+      wz = fmaf(wl, z[l], wz);
+      const float dL = dscale * wl;
+      v[A_LINES + 3 * l] += dL * dx;
+      v[A_LINES + 3 * l + 1] += dL * dy;
+      v[A_LINES + 3 * l + 2] += dL;
+    }
+  }
+  v[A_DDEL] += ok ? dphi * wz * inv_dls : 0.f;
+  P.GS = fmaf(w, gc, P.GS);
+  if (ok) P.T = Tp;
+}
+// z_l and sum 2^z_l at (dx, dy): eval_field's expressions (ACC) and order.
+template <int NL, int MAXK>
+__device__ __forceinline__ float line_sum_z(const LineSet<NL, MAXK> &L, float dx, float dy,
+                                            float (&z)[LineSet<NL, MAXK>::kN]) {
+  constexpr int N = LineSet<NL, MAXK>::kN;
+  float ex[N];
+#pragma unroll
+  for (int l = 0; l < N; l++) {
+    if (L.has(l)) {
+      z[l] = fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]));
+      ex[l] = acc_ex2(z[l]);
+    } else {
+      ex[l] = 0.f;
+    }
+  }
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int l = 0; l + w < N; l += 2 * w) ex[l] += ex[l + w];
+  return ex[0];
+}
+template <int NL, int MAXK>
+__device__ __forceinline__ float lse_shifted_z(const LineSet<NL, MAXK> &L, const float (&z)[LineSet<NL, MAXK>::kN]) {
+  constexpr int N = LineSet<NL, MAXK>::kN;
+  float m = -INFINITY;
+#pragma unroll
+  for (int l = 0; l < N; l++)
+    if (L.has(l)) m = fmaxf(m, z[l]);
+  float s2 = 0.f;
+#pragma unroll
+  for (int l = 0; l < N; l++)
+    if (L.has(l)) s2 += acc_ex2(z[l] - m);
+  return m + acc_lg2(s2);
+}
+__device__ __forceinline__ Eval eval_finish_acc(float phi2, float sig, float o) {
+  Eval e;
+  const float u = acc_ex2(sig * phi2);
+  e.I = acc_rcp(1.f + u);
+  e.J = u > 1.f ? 1.f - e.I : u * e.I;
+  e.alpha_raw = o * e.I;
+  e.alpha = fminf(e.alpha_raw, (float)kAlphaMaxD);
+  e.phi2 = phi2;
+  return e;
+}
+// One candidate at both pixels of the lane (rows r and r + 4): one line load,
+// two independent evaluation chains, the terms added pixel 0 then pixel 1
+// (the order of the per-pixel calls).
+template <int NL, int MAXK, bool STATS, int VN>
+__device__ __forceinline__ void bwd_pair(const float4 *rec, float qx, float qy0, bool act0, bool act1, float cutoff,
+                                         BwdPixel &P0, BwdPixel &P1, float (&v)[VN], unsigned &n_lines, bool &ok0,
+                                         bool &ok1) {
+  constexpr int N = LineSet<NL, MAXK>::kN;
+  const float4 h0 = rec[0], h2 = rec[2];
+  LineSet<NL, MAXK> L;
+  L.load(rec, __float_as_int(h2.z));
+  float z0[N], z1[N];
+  const float s0 = line_sum_z(L, qx, qy0, z0), s1 = line_sum_z(L, qx, qy0 + 4.f, z1);
+  float phi0 = acc_lg2(s0), phi1 = acc_lg2(s1);
+  if (!(lse_in_range(s0) && lse_in_range(s1))) {
+    if (!lse_in_range(s0)) phi0 = lse_shifted_z(L, z0);
+    if (!lse_in_range(s1)) phi1 = lse_shifted_z(L, z1);
+  }
+  const Eval e0 = eval_finish_acc(phi0, h0.z, h0.w), e1 = eval_finish_acc(phi1, h0.z, h0.w);
+  if (STATS) n_lines += (unsigned)L.nl * ((act0 ? 1u : 0u) + (act1 ? 1u : 0u));
+  ok0 = act0 && e0.alpha >= cutoff;
+  ok1 = act1 && e1.alpha >= cutoff;
+  const float4 h1 = rec[1];
+  bwd_terms(L, z0, e0, ok0, qx, qy0, h0, h1, h2, P0, v);
+  bwd_terms(L, z1, e1, ok1, qx, qy0 + 4.f, h0, h1, h2, P1, v);
+}
+
 // Backward blend (backward.py:110-205): the producer streams the tile list
 // back to front from the block's largest `last`; each consumer warp culls a
 // stage by ballot, reconstructs T_prev = T / (1 - alpha) per pixel and
@@ -1234,6 +1351,11 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
             any_act |= act[h];
           }
           bool contrib = false;
+#ifndef CS_BWD_NO_PAIR
+          const bool pair = PPL == 2 && __any_sync(0xffffffffu, act[0]) && __any_sync(0xffffffffu, act[PPL - 1]);
+#else
+          const bool pair = false;
+#endif
 #define CS_BWD2_PX(NLV, H)                                                                       \
   if (H < PPL && act[H % PPL]) {                                                                   \
     const bool c_ = bwd_candidate<NLV, MAXK, STATS>(rec, qx, qy0 + (float)(4 * (H % PPL)), a.cutoff, P[H % PPL], v, n_lines); \
@@ -1241,7 +1363,24 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
     if (STATS) n_bblend += (unsigned)c_;                                                           \
   }
 #define CS_BWD2_CASE(NLV) CS_BWD2_PX(NLV, 0) CS_BWD2_PX(NLV, 1) CS_BWD2_PX(NLV, 2) CS_BWD2_PX(NLV, 3)
-          if (MAXK == 8) {
+#define CS_BWD2_PAIR(NLV)                                                                        \
+  {                                                                                                \
+    bool o0_, o1_;                                                                                 \
+    bwd_pair<NLV, MAXK, STATS>(rec, qx, qy0, act[0], act[PPL - 1], a.cutoff, P[0], P[PPL - 1], v, n_lines, o0_, o1_); \
+    contrib = o0_ || o1_;                                                                          \
+    if (STATS) n_bblend += (unsigned)o0_ + (unsigned)o1_;                                         \
+  }
+          if (pair) {
+            if (MAXK == 8) {
+              const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
+              if (nl == 5) CS_BWD2_PAIR(5)
+              else if (nl == 6) CS_BWD2_PAIR(6)
+              else if (nl == 4) CS_BWD2_PAIR(4)
+              else CS_BWD2_PAIR(0)
+            } else {
+              CS_BWD2_PAIR(0)
+            }
+          } else if (MAXK == 8) {
             const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
             if (nl == 5) { CS_BWD2_CASE(5) }
             else if (nl == 6) { CS_BWD2_CASE(6) }
@@ -1250,6 +1389,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           } else {
             CS_BWD2_CASE(0)
           }
+#undef CS_BWD2_PAIR
 #undef CS_BWD2_CASE
 #undef CS_BWD2_PX
           if (STATS) n_warp_evals += __any_sync(0xffffffffu, any_act) ? 1u : 0u;
