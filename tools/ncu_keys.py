@@ -43,7 +43,7 @@ for rep in sys.argv[1:]:
             print(f"   {label:32s} {d[k]:>16s} {u.get(k, '')}")
     stalls = []
     for k in h:
-        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and k.endswith(".sum") and "not_issued" not in k:
+        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and "not_issued" not in k:
             try:
                 stalls.append((float(d[k].replace(",", "")), k))
             except ValueError:
