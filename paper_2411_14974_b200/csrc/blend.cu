@@ -216,12 +216,12 @@ template <int NC> __host__ __device__ constexpr int pipe_threads() { return 32 *
 // Ring depth: the forward stops early (saturated pixels), so a deep ring
 // mostly prefetches records nobody evaluates; the backward walks the whole
 // list up to each warp's last candidate and profits from more lookahead
-// (measured: 4 / 6 stages best).
+// (measured per kernel: the counts below).
 #ifndef CS_FWD_STAGES
-#define CS_FWD_STAGES 4
+#define CS_FWD_STAGES 3   // forward2: 3 / 4 / 5 / 6 stages 327 / 329 / 335 / 351 us
 #endif
 #ifndef CS_BWD_STAGES
-#define CS_BWD_STAGES 6
+#define CS_BWD_STAGES 5   // paired backward: 3 / 4 / 5 / 6 / 7 / 8 stages 620 / 672 / 622 / 632 / 650 / 736 us
 #endif
 constexpr int kStageCands = 32;
 // longest back-off sleep of the producer waiting for a free stage
