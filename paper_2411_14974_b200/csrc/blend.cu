@@ -893,11 +893,17 @@ __global__ void __launch_bounds__(pipe_threads<4>(), CS_FWD2_MINB) forward2_kern
       }
       __syncwarp();
     };
+    WS_T0(tc);
     if (warp_done) leave(0);
     const bool cull = !STATS && a.cutoff > 0.f;
     for (int b = 0; b < nbatch && !warp_done; b++) {
       const int s = b % kStages;
-      mbar_wait(&sm.full[s], (b / kStages) & 1);
+      {
+        WS_T0(tw);
+        mbar_wait(&sm.full[s], (b / kStages) & 1);
+        if (lane == 0) WS_ADD(1, tw);
+        if (lane == 0 && b == 0) WS_ADD(8, tw);
+      }
       if (*reinterpret_cast<volatile int *>(&sm.stop) == b + 1) break;
       {
         const uint32_t first = range.x + (uint32_t)b * kStageCands;
@@ -981,6 +987,7 @@ __global__ void __launch_bounds__(pipe_threads<4>(), CS_FWD2_MINB) forward2_kern
         mbar_arrive(&sm.empty[s]);
       }
     }
+    if (lane == 0) WS_ADD(0, tc);
     n_blend = (unsigned)(P0.nblend + P1.nblend);
 #pragma unroll
     for (int h = 0; h < 2; h++) {
