@@ -166,6 +166,12 @@ __device__ __forceinline__ G g_rcp(G x) { return __frcp_rn(x); }
 __device__ __forceinline__ G g_rsqrt(G x) { return rsqrtf(x); }
 #endif
 
+#if defined(CS_CHAIN_ACC_F64) && !defined(CS_ACC_F32)
+typedef double AccR;
+#else
+typedef float AccR;
+#endif
+
 template <int MAXK, bool OW>
 __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainArgs a) {   // 5: the SH staging limits it anyway
   constexpr int kChainThreads = chain_threads<MAXK>();
@@ -208,15 +214,17 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
   }
   const int k = a.k;
   const G inv_k = G(1) / (G)k;
-  // the convex's screen-space accumulators, loaded as float4 up front
-  AccT acc[AF];
+  // the convex's screen-space accumulators, loaded up front (float64 sums
+  // rounded once to the chain's float32 arithmetic; -DCS_CHAIN_ACC_F64 keeps
+  // them in float64)
+  AccR acc[AF];
   {
-#ifdef CS_ACC_F64
+#ifndef CS_ACC_F32
     const double2 *acc2 = reinterpret_cast<const double2 *>(a.accum + i * AF);
 #pragma unroll
     for (int q = 0; q < AF / 2; q++) {
       const double2 v = __ldg(acc2 + q);
-      acc[2 * q] = v.x; acc[2 * q + 1] = v.y;
+      acc[2 * q] = (AccR)v.x; acc[2 * q + 1] = (AccR)v.y;
     }
 #else
     const float4 *acc4 = reinterpret_cast<const float4 *>(a.accum + i * AF);
@@ -312,8 +320,8 @@ __global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainAr
       const G gs = (G)acc[A_LINES + 3 * j + 2];
       // reference gn = sum dL*q - gs*v = sum dL*(q-a) - gs*(v-a); u is anchor-relative
       // (the cancellation of the two sums is formed in the accumulator type)
-      const G gx = (G)fma(-acc[A_LINES + 3 * j + 2], (AccT)ux, acc[A_LINES + 3 * j]);
-      const G gy = (G)fma(-acc[A_LINES + 3 * j + 2], (AccT)uy, acc[A_LINES + 3 * j + 1]);
+      const G gx = (G)fma(-acc[A_LINES + 3 * j + 2], (AccR)ux, acc[A_LINES + 3 * j]);
+      const G gy = (G)fma(-acc[A_LINES + 3 * j + 2], (AccR)uy, acc[A_LINES + 3 * j + 1]);
       const G nd = fma(nx, gx, ny * gy);
       const G rx = (gx - nx * nd) * il, ry = (gy - ny * nd) * il;
       s_dx[v][t] += -ry;

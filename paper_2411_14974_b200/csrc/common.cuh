@@ -60,11 +60,15 @@ template <int MAXK> struct Acc {
   static constexpr int kFloats = A_LINES + 3 * MAXK;
 };
 // Accumulator element type: the per-warp float32 partial sums of the
-// backward blend are added into AccT by global atomics.
-#ifdef CS_ACC_F64
-typedef double AccT;
-#else
+// backward blend are added into AccT by global atomics.  float64 (native
+// red.global.add.f64): the order of those additions varies from run to run,
+// and in float32 a convex spread over thousands of tiles changed its
+// near-cancelling sums by up to ~7e-4 relative between runs; in float64 the
+// order costs ~1e-16.  -DCS_ACC_F32 for the float32 accumulators.
+#ifdef CS_ACC_F32
 typedef float AccT;
+#else
+typedef double AccT;
 #endif
 
 // Counters at the head of the workspace.
