@@ -269,7 +269,7 @@ def graph_times(r, fr, d_image, grads, flush, dev, steps: int, warmup: int, back
         return g
 
     def fwdbwd():
-        r.launch_forward(fr, 0, 2)
+        r.launch_forward(fr, 0, 2, zero_accumulators=True)   # the accumulator reset runs under the forward
         r.launch_backward(fr, d_image, grads, 0, 0)
         r.launch_backward(fr, d_image, grads, 1, 1, overwrite=True)
 
@@ -592,7 +592,7 @@ def main():
         return g
 
     def fwdbwd():
-        r.launch_forward(fr, 0, 2)
+        r.launch_forward(fr, 0, 2, zero_accumulators=True)   # the accumulator reset runs under the forward
         r.launch_backward(fr, d_image, grads, 0, 0)
         r.launch_backward(fr, d_image, grads, 1, 1, overwrite=True)   # fresh gradients, no zeroing pass
 

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 7
+#define CS_ABI_VERSION 8
 
 #if defined(__GNUC__)
 #define CS_API __attribute__((visibility("default")))
@@ -264,10 +264,22 @@ CS_API int cs_backward_signal(const cs_camera *cam, const cs_settings *set, cons
  * half of the accumulation.  CS_WORK_COUNTERS: count the backward blend's
  * work (see cs_forward_ex).  cs_backward == flags 0, stages 0..1. */
 #define CS_GRADS_OVERWRITE 1u
+/* CS_ACCUM_ZEROED: the backward blend's screen-space accumulators were
+ * already reset by cs_zero_accumulators, ordered before this call (stage 0
+ * then skips its own reset). */
+#define CS_ACCUM_ZEROED 4u
 CS_API int cs_backward_ex(const cs_camera *cam, const cs_settings *set, const cs_params *params,
                           void *workspace, size_t workspace_bytes, int64_t pair_capacity,
                           const float *d_image, const cs_grads *grads, const cs_view_signal *signal,
                           uint32_t flags, int32_t first_stage, int32_t last_stage, void *stream);
+
+/* Reset the backward blend's per-convex screen-space accumulators (the
+ * first half of stage 0 of cs_backward_ex; no reference counterpart -- the
+ * reference accumulates into fresh NumPy arrays, backward.py:125-131).  As
+ * its own entry it can run on a second stream while the forward of the same
+ * view renders; the backward then passes CS_ACCUM_ZEROED. */
+CS_API int cs_zero_accumulators(const cs_camera *cam, const cs_settings *set, const cs_params *params,
+                                void *workspace, size_t workspace_bytes, int64_t pair_capacity, void *stream);
 
 /* The chain stage (stage 1) of cs_backward_ex over the convexes
  * [first, last) only: the gradient rows of a convex range are final as soon

@@ -15,13 +15,15 @@ EXPORTS = ("cs_abi_version", "cs_error_string", "cs_workspace_layout", "cs_forwa
            "cs_forward_stages", "cs_forward_ex", "cs_backward_stages", "cs_read_counters", "cs_graham_scan_batch",
            "cs_backward_signal", "cs_backward_ex", "cs_image_loss_workspace", "cs_image_loss", "cs_adam_step",
            "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags", "cs_density_scatter",
-           "cs_read_status", "cs_forward_record", "cs_prepare_view_export", "cs_backward_chain_range")
-ABI_VERSION = 7
+           "cs_read_status", "cs_forward_record", "cs_prepare_view_export", "cs_backward_chain_range",
+           "cs_zero_accumulators")
+ABI_VERSION = 8
 ERR_WORKSPACE = 3     # CS_ERR_WORKSPACE
 ERR_NONFINITE = 4     # CS_ERR_NONFINITE
 ERR_UNSUPPORTED = 5   # CS_ERR_UNSUPPORTED
 GRADS_OVERWRITE = 1   # CS_GRADS_OVERWRITE
 WORK_COUNTERS = 2     # CS_WORK_COUNTERS
+ACCUM_ZEROED = 4      # CS_ACCUM_ZEROED
 
 _vp = ctypes.c_void_p
 
@@ -128,6 +130,8 @@ def load(path: str = None):
                                           ctypes.POINTER(CsParams), _vp, ctypes.c_size_t, ctypes.c_int64,
                                           ctypes.POINTER(CsGrads), ctypes.POINTER(CsViewSignal), ctypes.c_uint32,
                                           ctypes.c_int64, ctypes.c_int64, _vp]
+    L.cs_zero_accumulators.argtypes = [ctypes.POINTER(CsCamera), ctypes.POINTER(CsSettings),
+                                       ctypes.POINTER(CsParams), _vp, ctypes.c_size_t, ctypes.c_int64, _vp]
     L.cs_prepare_view_export.argtypes = [ctypes.POINTER(CsCamera), ctypes.POINTER(CsSettings),
                                          ctypes.POINTER(CsParams), _vp, ctypes.c_size_t, ctypes.c_int64,
                                          ctypes.POINTER(CsViewExport), _vp]
@@ -154,7 +158,7 @@ def load(path: str = None):
                "cs_image_loss_workspace",
                "cs_image_loss", "cs_adam_step", "cs_checkpoint_unpack", "cs_checkpoint_pack", "cs_density_flags",
                "cs_density_scatter", "cs_read_status", "cs_forward_record", "cs_prepare_view_export",
-               "cs_backward_chain_range"):
+               "cs_backward_chain_range", "cs_zero_accumulators"):
         getattr(L, fn).restype = ctypes.c_int
     if L.cs_abi_version() != ABI_VERSION:
         raise CsError(f"ABI mismatch: library {L.cs_abi_version()} != {ABI_VERSION}")

@@ -1536,18 +1536,24 @@ __global__ void __launch_bounds__(512) zero_kernel(float4 *p, size_t n4) {
   for (size_t i = (size_t)blockIdx.x * 512 + threadIdx.x; i < n4; i += (size_t)gridDim.x * 512) __stcs(p + i, z);
 }
 
-int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                          const cs_layout &L, char *ws, const float *d_image, bool stats, cudaStream_t s) {
-  BlendArgs a = make_args(cam, set, L, ws);
-  a.d_image = d_image;
+int launch_zero_accumulators(const cs_params &p, const cs_layout &L, char *ws, cudaStream_t s) {
   if (p.n > 0) {
+    AccT *acc = reinterpret_cast<AccT *>(ws + L.grad_accum);
 #ifdef CS_MEMSET_ACCUM
-    cudaMemsetAsync(a.accum, 0, (size_t)p.n * L.acc_floats * sizeof(AccT), s);
+    cudaMemsetAsync(acc, 0, (size_t)p.n * L.acc_floats * sizeof(AccT), s);
 #else
     const size_t n4 = (size_t)p.n * L.acc_floats * sizeof(AccT) / 16;   // acc_floats is a multiple of 4
-    zero_kernel<<<(int)std::min<size_t>((n4 + 511) / 512, 148 * 8), 512, 0, s>>>(reinterpret_cast<float4 *>(a.accum), n4);
+    zero_kernel<<<(int)std::min<size_t>((n4 + 511) / 512, 148 * 8), 512, 0, s>>>(reinterpret_cast<float4 *>(acc), n4);
 #endif
   }
+  return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+}
+
+int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
+                          const cs_layout &L, char *ws, const float *d_image, bool stats, bool zero, cudaStream_t s) {
+  BlendArgs a = make_args(cam, set, L, ws);
+  a.d_image = d_image;
+  if (zero) launch_zero_accumulators(p, L, ws, s);
   const int tiles = L.tiles_x * L.tiles_y;
   if (L.max_k == 8) {
     auto k = stats ? backward_kernel<8, CS_BWD_PPL, true> : backward_kernel<8, CS_BWD_PPL, false>;

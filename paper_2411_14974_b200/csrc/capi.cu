@@ -166,7 +166,7 @@ static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_
                          const cs_view_signal *sig, uint32_t flags, int32_t first_stage, int32_t last_stage,
                          void *stream) {
   if (!params || !grads || !workspace || !d_image) return CS_ERR_ARG;
-  if (flags & ~(uint32_t)(CS_GRADS_OVERWRITE | CS_WORK_COUNTERS)) return CS_ERR_ARG;
+  if (flags & ~(uint32_t)(CS_GRADS_OVERWRITE | CS_WORK_COUNTERS | CS_ACCUM_ZEROED)) return CS_ERR_ARG;
   if (sig && (!sig->sigma_signal || !sig->sigma_views || !sig->visible)) return CS_ERR_ARG;
   if (first_stage < 0 || last_stage > 1 || first_stage > last_stage) return CS_ERR_ARG;
   cs_layout L;
@@ -180,12 +180,23 @@ static int backward_impl(const cs_camera *cam, const cs_settings *set, const cs_
   char *ws = static_cast<char *>(workspace);
   if (first_stage == 0) {
     cudaMemsetAsync(ws + L.counters + sizeof(uint32_t) * cs::C_NONFINITE, 0, sizeof(uint32_t), s);
-    if ((rc = cs::launch_backward_blend(*cam, *set, *params, L, ws, d_image, (flags & CS_WORK_COUNTERS) != 0, s)))
+    if ((rc = cs::launch_backward_blend(*cam, *set, *params, L, ws, d_image, (flags & CS_WORK_COUNTERS) != 0,
+                                        (flags & CS_ACCUM_ZEROED) == 0, s)))
       return rc;
   }
   if (last_stage == 1)
     return cs::launch_chain(*cam, *set, *params, L, ws, *grads, sig, (flags & CS_GRADS_OVERWRITE) != 0, s);
   return CS_OK;
+}
+
+int cs_zero_accumulators(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,
+                         size_t workspace_bytes, int64_t pair_capacity, void *stream) {
+  if (!params || !workspace) return CS_ERR_ARG;
+  cs_layout L;
+  int rc = cs_workspace_layout(cam, set, params->n, params->k, pair_capacity, &L);
+  if (rc) return rc;
+  if (workspace_bytes < L.total_bytes) return CS_ERR_WORKSPACE;
+  return cs::launch_zero_accumulators(*params, L, static_cast<char *>(workspace), reinterpret_cast<cudaStream_t>(stream));
 }
 
 int cs_backward_chain_range(const cs_camera *cam, const cs_settings *set, const cs_params *params, void *workspace,

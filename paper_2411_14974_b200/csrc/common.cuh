@@ -268,7 +268,8 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
                          const cs_layout &L, char *ws, const cs_frame &f, bool stats, cudaStream_t s,
                          const int64_t *rec_off = nullptr, int32_t *rec_pos = nullptr);
 int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs_params &p,
-                          const cs_layout &L, char *ws, const float *d_image, bool stats, cudaStream_t s);
+                          const cs_layout &L, char *ws, const float *d_image, bool stats, bool zero, cudaStream_t s);
+int launch_zero_accumulators(const cs_params &p, const cs_layout &L, char *ws, cudaStream_t s);
 int launch_chain(const cs_camera &cam, const cs_settings &set, const cs_params &p,
                  const cs_layout &L, char *ws, const cs_grads &g, const cs_view_signal *sig, bool overwrite,
                  cudaStream_t s, int64_t first = 0, int64_t last = -1);

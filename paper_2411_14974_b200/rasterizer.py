@@ -141,6 +141,7 @@ class Rasterizer:
         self.device = _device(device)
         self.growth = growth
         self._cap_hint = {}
+        self._side_streams = {}
         _lib.load()
 
     def _initial_capacity(self, st: SceneTensors, cam: Camera) -> int:
@@ -152,7 +153,12 @@ class Rasterizer:
 
     def forward(self, scene, cam: Camera, mode=ScalingMode.DEPTH, settings: RenderSettings = RenderSettings(),
                 workspace: Optional[Workspace] = None, capacity: Optional[int] = None, check: bool = True,
-                outputs: Optional[dict] = None) -> Frame:
+                outputs: Optional[dict] = None, zero_accumulators: bool = False) -> Frame:
+        """Render (cs_forward).  ``check``: read the pair count back and
+        re-render with a larger capacity on overflow (one host sync).
+        ``zero_accumulators``: also reset the backward accumulators on a side
+        stream (``zero_accumulators_async``; overlapping the forward when
+        ``check`` is off)."""
         st = as_scene_tensors(scene, self.device)
         cam_c = camera_struct(cam)
         set_c = settings_struct(settings, mode, st.background)
@@ -172,28 +178,61 @@ class Rasterizer:
         stream = torch.cuda.current_stream(self.device).cuda_stream
         while True:
             ws.ensure(cam_c, set_c, n, st.k, cap)
+            zeroed = self._fork_zero(cam_c, set_c, params_c, ws, cap) if zero_accumulators and not check else None
             _lib.check(_lib.load().cs_forward(ctypes.byref(cam_c), ctypes.byref(set_c), ctypes.byref(params_c),
                                               ws.ptr, ws.nbytes, cap, ctypes.byref(frame_c), stream), "cs_forward")
             fr = Frame(outputs["image"], outputs["final_T"], outputs["count"], outputs["weight_sum"],
                        outputs["depth"], outputs["visible"][:n], ws, st, cam_c, set_c, params_c, cap)
             fr.extras["frame_c"] = frame_c
             if not check:
+                if zeroed is not None:
+                    fr.extras["accum_zeroed"] = zeroed
                 return fr
             counts = (ctypes.c_uint32 * 4)()
             _lib.check(_lib.load().cs_read_counters(ctypes.c_void_p(ws.ptr), counts, stream), "cs_read_counters")
             fr.n_visible, fr.n_pairs = int(counts[0]), int(counts[1])
             if counts[2] == 0:
                 self._cap_hint[(n, W, H)] = max(cap, int(fr.n_pairs * self.growth) + 1024)
+                if zero_accumulators:
+                    self.zero_accumulators_async(fr)
                 return fr
             cap = int(fr.n_pairs * self.growth) + 1024   # overflow: grow and re-render
             if cap >= (1 << 30):
                 raise _lib.CsError(f"{fr.n_pairs} tile pairs exceed the supported 2^30")
 
-    def launch_forward(self, fr: Frame, first_stage: int = 0, last_stage: int = 2, work_counters: bool = False):
+    def _fork_zero(self, cam_c, set_c, params_c, ws, cap) -> torch.cuda.Event:
+        cur = torch.cuda.current_stream(self.device)
+        side = self._side_streams.get(cur.cuda_stream)
+        if side is None:   # one side stream per issuing stream (view lanes run concurrently)
+            side = self._side_streams[cur.cuda_stream] = torch.cuda.Stream(self.device)
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        side.wait_event(fork)
+        _lib.check(_lib.load().cs_zero_accumulators(ctypes.byref(cam_c), ctypes.byref(set_c), ctypes.byref(params_c),
+                                                    ws.ptr, ws.nbytes, cap, side.cuda_stream), "cs_zero_accumulators")
+        done = torch.cuda.Event()
+        done.record(side)
+        return done
+
+    def zero_accumulators_async(self, fr: Frame):
+        """Reset ``fr``'s backward accumulators on a side stream, forked from
+        the current stream now (after everything already queued on it, e.g.
+        the previous chain that read them); the next ``launch_backward`` of
+        the frame joins it and skips its own reset (CS_ACCUM_ZEROED).  Issued
+        before the forward's launches, the 256 MB reset (1M convexes) runs
+        under the latency-bound forward kernels instead of after them."""
+        fr.extras["accum_zeroed"] = self._fork_zero(fr.cam_c, fr.set_c, fr.params_c, fr.workspace, fr.capacity)
+
+    def launch_forward(self, fr: Frame, first_stage: int = 0, last_stage: int = 2, work_counters: bool = False,
+                       zero_accumulators: bool = False):
         """Re-run forward stages of an existing frame (same scene tensors,
         camera, workspace and outputs) without any host synchronisation;
         stages: 0 preprocess, 1 depth order + binning, 2 blend.
-        ``work_counters``: the blend also counts its work (``read_stats``)."""
+        ``work_counters``: the blend also counts its work (``read_stats``).
+        ``zero_accumulators``: reset the backward accumulators alongside
+        (``zero_accumulators_async``)."""
+        if zero_accumulators:
+            self.zero_accumulators_async(fr)
         ws = fr.workspace
         stream = torch.cuda.current_stream(self.device).cuda_stream
         _lib.check(_lib.load().cs_forward_ex(ctypes.byref(fr.cam_c), ctypes.byref(fr.set_c),
@@ -212,7 +251,14 @@ class Rasterizer:
         g = _lib.CsGrads(grads["points"].data_ptr(), grads["raw_delta"].data_ptr(), grads["raw_sigma"].data_ptr(),
                          grads["raw_opacity"].data_ptr(), grads["raw_mask"].data_ptr(), grads["sh"].data_ptr())
         ws = fr.workspace
-        stream = torch.cuda.current_stream(self.device).cuda_stream
+        cur = torch.cuda.current_stream(self.device)
+        stream = cur.cuda_stream
+        zeroed = 0
+        if first_stage == 0:
+            ev = fr.extras.pop("accum_zeroed", None)
+            if ev is not None:      # the reset forked by zero_accumulators_async
+                cur.wait_event(ev)
+                zeroed = _lib.ACCUM_ZEROED
         sig = None
         if signal is not None:
             if (first_stage, last_stage) != (0, 1):
@@ -223,8 +269,8 @@ class Rasterizer:
                                               d_image.data_ptr(), ctypes.byref(g),
                                               ctypes.byref(sig) if sig is not None else None,
                                               (_lib.GRADS_OVERWRITE if overwrite else 0) |
-                                              (_lib.WORK_COUNTERS if work_counters else 0), first_stage, last_stage,
-                                              stream), "cs_backward_ex")
+                                              (_lib.WORK_COUNTERS if work_counters else 0) | zeroed, first_stage,
+                                              last_stage, stream), "cs_backward_ex")
 
     def launch_chain_range(self, fr: Frame, grads: dict, first: int, last: int, signal=None):
         """Stage 1 (the per-convex chain) of a backward whose stage 0 ran,

@@ -365,10 +365,11 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
         cam, target = view
         ws, lw = ln["ws"], ln["lw"]
         if state["cap"] is None:      # first view ever: size the capacity with a checked forward
-            fr = r.forward(scene, cam, mode, settings, workspace=ws)
+            fr = r.forward(scene, cam, mode, settings, workspace=ws, zero_accumulators=True)
             state["cap"] = fr.capacity
-        else:
-            fr = r.forward(scene, cam, mode, settings, workspace=ws, capacity=state["cap"], check=False)
+        else:   # the accumulator reset runs on a side stream under the forward
+            fr = r.forward(scene, cam, mode, settings, workspace=ws, capacity=state["cap"], check=False,
+                           zero_accumulators=True)
         torch.maximum(ln["max"][0:2], ws.counters()[1:3], out=ln["max"][0:2])   # (pairs, overflow)
         loss = cuda_image_loss(fr.image, target, scene.raw_mask, config.lambda_dssim, config.beta_mask,
                                d_raw_mask=grads["raw_mask"], workspace=lw)

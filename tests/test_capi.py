@@ -129,7 +129,9 @@ def test_training_entry_points_validate_before_launching(lib):
     cfg = _lib.CsDensityConfig()
     assert lib.cs_density_flags(ctypes.byref(p), None, None, None, None, None, None, None) == 1
     assert lib.cs_density_flags(ctypes.byref(p), None, ctypes.byref(cfg), None, None, None, None, None) == 0
-    assert lib.cs_abi_version() == _lib.ABI_VERSION == 7
+    assert lib.cs_abi_version() == _lib.ABI_VERSION == 8
+    # cs_zero_accumulators validates before launching
+    assert lib.cs_zero_accumulators(None, None, None, None, 0, 0, None) == 1
 
 
 def test_backward_ex_validates_flags_and_signal(lib):
@@ -143,7 +145,7 @@ def test_backward_ex_validates_flags_and_signal(lib):
     g = _lib.CsGrads()
     one = ctypes.c_void_p(1)
     args = (ctypes.byref(cam), ctypes.byref(st), ctypes.byref(p), one, 1 << 30, 0, one, ctypes.byref(g))
-    assert lib.cs_backward_ex(*args, None, 4, 0, 1, None) == 1                     # unknown flag
+    assert lib.cs_backward_ex(*args, None, 8, 0, 1, None) == 1                     # unknown flag
     sig = _lib.CsViewSignal(None, None, None)
     assert lib.cs_backward_ex(*args, ctypes.byref(sig), 0, 0, 1, None) == 1        # null signal arrays
     assert lib.cs_backward_ex(*args, None, 1, 1, 0, None) == 1                     # stages out of order
