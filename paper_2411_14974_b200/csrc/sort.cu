@@ -37,7 +37,16 @@ constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortThreads = CS_SORT_THREADS;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = CS_SORT_ITEMS;
-constexpr int kSortChunk = kSortThreads * kSortItems;  // 4096 keys per chunk
+constexpr int kSortChunk = kSortThreads * kSortItems;  // 4096 keys per chunk (the pair sort)
+// keys per thread of the depth sort's chunks (binning at 1M @1080p with 1 /
+// 2 / 4 / 8 / 16: 283 / 261 / 246 / 236 / 238 us -- smaller chunks, more
+// blocks for the 1M keys, lose more to the longer look-back than they win;
+// the pair sort at 8 / 12 / 16: 236 / 241 / 244 us)
+#ifndef CS_DEPTH_SORT_ITEMS
+#define CS_DEPTH_SORT_ITEMS 8
+#endif
+constexpr int kDepthSortItems = CS_DEPTH_SORT_ITEMS;
+constexpr int kDepthChunk = kSortThreads * kDepthSortItems;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
@@ -119,18 +128,19 @@ __device__ __forceinline__ uint32_t block_exclusive_scan256(uint32_t v, uint32_t
   return s_warp[w] + inc - v;
 }
 
-template <typename KeyT>
-constexpr size_t onesweep_dyn_smem() { return (size_t)kSortChunk * (sizeof(KeyT) + sizeof(uint32_t)); }
+template <typename KeyT, int ITEMS>
+constexpr size_t onesweep_dyn_smem() { return (size_t)kSortThreads * ITEMS * (sizeof(KeyT) + sizeof(uint32_t)); }
 
 // One LSD digit.  Items are ranked per warp with __match_any_sync, the
 // chunk's digit counts are published for decoupled look-back, and the chunk
 // is first scattered into shared memory in digit order so that the global
 // writes come out as contiguous runs per digit (coalesced).
-template <typename KeyT>
+template <typename KeyT, int ITEMS>
 __global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(PassArgs<KeyT> a) {
+  constexpr int kChunk = kSortThreads * ITEMS;
   extern __shared__ __align__(16) unsigned char onesweep_dyn[];
   KeyT *s_keys = reinterpret_cast<KeyT *>(onesweep_dyn);
-  uint32_t *s_vals = reinterpret_cast<uint32_t *>(onesweep_dyn + sizeof(KeyT) * kSortChunk);
+  uint32_t *s_vals = reinterpret_cast<uint32_t *>(onesweep_dyn + sizeof(KeyT) * kChunk);
   __shared__ uint32_t s_hist[kSortWarps][kRadix];
   __shared__ uint32_t s_dexcl[kRadix];
   __shared__ uint32_t s_base[kRadix];
@@ -142,18 +152,18 @@ __global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(Pa
   __syncthreads();
   const uint32_t chunk = s_chunk;
   const uint32_t n = a.count ? *a.count : a.n_fixed;
-  const uint32_t start = chunk * kSortChunk;
+  const uint32_t start = chunk * kChunk;
   if (start >= n) return;  // no later chunk holds items, nobody looks back here
-  const uint32_t nvalid = min((uint32_t)kSortChunk, n - start);
+  const uint32_t nvalid = min((uint32_t)kChunk, n - start);
 
   const uint32_t lt_mask = (1u << lane) - 1u;
-  KeyT key[kSortItems];
-  uint32_t val[kSortItems];
-  uint32_t dig[kSortItems];
-  uint32_t rank[kSortItems];
-  const uint32_t wbase = start + w * (32 * kSortItems);
+  KeyT key[ITEMS];
+  uint32_t val[ITEMS];
+  uint32_t dig[ITEMS];
+  uint32_t rank[ITEMS];
+  const uint32_t wbase = start + w * (32 * ITEMS);
 #pragma unroll
-  for (int i = 0; i < kSortItems; i++) {
+  for (int i = 0; i < ITEMS; i++) {
     const uint32_t idx = wbase + i * 32 + lane;
     const bool valid = idx < n;
     key[i] = valid ? a.keys_in[idx] : (KeyT)0;
@@ -161,7 +171,7 @@ __global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(Pa
     dig[i] = valid ? (uint32_t)(key[i] >> a.shift) & (kRadix - 1) : kRadix;
   }
 #pragma unroll
-  for (int i = 0; i < kSortItems; i++) {
+  for (int i = 0; i < ITEMS; i++) {
     const uint32_t d = dig[i];
     // lanes holding the same digit: AND of 8 bit ballots (cheaper than MATCH)
     uint32_t peers = __ballot_sync(0xffffffffu, d < kRadix);
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(Pa
   // local scatter into digit order first: the predecessors' prefixes get
   // the scatter's time to appear before the look-back reads them
 #pragma unroll
-  for (int i = 0; i < kSortItems; i++) {
+  for (int i = 0; i < ITEMS; i++) {
     const uint32_t dd = dig[i];
     if (dd < kRadix) {
       const uint32_t pos = s_dexcl[dd] + s_hist[w][dd] + rank[i];
@@ -256,20 +266,21 @@ __global__ void __launch_bounds__(kSortThreads, CS_SORT_MINB) onesweep_kernel(Pa
 // Full LSD sort over `passes` digits starting at bit shift0.  Ping-pongs
 // (k0,v0) <-> (k1,v1); returns true when the result ends in (k1,v1).  With
 // hist_ready the caller has already accumulated the digit histograms.
-template <typename KeyT>
+template <typename KeyT, int ITEMS>
 static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uint32_t *count, int key_bits,
                        uint32_t n_fixed, uint32_t n_cap, int passes, int shift0, uint32_t *hist,
                        uint32_t *offsets, uint32_t *lookback, uint32_t *chunk_counters, bool hist_ready,
                        cudaStream_t s) {
-  const int chunks = (int)((n_cap + kSortChunk - 1) / kSortChunk);
+  constexpr int kChunk = kSortThreads * ITEMS;
+  const int chunks = (int)((n_cap + kChunk - 1) / kChunk);
   if (chunks == 0) return false;
   if (!hist_ready) {
     const int hist_blocks = min(chunks * 4, 148 * 8);
     radix_hist_kernel<KeyT><<<hist_blocks, kSortThreads, 0, s>>>(k0, count, n_fixed, passes, shift0, hist);
   }
   radix_offsets_kernel<<<passes, kRadix, 0, s>>>(hist, offsets);
-  constexpr size_t dyn = onesweep_dyn_smem<KeyT>();
-  cudaFuncSetAttribute(onesweep_kernel<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  constexpr size_t dyn = onesweep_dyn_smem<KeyT, ITEMS>();
+  cudaFuncSetAttribute(onesweep_kernel<KeyT, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   for (int p = 0; p < passes; p++) {
     PassArgs<KeyT> a;
     bool odd = p & 1;
@@ -284,7 +295,7 @@ static bool radix_sort(KeyT *k0, uint32_t *v0, KeyT *k1, uint32_t *v1, const uin
     a.offsets = offsets + p * kRadix;
     a.lookback = lookback + (size_t)p * chunks * kRadix;
     a.chunk_counter = chunk_counters + p;
-    onesweep_kernel<KeyT><<<chunks, kSortThreads, dyn, s>>>(a);
+    onesweep_kernel<KeyT, ITEMS><<<chunks, kSortThreads, dyn, s>>>(a);
   }
   return passes & 1;
 }
@@ -646,7 +657,7 @@ uint32_t blend_mask_words(int64_t cap, int tiles) {
 size_t scratch_bytes(int64_t n, int64_t cap, int pair_passes, int tiles, Scratch *sc, char *base) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return base ? base + o : nullptr; };
-  const size_t dchunks = (size_t)((n + kSortChunk - 1) / kSortChunk);
+  const size_t dchunks = (size_t)((n + kDepthChunk - 1) / kDepthChunk);
   const size_t pchunks = (size_t)((cap + kSortChunk - 1) / kSortChunk);
   const size_t lb_words = (8 * dchunks + pair_passes * pchunks) * kRadix;
   take(sizeof(uint32_t) * kMaxTileOrder);   // tile_order first: the blends find it at scratch + 0
@@ -732,7 +743,7 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
 #endif
     const int kb = min((int)((n + kSortThreads - 1) / kSortThreads), 148 * CS_KEY_BLOCKS_PER_SM);
     depth_key32_kernel<<<kb, kSortThreads, 0, s>>>(dkeys, counters, n, k32b, sc.dvals_alt, sc.hist);
-    radix_sort<uint32_t>(k32b, sc.dvals_alt, k32, order, nullptr, kDepthBits + 1, n, n, kDepthPasses, 0, sc.hist,
+    radix_sort<uint32_t, kDepthSortItems>(k32b, sc.dvals_alt, k32, order, nullptr, kDepthBits + 1, n, n, kDepthPasses, 0, sc.hist,
                          sc.offsets, sc.lookback, counters + C_CHUNK0, true, s);
     depth_fixup_kernel<<<(n + 255) / 256, 256, 0, s>>>(dkeys, counters, k32, order);
     // pairs land in the buffer that makes the sorted result end in (ptiles, pids)
@@ -747,8 +758,8 @@ int launch_binning(const cs_camera &cam, const cs_settings &set, const cs_params
       uint32_t *kb = (pp & 1) ? ptiles : sc.ptiles_alt, *vb = (pp & 1) ? pids : sc.pids_alt;
       int tile_bits = 0;
       while ((1 << tile_bits) < tiles) tile_bits++;
-      radix_sort<uint32_t>(ka, va, kb, vb, counters + C_NSORT, tile_bits, 0, (uint32_t)cap, pp, 0, sc.hist + 8 * kRadix,
-                           sc.offsets + 8 * kRadix, sc.lookback + 8 * ((n + kSortChunk - 1) / kSortChunk) * kRadix,
+      radix_sort<uint32_t, kSortItems>(ka, va, kb, vb, counters + C_NSORT, tile_bits, 0, (uint32_t)cap, pp, 0, sc.hist + 8 * kRadix,
+                           sc.offsets + 8 * kRadix, sc.lookback + 8 * ((n + kDepthChunk - 1) / kDepthChunk) * kRadix,
                            counters + C_CHUNK0 + 8, true, s);
     }
     const int rb = (int)std::min<int64_t>((cap + 1023) / 1024, 148 * 16);
