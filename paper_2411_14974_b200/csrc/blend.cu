@@ -939,7 +939,9 @@ __global__ void __launch_bounds__(pipe_threads<4>(), CS_FWD2_MINB) forward2_kern
               const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
               if (nl == 5) fwd_pair<5, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
               else if (nl == 6) fwd_pair<6, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+#ifndef CS_FWD_NO_NL4
               else if (nl == 4) fwd_pair<4, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+#endif
               else fwd_pair<0, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
             } else {
               fwd_pair<0, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
@@ -955,7 +957,9 @@ __global__ void __launch_bounds__(pipe_threads<4>(), CS_FWD2_MINB) forward2_kern
                 const int nl = __float_as_int(rec[2].z);
                 if (nl == 5) bl = fwd_candidate<5, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
                 else if (nl == 6) bl = fwd_candidate<6, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+#ifndef CS_FWD_NO_NL4
                 else if (nl == 4) bl = fwd_candidate<4, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+#endif
                 else bl = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
               } else {
                 bl = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
@@ -1359,7 +1363,11 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
           }
           bool contrib = false;
 #ifndef CS_BWD_NO_PAIR
+#ifdef CS_BWD_PAIR_ONLY
+          const bool pair = PPL == 2;   // one code path (the idle pixel's terms are predicated off)
+#else
           const bool pair = PPL == 2 && __any_sync(0xffffffffu, act[0]) && __any_sync(0xffffffffu, act[PPL - 1]);
+#endif
 #else
           const bool pair = false;
 #endif
@@ -1382,7 +1390,9 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
               const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
               if (nl == 5) CS_BWD2_PAIR(5)
               else if (nl == 6) CS_BWD2_PAIR(6)
+#ifdef CS_BWD_NL4   // (a 4-line instance: more code than it saves, 647 vs 639 us)
               else if (nl == 4) CS_BWD2_PAIR(4)
+#endif
               else CS_BWD2_PAIR(0)
             } else {
               CS_BWD2_PAIR(0)
@@ -1391,7 +1401,9 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
             const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
             if (nl == 5) { CS_BWD2_CASE(5) }
             else if (nl == 6) { CS_BWD2_CASE(6) }
+#ifdef CS_BWD_NL4
             else if (nl == 4) { CS_BWD2_CASE(4) }
+#endif
             else { CS_BWD2_CASE(0) }
           } else {
             CS_BWD2_CASE(0)
