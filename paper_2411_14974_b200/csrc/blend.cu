@@ -1390,7 +1390,8 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
               const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
               if (nl == 5) CS_BWD2_PAIR(5)
               else if (nl == 6) CS_BWD2_PAIR(6)
-#ifdef CS_BWD_NL4   // (a 4-line instance: more code than it saves, 647 vs 639 us)
+#ifndef CS_BWD_NO_NL4   // (without the 4-line instance: 639 vs 647 us at the 1080p bench view,
+                        // but 129 vs 114 ms per config-5 step, whose views hold more 4-line hulls)
               else if (nl == 4) CS_BWD2_PAIR(4)
 #endif
               else CS_BWD2_PAIR(0)
@@ -1401,7 +1402,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
             const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
             if (nl == 5) { CS_BWD2_CASE(5) }
             else if (nl == 6) { CS_BWD2_CASE(6) }
-#ifdef CS_BWD_NL4
+#ifndef CS_BWD_NO_NL4
             else if (nl == 4) { CS_BWD2_CASE(4) }
 #endif
             else { CS_BWD2_CASE(0) }
