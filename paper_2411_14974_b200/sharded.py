@@ -19,6 +19,7 @@ reference the tests compare against and the CPU (gloo) tests use.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -336,7 +337,7 @@ def rasterizer_view_grad_fn(scene, mode, settings, config: StepConfig = StepConf
 
     r = rasterizer or default_rasterizer(scene.device)
     dev = scene.device
-    n_lanes = max(1, int(lanes))
+    n_lanes = max(1, int(os.environ.get("CS_VIEW_LANES", lanes)))   # (env: lane-count experiments)
     lane_state = [{"stream": torch.cuda.Stream(dev) if n_lanes > 1 else None, "ws": Workspace(dev),
                    "lw": LossWorkspace(),
                    # device maxima over the lane's views: (pairs, overflow, non-finite)
