@@ -43,7 +43,15 @@ struct ChainArgs {
 #ifdef CS_CHAIN_F64   // float64 geometry arrays: half the threads keep the static shared memory under 48 KB
 template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 64 : 32; }
 #else
-template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 128 : 64; }
+#ifndef CS_CHAIN_THREADS
+#define CS_CHAIN_THREADS 64   // 64 / 128 threads: 235 / 238 us
+#endif
+template <int MAXK> __host__ __device__ constexpr int chain_threads() {
+  return MAXK <= 8 ? CS_CHAIN_THREADS : CS_CHAIN_THREADS / 2;
+}
+#endif
+#ifndef CS_CHAIN_MINB
+#define CS_CHAIN_MINB (640 / CS_CHAIN_THREADS)   // the SH staging limits it anyway
 #endif
 
 // Accumulation into the caller's gradient buffers (+=, GradientBuffer.add).
@@ -173,7 +181,7 @@ typedef float AccR;
 #endif
 
 template <int MAXK, bool OW>
-__global__ void __launch_bounds__(chain_threads<MAXK>(), 5) chain_kernel(ChainArgs a) {   // 5: the SH staging limits it anyway
+__global__ void __launch_bounds__(chain_threads<MAXK>(), CS_CHAIN_MINB) chain_kernel(ChainArgs a) {
   constexpr int kChainThreads = chain_threads<MAXK>();
   // per-thread slots for the dynamically indexed per-point arrays
   __shared__ G s_x[MAXK][kChainThreads], s_y[MAXK][kChainThreads];

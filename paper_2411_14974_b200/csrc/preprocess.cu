@@ -168,13 +168,16 @@ __device__ __forceinline__ double depth_scale(int mode, double d) {  // field.py
   }
 }
 
-constexpr int kPreThreads = 128;
+#ifndef CS_PRE_THREADS
+#define CS_PRE_THREADS 64   // 64 / 128 / 256 threads (12 / 6 / 3 blocks per SM): 182 / 184 / 191 us
+#endif
+constexpr int kPreThreads = CS_PRE_THREADS;
 #ifndef CS_PRE_LINES_UNROLL
 #define CS_PRE_LINES_UNROLL 2   // code size: 1 / 2 / 8: 184 / 183 / 192 us (instruction-cache misses)
 #endif
 constexpr int kPreLinesUnroll = CS_PRE_LINES_UNROLL;
 #ifndef CS_PRE_BLOCKS
-#define CS_PRE_BLOCKS 6   // resident blocks per SM (register budget 85)
+#define CS_PRE_BLOCKS (768 / CS_PRE_THREADS)   // resident blocks per SM (register budget 85)
 #endif
 
 // Index list of up to 16 entries packed as 4-bit nibbles in a register, so
