@@ -349,7 +349,8 @@ class _RasterizeFunction(torch.autograd.Function):
         st = SceneTensors(points.detach().contiguous(), raw_delta.detach().contiguous(),
                           raw_sigma.detach().contiguous(), raw_opacity.detach().contiguous(),
                           raw_mask.detach().contiguous(), sh.detach().contiguous(), background)
-        fr = rasterizer.forward(st, cam, mode, settings)
+        # a backward will follow: its accumulator reset runs on a side stream now
+        fr = rasterizer.forward(st, cam, mode, settings, zero_accumulators=any(ctx.needs_input_grad[5:]))
         ctx.frame, ctx.rasterizer = fr, rasterizer
         ctx.mark_non_differentiable(fr.final_T, fr.count, fr.weight_sum, fr.depth, fr.visible)
         return fr.image, fr.final_T, fr.count, fr.weight_sum, fr.depth, fr.visible
