@@ -115,6 +115,12 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def workload_name(args) -> str:
+    """The headline workload, named identically by both arms."""
+    return (f"config4: G({args.n},{args.seed}) 6-point convexes @ {args.width}x{args.height}, "
+            "DEPTH scaling, RenderSettings() defaults; each rank renders a replica view")
+
+
 def workload(args):
     from paper_2411_14974_b200 import synthetic
     arrays = synthetic.quantize32(synthetic.generate_scene(args.n, args.seed))
@@ -245,7 +251,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config4: {args.n} 6-point convexes @ {args.width}x{args.height} forward",
+            "config": {"workload": workload_name(args),
                        "impl_detail": "oracle/cs_oracle.c float64 C port of convexsplat 0.1.0 (reference is "
                                       "pure NumPy; not compiled), OpenMP over tiles"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
@@ -808,8 +814,7 @@ def main():
         "metric": METRIC, "value": world * 1000.0 / fwd_ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": fwd_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 (f64 preprocess)", "data": "synthetic",
-        "config": {"workload": f"config4: G({args.n},{args.seed}) 6-point convexes @ {args.width}x{args.height}, "
-                               "DEPTH scaling, RenderSettings() defaults; each rank renders a replica view",
+        "config": {"workload": workload_name(args),
                    "convexes": n, "width": args.width, "height": args.height, "visible": V, "pairs": P,
                    "l2": "flushed before every timed step (512 MB write, untimed)",
                    "launch": "CUDA graph replay of the frame's C-ABI launches (captured once)",
