@@ -40,16 +40,12 @@ struct ChainArgs {
   int64_t first;        // convexes [first, n) (a range: cs_backward_chain_range)
 };
 
-#ifdef CS_CHAIN_F64   // float64 geometry arrays: half the threads keep the static shared memory under 48 KB
-template <int MAXK> __host__ __device__ constexpr int chain_threads() { return MAXK <= 8 ? 64 : 32; }
-#else
 #ifndef CS_CHAIN_THREADS
-#define CS_CHAIN_THREADS 64   // 64 / 128 threads: 235 / 238 us
+#define CS_CHAIN_THREADS 64   // 64 / 128 threads: 235 / 238 us (also keeps CS_CHAIN_F64's smem under 48 KB)
 #endif
 template <int MAXK> __host__ __device__ constexpr int chain_threads() {
   return MAXK <= 8 ? CS_CHAIN_THREADS : CS_CHAIN_THREADS / 2;
 }
-#endif
 #ifndef CS_CHAIN_MINB
 #define CS_CHAIN_MINB (640 / CS_CHAIN_THREADS)   // the SH staging limits it anyway
 #endif

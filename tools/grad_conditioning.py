@@ -7,16 +7,18 @@ the relative change of each gradient kind (floor 2e-4 x max_kind) is the
 error any float32 implementation inherits from its inputs alone, before a
 single float32 operation.
 
-    python tools/grad_conditioning.py
+    python tools/grad_conditioning.py [mode] [seed]
 """
 import numpy as np, sys
 sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import oracle
 from paper_2411_14974_b200 import synthetic
-n, w, h, seed = 20000, 640, 480, 1
+n, w, h = 20000, 640, 480
+mode = sys.argv[1] if len(sys.argv) > 1 else "depth"
+seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 arrays = synthetic.quantize32(synthetic.generate_scene(n, seed))
 cam = synthetic.camera_dict(synthetic.bench_camera(w, h))
-o_set = dict(cutoff=2e-4, floor=1e-4, tile=16, sh_degree=3, mode="depth", background=np.zeros(3))
+o_set = dict(cutoff=2e-4, floor=1e-4, tile=16, sh_degree=3, mode=mode, background=np.zeros(3))
 d_img = np.random.default_rng(seed).normal(0, 1e-2, size=(h, w, 3))
 def run(q_inputs, q_dimg):
     view = oracle.prepare_view(arrays, cam, o_set, n_threads=8)
