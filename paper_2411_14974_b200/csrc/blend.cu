@@ -104,7 +104,7 @@ __device__ __forceinline__ int4 rec_bbox(const float4 *rec) {
 // Line coefficients of a candidate record in shared memory.  NL > 0: the
 // warp-uniform line count is a compile-time constant (the hot path, one
 // instantiation per count); NL == 0: runtime count nl <= MAXK (fallback).
-template <int NL, int MAXK>
+template <int NL, int MAXK, bool Z64 = false>
 struct LineSet {
   static constexpr int kN = NL > 0 ? NL : MAXK;
   float c[3 * kN];
@@ -124,6 +124,29 @@ struct LineSet {
       }
   }
   __device__ __forceinline__ bool has(int l) const { return NL > 0 ? true : l < nl; }
+  // z_l at (dx, dy) relative to the tile's re-basing point
+  __device__ __forceinline__ float z(int l, float dx, float dy) const {
+    return fmaf(c[3 * l], dx, fmaf(c[3 * l + 1], dy, c[3 * l + 2]));
+  }
+};
+// Float64 planes (StageRec<MAXK, true>): z formed in float64 from the staged
+// coefficients (read from shared memory at each use, so no float64 registers
+// stay live) and rounded once.  The float32 fma chain loses ~2^-24 of its
+// largest intermediate, |C' + B dy|, which steep lines (the NONE and
+// DEPTH_SQUARED scalings of the bench scenes) make large against z.
+template <int NL, int MAXK>
+struct LineSet<NL, MAXK, true> {
+  static constexpr int kN = NL > 0 ? NL : MAXK;
+  const double *p;   // A[MAXK] | B[MAXK] | C'[MAXK]
+  int nl;
+  __device__ __forceinline__ void load(const float4 *rec, int nl_rt) {
+    nl = NL > 0 ? NL : nl_rt;
+    p = reinterpret_cast<const double *>(rec + R_HEADER / 4);
+  }
+  __device__ __forceinline__ bool has(int l) const { return NL > 0 ? true : l < nl; }
+  __device__ __forceinline__ float z(int l, float dx, float dy) const {
+    return (float)fma(p[l], (double)dx, fma(p[MAXK + l], (double)dy, p[2 * MAXK + l]));
+  }
 };
 
 // Smooth field of a candidate at pixel (dx, dy) relative to the tile's
@@ -143,15 +166,14 @@ __device__ __forceinline__ float acc_lg2(float x) { return lg2(x); }
 __device__ __forceinline__ float acc_rcp(float x) { return rcp(x); }
 #endif
 
-template <int NL, int MAXK, bool ACC = false>
-__device__ __forceinline__ Eval eval_field(const LineSet<NL, MAXK> &L, float sig, float o, float dx, float dy,
-                                           float (&z)[LineSet<NL, MAXK>::kN]) {
-  constexpr int N = LineSet<NL, MAXK>::kN;
+template <bool ACC = false, typename LS>
+__device__ __forceinline__ Eval eval_field(const LS &L, float sig, float o, float dx, float dy, float (&z)[LS::kN]) {
+  constexpr int N = LS::kN;
   float ex[N];
 #pragma unroll
   for (int l = 0; l < N; l++) {
     if (L.has(l)) {
-      z[l] = fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]));
+      z[l] = L.z(l, dx, dy);
       ex[l] = ACC ? acc_ex2(z[l]) : ex2(z[l]);
     } else {
       ex[l] = 0.f;
@@ -230,10 +252,10 @@ constexpr int kStageCands = 32;
 #endif
 
 
-template <int MAXK, int kStages>
+template <int MAXK, int kStages, bool Z64 = false>
 struct PipeSmem {
   static constexpr int kRing = kStages;
-  float4 rec[kStages][kStageCands][Rec<MAXK>::kFloats / 4];
+  float4 rec[kStages][kStageCands][StageRec<MAXK, Z64>::kFloats / 4];
   uint32_t id[kStages][kStageCands];
   uint8_t bmask[kStages][kStageCands];   // forward: 8x4 blocks that may reach the cutoff (bit = warp)
   uint32_t vis[kStages];
@@ -247,8 +269,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int MAXK, int kStages>
-__device__ __forceinline__ void flush_visible(PipeSmem<MAXK, kStages> &sm, int s, uint8_t *visible) {
+template <int MAXK, int kStages, bool Z64>
+__device__ __forceinline__ void flush_visible(PipeSmem<MAXK, kStages, Z64> &sm, int s, uint8_t *visible) {
   const int lane = threadIdx.x & 31;
   const uint32_t vm = *reinterpret_cast<volatile uint32_t *>(&sm.vis[s]);
   if (visible && ((vm >> lane) & 1u)) visible[sm.id[s][lane]] = 1;
@@ -273,7 +295,7 @@ struct TileLines {
   double tx, ty;    // re-basing point (pixel coordinates)
   float cutoff;     // > 0: compute the forward cull mask
 };
-template <int MAXK>
+template <int MAXK, bool Z64 = false>
 __device__ __forceinline__ uint32_t stage_lines(const float *rec_g, const double *lines_g, float4 *rec_s,
                                                 const TileLines &tl) {
   const float4 h0 = __ldg(reinterpret_cast<const float4 *>(rec_g)), h2 = __ldg(reinterpret_cast<const float4 *>(rec_g) + 2);
@@ -293,10 +315,18 @@ __device__ __forceinline__ uint32_t stage_lines(const float *rec_g, const double
     if (l < nl) {
       double A, B, C, pad;
       ld_global_nc_v4d(lines_g + 4 * l, A, B, C, pad);
-      const float Af = (float)A, Bf = (float)B, Cf = (float)fma(A, X, fma(B, Y, C));
-      As[l] = Af;
-      Bs[l] = Bf;
-      Cs[l] = Cf;
+      const double Cr = fma(A, X, fma(B, Y, C));   // re-based onto T
+      const float Af = (float)A, Bf = (float)B, Cf = (float)Cr;
+      if (Z64) {   // float64 planes A | B | C' (StageRec<MAXK, true>)
+        double *D = reinterpret_cast<double *>(As);
+        D[l] = A;
+        D[MAXK + l] = B;
+        D[2 * MAXK + l] = Cr;
+      } else {
+        As[l] = Af;
+        Bs[l] = Bf;
+        Cs[l] = Cf;
+      }
       if (cull) {
         mag = fmaxf(mag, fabsf(Cf) + 8.f * (fabsf(Af) + fabsf(Bf)));
 #pragma unroll
@@ -328,8 +358,8 @@ __device__ __forceinline__ uint32_t stage_lines(const float *rec_g, const double
 struct NoLookAhead {
   __device__ __forceinline__ void operator()(int) const {}
 };
-template <int MAXK, int kStages, int NC, typename Batch, typename LookAhead = NoLookAhead>
-__device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const float *records, const double *lines,
+template <int MAXK, int kStages, int NC, bool Z64, typename Batch, typename LookAhead = NoLookAhead>
+__device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages, Z64> &sm, const float *records, const double *lines,
                                              const uint32_t *pair_ids, int nbatch, Batch batch, bool forward,
                                              uint8_t *visible, const TileLines &tl, bool cull,
                                              LookAhead look_ahead = LookAhead()) {
@@ -426,7 +456,7 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
     }
     uint32_t bm = 0xffu;
     if (lane < (int)count)
-      bm = stage_lines<MAXK>(records + (size_t)id * RG, lines + (size_t)id * Rec<MAXK>::kLines64, sm.rec[s][lane],
+      bm = stage_lines<MAXK, Z64>(records + (size_t)id * RG, lines + (size_t)id * Rec<MAXK>::kLines64, sm.rec[s][lane],
                              TileLines{tl.tx, tl.ty, cull ? tl.cutoff : 0.f});
     sm.bmask[s][lane] = (uint8_t)bm;
     mbar_arrive(&sm.full[s]);   // release: this lane's shared stores
@@ -456,8 +486,8 @@ __device__ __forceinline__ void pipe_produce(PipeSmem<MAXK, kStages> &sm, const 
   if (lane == 0) WS_ADD(forward ? 2 : 6, tp);
 }
 
-template <int MAXK, int kStages, int NC>
-__device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages> &sm) {
+template <int MAXK, int kStages, int NC, bool Z64>
+__device__ __forceinline__ void pipe_init(PipeSmem<MAXK, kStages, Z64> &sm) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
       mbar_init(&sm.full[s], 64);   // per producer lane: its cp.async completion + its line stores
@@ -484,14 +514,14 @@ struct FwdPixel {
 // One candidate at one pixel: evaluate, and blend iff (T >= floor if floor >
 // 0) and alpha >= cutoff (rasterize.py:194-204).  Returns whether it blended.
 // (dqx, dqy): the pixel centre relative to the tile's re-basing point.
-template <int NL, int MAXK, bool STATS>
+template <int NL, int MAXK, bool STATS, bool Z64 = false>
 __device__ __forceinline__ bool fwd_candidate(const float4 *rec, float dqx, float dqy, float cutoff, float floor_,
                                               bool use_floor, int pos, FwdPixel &P, unsigned &n_lines) {
   const float4 h0 = rec[0], h2 = rec[2];
-  LineSet<NL, MAXK> L;
+  LineSet<NL, MAXK, Z64> L;
   L.load(rec, __float_as_int(h2.z));
-  float z[LineSet<NL, MAXK>::kN];
-  const Eval e = eval_field<NL, MAXK>(L, h0.z, h0.w, dqx, dqy, z);
+  float z[LineSet<NL, MAXK, Z64>::kN];
+  const Eval e = eval_field<false>(L, h0.z, h0.w, dqx, dqy, z);
   if (STATS) n_lines += L.nl;
 #ifdef CS_FWD_BRANCHY
   if (!(e.alpha >= cutoff)) return false;
@@ -728,13 +758,13 @@ __global__ void __launch_bounds__(pipe_threads<CS_FWD_NC>(), CS_FWD_MINB) forwar
 // ---------------------------------------------------------------------------
 
 // 2^z summed over the lines at (dx, dy): eval_field's expression and order.
-template <int NL, int MAXK>
-__device__ __forceinline__ float line_sum(const LineSet<NL, MAXK> &L, float dx, float dy) {
-  constexpr int N = LineSet<NL, MAXK>::kN;
+template <typename LS>
+__device__ __forceinline__ float line_sum(const LS &L, float dx, float dy) {
+  constexpr int N = LS::kN;
   float ex[N];
 #pragma unroll
   for (int l = 0; l < N; l++)
-    ex[l] = L.has(l) ? ex2(fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]))) : 0.f;
+    ex[l] = L.has(l) ? ex2(L.z(l, dx, dy)) : 0.f;
 #pragma unroll
   for (int w = 1; w < N; w *= 2)
 #pragma unroll
@@ -744,17 +774,17 @@ __device__ __forceinline__ float line_sum(const LineSet<NL, MAXK> &L, float dx, 
 __device__ __forceinline__ bool lse_in_range(float s) { return s >= 0x1p-100f && s <= 0x1p100f; }
 // eval_field's max-shifted log-sum-exp (a sum outside [2^-100, 2^100]; rare):
 // the lines are re-read from the stage
-template <int NL, int MAXK>
+template <int NL, int MAXK, bool Z64>
 __device__ __noinline__ float lse_shifted(const float4 *rec, float dx, float dy) {
-  constexpr int N = LineSet<NL, MAXK>::kN;
-  LineSet<NL, MAXK> L;
+  constexpr int N = LineSet<NL, MAXK, Z64>::kN;
+  LineSet<NL, MAXK, Z64> L;
   L.load(rec, __float_as_int(rec[2].z));
   float z[N];
   float m = -INFINITY;
 #pragma unroll
   for (int l = 0; l < N; l++)
     if (L.has(l)) {
-      z[l] = fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]));
+      z[l] = L.z(l, dx, dy);
       m = fmaxf(m, z[l]);
     }
   float s2 = 0.f;
@@ -786,13 +816,13 @@ __device__ __forceinline__ void blend_update(FwdPixel &P, const Eval &e, bool ok
   P.last = ok ? pos : P.last;
 }
 // One candidate at both pixels of the lane (act0 / act1: which of them to blend).
-template <int NL, int MAXK, bool STATS>
+template <int NL, int MAXK, bool STATS, bool Z64 = false>
 __device__ __forceinline__ void fwd_pair(const float4 *rec, float qx, float qy0, bool act0, bool act1, float cutoff,
                                          int pos, FwdPixel &P0, FwdPixel &P1, unsigned &n_lines, bool &bl0, bool &bl1) {
   const float4 h0 = rec[0], h2 = rec[2];
   float s0, s1;
   {
-    LineSet<NL, MAXK> L;
+    LineSet<NL, MAXK, Z64> L;
     L.load(rec, __float_as_int(h2.z));
     s0 = line_sum(L, qx, qy0);
     s1 = line_sum(L, qx, qy0 + 4.f);
@@ -800,8 +830,8 @@ __device__ __forceinline__ void fwd_pair(const float4 *rec, float qx, float qy0,
   }
   float phi0 = lg2(s0), phi1 = lg2(s1);
   if (!(lse_in_range(s0) && lse_in_range(s1))) {
-    if (!lse_in_range(s0)) phi0 = lse_shifted<NL, MAXK>(rec, qx, qy0);
-    if (!lse_in_range(s1)) phi1 = lse_shifted<NL, MAXK>(rec, qx, qy0 + 4.f);
+    if (!lse_in_range(s0)) phi0 = lse_shifted<NL, MAXK, Z64>(rec, qx, qy0);
+    if (!lse_in_range(s1)) phi1 = lse_shifted<NL, MAXK, Z64>(rec, qx, qy0 + 4.f);
   }
   const Eval e0 = eval_finish(phi0, h0.z, h0.w), e1 = eval_finish(phi1, h0.z, h0.w);
   const float4 h1 = rec[1];
@@ -814,12 +844,12 @@ __device__ __forceinline__ void fwd_pair(const float4 *rec, float qx, float qy0,
 #ifndef CS_FWD2_MINB
 #define CS_FWD2_MINB 5
 #endif
-template <int MAXK, bool STATS, bool REC = false>
+template <int MAXK, bool STATS, bool REC = false, bool Z64 = false>
 __global__ void __launch_bounds__(pipe_threads<4>(), CS_FWD2_MINB) forward2_kernel(BlendArgs a) {
   constexpr int kStages = CS_FWD_STAGES;
   constexpr int NC = 4;
   extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
-  PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
+  PipeSmem<MAXK, kStages, Z64> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages, Z64> *>(pipe_dyn_smem);
   const int unit = (int)blockIdx.x;
   const int tile = a.tile_order ? (int)a.tile_order[unit] : unit;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -937,14 +967,14 @@ __global__ void __launch_bounds__(pipe_threads<4>(), CS_FWD2_MINB) forward2_kern
           if (any0 && any1) {
             if (MAXK == 8) {
               const int nl = __float_as_int(rec[2].z);   // warp-uniform line count
-              if (nl == 5) fwd_pair<5, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
-              else if (nl == 6) fwd_pair<6, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+              if (nl == 5) fwd_pair<5, MAXK, STATS, Z64>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+              else if (nl == 6) fwd_pair<6, MAXK, STATS, Z64>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
 #ifndef CS_FWD_NO_NL4
-              else if (nl == 4) fwd_pair<4, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+              else if (nl == 4) fwd_pair<4, MAXK, STATS, Z64>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
 #endif
-              else fwd_pair<0, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+              else fwd_pair<0, MAXK, STATS, Z64>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
             } else {
-              fwd_pair<0, MAXK, STATS>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
+              fwd_pair<0, MAXK, STATS, Z64>(rec, qx, qy0, act0, act1, a.cutoff, pos, P0, P1, n_lines, bl0, bl1);
             }
           } else {
             // one of the two 8x4 blocks: the single-pixel evaluation
@@ -955,14 +985,14 @@ __global__ void __launch_bounds__(pipe_threads<4>(), CS_FWD2_MINB) forward2_kern
             if (act) {
               if (MAXK == 8) {
                 const int nl = __float_as_int(rec[2].z);
-                if (nl == 5) bl = fwd_candidate<5, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
-                else if (nl == 6) bl = fwd_candidate<6, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+                if (nl == 5) bl = fwd_candidate<5, MAXK, STATS, Z64>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+                else if (nl == 6) bl = fwd_candidate<6, MAXK, STATS, Z64>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
 #ifndef CS_FWD_NO_NL4
-                else if (nl == 4) bl = fwd_candidate<4, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+                else if (nl == 4) bl = fwd_candidate<4, MAXK, STATS, Z64>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
 #endif
-                else bl = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+                else bl = fwd_candidate<0, MAXK, STATS, Z64>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
               } else {
-                bl = fwd_candidate<0, MAXK, STATS>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
+                bl = fwd_candidate<0, MAXK, STATS, Z64>(rec, qx, qy, a.cutoff, a.floor, false, pos, P, n_lines);
               }
             }
             if (any0) bl0 = bl; else bl1 = bl;
@@ -1051,17 +1081,17 @@ struct BwdPixel {
 // reconstruct T_prev = T / (1 - alpha), and add the pixel's 32 screen-space
 // gradient terms to v (unchanged when it did not blend).  Returns whether
 // it did.
-template <int NL, int MAXK, bool STATS, int VN>
+template <int NL, int MAXK, bool STATS, int VN, bool Z64 = false>
 __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float qy, float cutoff, BwdPixel &P,
                                               float (&v)[VN], unsigned &n_lines) {
   const float4 h0 = rec[0], h2 = rec[2];
-  LineSet<NL, MAXK> L;
+  LineSet<NL, MAXK, Z64> L;
   L.load(rec, __float_as_int(h2.z));
-  constexpr int N = LineSet<NL, MAXK>::kN;
+  constexpr int N = LineSet<NL, MAXK, Z64>::kN;
   float z[N];
   const float dx = qx, dy = qy;   // relative to the tile's re-basing point
   const float o = h0.w, sig = h0.z, dls = h2.y, inv_dls = h2.w;
-  const Eval e = eval_field<NL, MAXK, true>(L, sig, o, dx, dy, z);
+  const Eval e = eval_field<true>(L, sig, o, dx, dy, z);
   if (STATS) n_lines += L.nl;
   if (!(e.alpha >= cutoff)) return false;
   const float4 h1 = rec[1];
@@ -1108,11 +1138,11 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
 // the blend decision as a predicate: a pixel that did not blend adds exact
 // zeros (v never holds -0, so v + 0 == v) and keeps its state -- the same
 // sums, in the same order, as the branch in bwd_candidate.
-template <int NL, int MAXK, int VN>
-__device__ __forceinline__ void bwd_terms(const LineSet<NL, MAXK> &L, const float (&z)[LineSet<NL, MAXK>::kN],
+template <typename LS, int VN>
+__device__ __forceinline__ void bwd_terms(const LS &L, const float (&z)[LS::kN],
                                           const Eval &e, bool ok, float dx, float dy, float4 h0, float4 h1,
                                           float4 h2, BwdPixel &P, float (&v)[VN]) {
-  constexpr int N = LineSet<NL, MAXK>::kN;
+  constexpr int N = LS::kN;
   const float o = h0.w, sig = h0.z, dls = h2.y, inv_dls = h2.w;
   const float om = fmaxf(fmaf(o, e.J, h2.x), 1e-6f);  // 1 - alpha
 #ifdef CS_EXACT_RECIP
@@ -1151,15 +1181,14 @@ __device__ __forceinline__ void bwd_terms(const LineSet<NL, MAXK> &L, const floa
   if (ok) P.T = Tp;
 }
 // z_l and sum 2^z_l at (dx, dy): eval_field's expressions (ACC) and order.
-template <int NL, int MAXK>
-__device__ __forceinline__ float line_sum_z(const LineSet<NL, MAXK> &L, float dx, float dy,
-                                            float (&z)[LineSet<NL, MAXK>::kN]) {
-  constexpr int N = LineSet<NL, MAXK>::kN;
+template <typename LS>
+__device__ __forceinline__ float line_sum_z(const LS &L, float dx, float dy, float (&z)[LS::kN]) {
+  constexpr int N = LS::kN;
   float ex[N];
 #pragma unroll
   for (int l = 0; l < N; l++) {
     if (L.has(l)) {
-      z[l] = fmaf(L.c[3 * l], dx, fmaf(L.c[3 * l + 1], dy, L.c[3 * l + 2]));
+      z[l] = L.z(l, dx, dy);
       ex[l] = acc_ex2(z[l]);
     } else {
       ex[l] = 0.f;
@@ -1171,9 +1200,9 @@ __device__ __forceinline__ float line_sum_z(const LineSet<NL, MAXK> &L, float dx
     for (int l = 0; l + w < N; l += 2 * w) ex[l] += ex[l + w];
   return ex[0];
 }
-template <int NL, int MAXK>
-__device__ __forceinline__ float lse_shifted_z(const LineSet<NL, MAXK> &L, const float (&z)[LineSet<NL, MAXK>::kN]) {
-  constexpr int N = LineSet<NL, MAXK>::kN;
+template <typename LS>
+__device__ __forceinline__ float lse_shifted_z(const LS &L, const float (&z)[LS::kN]) {
+  constexpr int N = LS::kN;
   float m = -INFINITY;
 #pragma unroll
   for (int l = 0; l < N; l++)
@@ -1197,13 +1226,13 @@ __device__ __forceinline__ Eval eval_finish_acc(float phi2, float sig, float o) 
 // One candidate at both pixels of the lane (rows r and r + 4): one line load,
 // two independent evaluation chains, the terms added pixel 0 then pixel 1
 // (the order of the per-pixel calls).
-template <int NL, int MAXK, bool STATS, int VN>
+template <int NL, int MAXK, bool STATS, int VN, bool Z64 = false>
 __device__ __forceinline__ void bwd_pair(const float4 *rec, float qx, float qy0, bool act0, bool act1, float cutoff,
                                          BwdPixel &P0, BwdPixel &P1, float (&v)[VN], unsigned &n_lines, bool &ok0,
                                          bool &ok1) {
-  constexpr int N = LineSet<NL, MAXK>::kN;
+  constexpr int N = LineSet<NL, MAXK, Z64>::kN;
   const float4 h0 = rec[0], h2 = rec[2];
-  LineSet<NL, MAXK> L;
+  LineSet<NL, MAXK, Z64> L;
   L.load(rec, __float_as_int(h2.z));
   float z0[N], z1[N];
   const float s0 = line_sum_z(L, qx, qy0, z0), s1 = line_sum_z(L, qx, qy0 + 4.f, z1);
@@ -1237,14 +1266,14 @@ __device__ __forceinline__ void bwd_pair(const float4 *rec, float qx, float qy0,
 #ifndef CS_BWD_PPL
 #define CS_BWD_PPL 2
 #endif
-template <int MAXK, int PPL, bool STATS>
+template <int MAXK, int PPL, bool STATS, bool Z64 = false>
 __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward_kernel(BlendArgs a) {
   constexpr int NC = 8 / PPL;   // warps of 8 x (4 PPL) pixels
   constexpr int AF = Acc<MAXK>::kFloats;
   constexpr int NG = (AF + 31) / 32;
   constexpr int kStages = CS_BWD_STAGES;
   extern __shared__ __align__(16) unsigned char pipe_dyn_smem[];
-  PipeSmem<MAXK, kStages> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages> *>(pipe_dyn_smem);
+  PipeSmem<MAXK, kStages, Z64> &sm = *reinterpret_cast<PipeSmem<MAXK, kStages, Z64> *>(pipe_dyn_smem);
   __shared__ int s_last[NC];
 #ifdef CS_BWD_SMEM_REDUCE
   // per-warp transpose scratch: lane L's 32 values at row L (stride 36
@@ -1373,7 +1402,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
 #endif
 #define CS_BWD2_PX(NLV, H)                                                                       \
   if (H < PPL && act[H % PPL]) {                                                                   \
-    const bool c_ = bwd_candidate<NLV, MAXK, STATS>(rec, qx, qy0 + (float)(4 * (H % PPL)), a.cutoff, P[H % PPL], v, n_lines); \
+    const bool c_ = bwd_candidate<NLV, MAXK, STATS, NG * 32, Z64>(rec, qx, qy0 + (float)(4 * (H % PPL)), a.cutoff, P[H % PPL], v, n_lines); \
     contrib |= c_;                                                                                 \
     if (STATS) n_bblend += (unsigned)c_;                                                           \
   }
@@ -1381,7 +1410,7 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
 #define CS_BWD2_PAIR(NLV)                                                                        \
   {                                                                                                \
     bool o0_, o1_;                                                                                 \
-    bwd_pair<NLV, MAXK, STATS>(rec, qx, qy0, act[0], act[PPL - 1], a.cutoff, P[0], P[PPL - 1], v, n_lines, o0_, o1_); \
+    bwd_pair<NLV, MAXK, STATS, NG * 32, Z64>(rec, qx, qy0, act[0], act[PPL - 1], a.cutoff, P[0], P[PPL - 1], v, n_lines, o0_, o1_); \
     contrib = o0_ || o1_;                                                                          \
     if (STATS) n_bblend += (unsigned)o0_ + (unsigned)o1_;                                         \
   }
@@ -1463,6 +1492,19 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
   }
 }
 
+// Blend lines staged and evaluated in float64 for the scalings whose line
+// slopes the float32 evaluation cannot hold at scale (NONE: no depth factor,
+// DEPTH_SQUARED: its square); DEPTH and SQRT_DEPTH (the
+// configs' scaling) keep the float32 planes.
+static bool lines_f64(const cs_settings &set) {
+#ifdef CS_LINES_F32_ONLY
+  (void)set;
+  return false;
+#else
+  return set.scaling_mode == CS_SCALE_NONE || set.scaling_mode == CS_SCALE_DEPTH2;
+#endif
+}
+
 static BlendArgs make_args(const cs_camera &cam, const cs_settings &set, const cs_layout &L, char *ws) {
   BlendArgs a;
   a.records = reinterpret_cast<const float *>(ws + L.records);
@@ -1519,14 +1561,26 @@ int launch_forward_blend(const cs_camera &cam, const cs_settings &set, const cs_
   }
 #ifndef CS_FWD_PPL1
   a.ahead = a.ahead / CS_FWD_MINB * CS_FWD2_MINB;
-  if (L.max_k == 8) {
-    auto k = rec ? forward2_kernel<8, false, true> : stats ? forward2_kernel<8, true> : forward2_kernel<8, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_FWD_STAGES>));
-    k<<<tiles, pipe_threads<4>(), sizeof(PipeSmem<8, CS_FWD_STAGES>), s>>>(a);
+  auto go = [&](auto kernel, size_t smem) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel<<<tiles, pipe_threads<4>(), smem, s>>>(a);
+  };
+  if (lines_f64(set)) {
+    if (L.max_k == 8)
+      go(rec ? forward2_kernel<8, false, true, true> : stats ? forward2_kernel<8, true, false, true>
+                                                             : forward2_kernel<8, false, false, true>,
+         sizeof(PipeSmem<8, CS_FWD_STAGES, true>));
+    else
+      go(rec ? forward2_kernel<16, false, true, true> : stats ? forward2_kernel<16, true, false, true>
+                                                              : forward2_kernel<16, false, false, true>,
+         sizeof(PipeSmem<16, CS_FWD_STAGES, true>));
   } else {
-    auto k = rec ? forward2_kernel<16, false, true> : stats ? forward2_kernel<16, true> : forward2_kernel<16, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_FWD_STAGES>));
-    k<<<tiles, pipe_threads<4>(), sizeof(PipeSmem<16, CS_FWD_STAGES>), s>>>(a);
+    if (L.max_k == 8)
+      go(rec ? forward2_kernel<8, false, true> : stats ? forward2_kernel<8, true> : forward2_kernel<8, false>,
+         sizeof(PipeSmem<8, CS_FWD_STAGES>));
+    else
+      go(rec ? forward2_kernel<16, false, true> : stats ? forward2_kernel<16, true> : forward2_kernel<16, false>,
+         sizeof(PipeSmem<16, CS_FWD_STAGES>));
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 #endif
@@ -1568,14 +1622,24 @@ int launch_backward_blend(const cs_camera &cam, const cs_settings &set, const cs
   a.d_image = d_image;
   if (zero) launch_zero_accumulators(p, L, ws, s);
   const int tiles = L.tiles_x * L.tiles_y;
-  if (L.max_k == 8) {
-    auto k = stats ? backward_kernel<8, CS_BWD_PPL, true> : backward_kernel<8, CS_BWD_PPL, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<8, CS_BWD_STAGES>));
-    k<<<tiles, pipe_threads<8 / CS_BWD_PPL>(), sizeof(PipeSmem<8, CS_BWD_STAGES>), s>>>(a);
+  auto go = [&](auto kernel, size_t smem) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel<<<tiles, pipe_threads<8 / CS_BWD_PPL>(), smem, s>>>(a);
+  };
+  if (lines_f64(set)) {
+    if (L.max_k == 8)
+      go(stats ? backward_kernel<8, CS_BWD_PPL, true, true> : backward_kernel<8, CS_BWD_PPL, false, true>,
+         sizeof(PipeSmem<8, CS_BWD_STAGES, true>));
+    else
+      go(stats ? backward_kernel<16, CS_BWD_PPL, true, true> : backward_kernel<16, CS_BWD_PPL, false, true>,
+         sizeof(PipeSmem<16, CS_BWD_STAGES, true>));
   } else {
-    auto k = stats ? backward_kernel<16, CS_BWD_PPL, true> : backward_kernel<16, CS_BWD_PPL, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<16, CS_BWD_STAGES>));
-    k<<<tiles, pipe_threads<8 / CS_BWD_PPL>(), sizeof(PipeSmem<16, CS_BWD_STAGES>), s>>>(a);
+    if (L.max_k == 8)
+      go(stats ? backward_kernel<8, CS_BWD_PPL, true> : backward_kernel<8, CS_BWD_PPL, false>,
+         sizeof(PipeSmem<8, CS_BWD_STAGES>));
+    else
+      go(stats ? backward_kernel<16, CS_BWD_PPL, true> : backward_kernel<16, CS_BWD_PPL, false>,
+         sizeof(PipeSmem<16, CS_BWD_STAGES>));
   }
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ERR_CUDA;
 }

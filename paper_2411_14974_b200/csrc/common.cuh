@@ -49,6 +49,14 @@ template <int MAXK> struct Rec {
   static constexpr int kLines64 = 4 * MAXK;             // doubles per convex in `lines`
   static_assert(kFloats % 4 == 0 && MAXK % 4 == 0, "record planes must be float4 aligned");
 };
+// A candidate's record in a blend stage: the header, then its hull lines
+// re-based onto the tile as planes A | B | C' -- float32, or float64 (Z64:
+// the scalings whose line slopes the float32 field evaluation cannot hold,
+// DESIGN.md section 2).
+template <int MAXK, bool Z64 = false> struct StageRec {
+  static constexpr int kFloats = R_HEADER + (Z64 ? 6 : 3) * MAXK;
+  static_assert(kFloats % 4 == 0, "stage records are float4 rows");
+};
 // Tile re-basing point: pixel (tx*16 + kRebase, ty*16 + kRebase).
 constexpr int kRebase = 8;
 
