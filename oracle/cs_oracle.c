@@ -927,6 +927,50 @@ int or_blend_decisions(const or_camera *cam, const or_settings *st, const or_vie
     return 0;
 }
 
+/* Analysis helper (test only): the pixels whose reference walk
+ * (rasterize.py:178-204, as or_blend_decisions) meets a decision within
+ * relative eps of its threshold -- alpha against the cutoff, or T against the
+ * floor.  A float32 renderer may decide those either way; near_tie[p] = 1. */
+int or_near_ties(const or_camera *cam, const or_settings *st, const or_view *V, const int64_t *tile_off,
+                 const int32_t *items, double eps, uint8_t *near_tie) {
+    const int W = cam->width, H = cam->height, ts = st->tile, k = V->k;
+    const int tx_n = (W + ts - 1) / ts, ty_n = (H + ts - 1) / ts;
+    double dist[OR_MAXPTS];
+    double *T = malloc(sizeof(double) * (size_t)W * H);
+    if (!T) return 1;
+    for (size_t p = 0; p < (size_t)W * H; p++) { T[p] = 1.0; near_tie[p] = 0; }
+    for (int64_t t = 0; t < (int64_t)tx_n * ty_n; t++) {
+        int ty = (int)(t / tx_n), tx = (int)(t % tx_n);
+        int ty0 = ty * ts, ty1 = ty0 + ts < H ? ty0 + ts : H;
+        int tx0 = tx * ts, tx1 = tx0 + ts < W ? tx0 + ts : W;
+        for (int64_t e = tile_off[t]; e < tile_off[t + 1]; e++) {
+            int i = V->order[items[e]];
+            const int32_t *bb = V->bbox + 4 * i;
+            int y0 = bb[2] > ty0 ? bb[2] : ty0, y1 = bb[3] < ty1 ? bb[3] : ty1;
+            int x0 = bb[0] > tx0 ? bb[0] : tx0, x1 = bb[1] < tx1 ? bb[1] : tx1;
+            const double *nrm = V->normals + (size_t)i * k * 2, *off = V->offsets + (size_t)i * k;
+            for (int y = y0; y < y1; y++)
+                for (int x = x0; x < x1; x++) {
+                    size_t p = (size_t)y * W + x;
+                    if (st->floor > 0.0) {
+                        if (fabs(T[p] - st->floor) <= eps * st->floor) near_tie[p] = 1;
+                        if (!(T[p] >= st->floor)) continue;
+                    }
+                    double phi, ind;
+                    field_at(nrm, off, V->hull_n[i], V->delta_s[i], V->sigma_s[i], x + 0.5, y + 0.5, dist, &phi,
+                             &ind);
+                    double a = V->opacity[i] * ind;
+                    if (a > OR_ALPHA_MAX) a = OR_ALPHA_MAX;
+                    if (fabs(a - st->cutoff) <= eps * st->cutoff) near_tie[p] = 1;
+                    if (!(a >= st->cutoff)) continue;
+                    T[p] *= 1.0 - a;
+                }
+        }
+    }
+    free(T);
+    return 0;
+}
+
 /* Analysis helper (test/tooling only): for each listed tile, the 256-bit
  * mask (bit = ly*16+lx) of pixels that EVALUATE each candidate of the tile
  * list in the reference walk (bbox holds the pixel and T >= floor when the

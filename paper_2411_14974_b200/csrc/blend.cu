@@ -107,6 +107,7 @@ __device__ __forceinline__ int4 rec_bbox(const float4 *rec) {
 template <int NL, int MAXK, bool Z64 = false>
 struct LineSet {
   static constexpr int kN = NL > 0 ? NL : MAXK;
+  static constexpr bool kPrecise = false;
   float c[3 * kN];
   int nl;
   // stage record planes A[MAXK] | B[MAXK] | C'[MAXK] after the header
@@ -137,6 +138,7 @@ struct LineSet {
 template <int NL, int MAXK>
 struct LineSet<NL, MAXK, true> {
   static constexpr int kN = NL > 0 ? NL : MAXK;
+  static constexpr bool kPrecise = true;
   const double *p;   // A[MAXK] | B[MAXK] | C'[MAXK]
   int nl;
   __device__ __forceinline__ void load(const float4 *rec, int nl_rt) {
@@ -165,6 +167,18 @@ __device__ __forceinline__ float acc_ex2(float x) { return ex2(x); }
 __device__ __forceinline__ float acc_lg2(float x) { return lg2(x); }
 __device__ __forceinline__ float acc_rcp(float x) { return rcp(x); }
 #endif
+// P: correctly rounded exp2 / log2 / reciprocal (the float64-line kernels:
+// their scalings put many more alphas next to the cutoff), else the
+// approximations (ACC: the backward's acc_* choice)
+template <bool P, bool ACC = false> __device__ __forceinline__ float fx2(float x) {
+  return P ? exp2f(x) : (ACC ? acc_ex2(x) : ex2(x));
+}
+template <bool P, bool ACC = false> __device__ __forceinline__ float flg2(float x) {
+  return P ? log2f(x) : (ACC ? acc_lg2(x) : lg2(x));
+}
+template <bool P, bool ACC = false> __device__ __forceinline__ float frcp(float x) {
+  return P ? 1.f / x : (ACC ? acc_rcp(x) : rcp(x));
+}
 
 template <bool ACC = false, typename LS>
 __device__ __forceinline__ Eval eval_field(const LS &L, float sig, float o, float dx, float dy, float (&z)[LS::kN]) {
@@ -174,7 +188,7 @@ __device__ __forceinline__ Eval eval_field(const LS &L, float sig, float o, floa
   for (int l = 0; l < N; l++) {
     if (L.has(l)) {
       z[l] = L.z(l, dx, dy);
-      ex[l] = ACC ? acc_ex2(z[l]) : ex2(z[l]);
+      ex[l] = fx2<LS::kPrecise, ACC>(z[l]);
     } else {
       ex[l] = 0.f;
     }
@@ -191,7 +205,7 @@ __device__ __forceinline__ Eval eval_field(const LS &L, float sig, float o, floa
 #else
   if (s >= 0x1p-100f && s <= 0x1p100f) {
 #endif
-    phi2 = ACC ? acc_lg2(s) : lg2(s);
+    phi2 = flg2<LS::kPrecise, ACC>(s);
   } else {
     float m = -INFINITY;
 #pragma unroll
@@ -200,12 +214,12 @@ __device__ __forceinline__ Eval eval_field(const LS &L, float sig, float o, floa
     float s2 = 0.f;
 #pragma unroll
     for (int l = 0; l < N; l++)
-      if (L.has(l)) s2 += ACC ? acc_ex2(z[l] - m) : ex2(z[l] - m);
-    phi2 = m + (ACC ? acc_lg2(s2) : lg2(s2));
+      if (L.has(l)) s2 += fx2<LS::kPrecise, ACC>(z[l] - m);
+    phi2 = m + flg2<LS::kPrecise, ACC>(s2);
   }
   Eval e;
-  const float u = ACC ? acc_ex2(sig * phi2) : ex2(sig * phi2);
-  e.I = ACC ? acc_rcp(1.f + u) : rcp(1.f + u);
+  const float u = fx2<LS::kPrecise, ACC>(sig * phi2);
+  e.I = frcp<LS::kPrecise, ACC>(1.f + u);
   // 1 - I without cancellation: u*I while I >= 1/2, else 1 - I (also covers
   // u so large that I flushes to zero)
   e.J = u > 1.f ? 1.f - e.I : u * e.I;
@@ -764,7 +778,7 @@ __device__ __forceinline__ float line_sum(const LS &L, float dx, float dy) {
   float ex[N];
 #pragma unroll
   for (int l = 0; l < N; l++)
-    ex[l] = L.has(l) ? ex2(L.z(l, dx, dy)) : 0.f;
+    ex[l] = L.has(l) ? fx2<LS::kPrecise>(L.z(l, dx, dy)) : 0.f;
 #pragma unroll
   for (int w = 1; w < N; w *= 2)
 #pragma unroll
@@ -790,13 +804,14 @@ __device__ __noinline__ float lse_shifted(const float4 *rec, float dx, float dy)
   float s2 = 0.f;
 #pragma unroll
   for (int l = 0; l < N; l++)
-    if (L.has(l)) s2 += ex2(z[l] - m);
-  return m + lg2(s2);
+    if (L.has(l)) s2 += fx2<Z64>(z[l] - m);
+  return m + flg2<Z64>(s2);
 }
+template <bool P = false>
 __device__ __forceinline__ Eval eval_finish(float phi2, float sig, float o) {
   Eval e;
-  const float u = ex2(sig * phi2);
-  e.I = rcp(1.f + u);
+  const float u = fx2<P>(sig * phi2);
+  e.I = frcp<P>(1.f + u);
   e.J = u > 1.f ? 1.f - e.I : u * e.I;
   e.alpha_raw = o * e.I;
   e.alpha = fminf(e.alpha_raw, (float)kAlphaMaxD);
@@ -828,12 +843,12 @@ __device__ __forceinline__ void fwd_pair(const float4 *rec, float qx, float qy0,
     s1 = line_sum(L, qx, qy0 + 4.f);
     if (STATS) n_lines += (unsigned)L.nl * ((act0 ? 1u : 0u) + (act1 ? 1u : 0u));
   }
-  float phi0 = lg2(s0), phi1 = lg2(s1);
+  float phi0 = flg2<Z64>(s0), phi1 = flg2<Z64>(s1);
   if (!(lse_in_range(s0) && lse_in_range(s1))) {
     if (!lse_in_range(s0)) phi0 = lse_shifted<NL, MAXK, Z64>(rec, qx, qy0);
     if (!lse_in_range(s1)) phi1 = lse_shifted<NL, MAXK, Z64>(rec, qx, qy0 + 4.f);
   }
-  const Eval e0 = eval_finish(phi0, h0.z, h0.w), e1 = eval_finish(phi1, h0.z, h0.w);
+  const Eval e0 = eval_finish<Z64>(phi0, h0.z, h0.w), e1 = eval_finish<Z64>(phi1, h0.z, h0.w);
   const float4 h1 = rec[1];
   bl0 = act0 && e0.alpha >= cutoff;
   bl1 = act1 && e1.alpha >= cutoff;
@@ -1099,7 +1114,7 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
 #ifdef CS_EXACT_RECIP
   const float rom = 1.f / om;
 #else
-  const float rom = rcp(om);
+  const float rom = frcp<Z64>(om);
 #endif
   const float Tp = P.T * rom;
   const float w = Tp * e.alpha;
@@ -1120,7 +1135,7 @@ __device__ __forceinline__ bool bwd_candidate(const float4 *rec, float qx, float
 #pragma unroll
   for (int l = 0; l < N; l++) {
     if (L.has(l)) {
-      const float wl = acc_ex2(z[l] - e.phi2);         // softmax_over_lines (field.py:62-67)
+      const float wl = fx2<Z64, true>(z[l] - e.phi2);   // softmax_over_lines (field.py:62-67)
       wz = fmaf(wl, z[l], wz);
       const float dL = dscale * wl;
       v[A_LINES + 3 * l] += dL * dx;
@@ -1148,7 +1163,7 @@ __device__ __forceinline__ void bwd_terms(const LS &L, const float (&z)[LS::kN],
 #ifdef CS_EXACT_RECIP
   const float rom = 1.f / om;
 #else
-  const float rom = rcp(om);
+  const float rom = frcp<LS::kPrecise>(om);
 #endif
   const float Tp = P.T * rom;
   const float w = ok ? Tp * e.alpha : 0.f;
@@ -1168,7 +1183,7 @@ __device__ __forceinline__ void bwd_terms(const LS &L, const float (&z)[LS::kN],
 #pragma unroll
   for (int l = 0; l < N; l++) {
     if (L.has(l)) {
-      const float wl = acc_ex2(z[l] - e.phi2);
+      const float wl = fx2<LS::kPrecise, true>(z[l] - e.phi2);
       wz = fmaf(wl, z[l], wz);
       const float dL = dscale * wl;
       v[A_LINES + 3 * l] += dL * dx;
@@ -1189,7 +1204,7 @@ __device__ __forceinline__ float line_sum_z(const LS &L, float dx, float dy, flo
   for (int l = 0; l < N; l++) {
     if (L.has(l)) {
       z[l] = L.z(l, dx, dy);
-      ex[l] = acc_ex2(z[l]);
+      ex[l] = fx2<LS::kPrecise, true>(z[l]);
     } else {
       ex[l] = 0.f;
     }
@@ -1210,13 +1225,14 @@ __device__ __forceinline__ float lse_shifted_z(const LS &L, const float (&z)[LS:
   float s2 = 0.f;
 #pragma unroll
   for (int l = 0; l < N; l++)
-    if (L.has(l)) s2 += acc_ex2(z[l] - m);
-  return m + acc_lg2(s2);
+    if (L.has(l)) s2 += fx2<LS::kPrecise, true>(z[l] - m);
+  return m + flg2<LS::kPrecise, true>(s2);
 }
+template <bool P = false>
 __device__ __forceinline__ Eval eval_finish_acc(float phi2, float sig, float o) {
   Eval e;
-  const float u = acc_ex2(sig * phi2);
-  e.I = acc_rcp(1.f + u);
+  const float u = fx2<P, true>(sig * phi2);
+  e.I = frcp<P, true>(1.f + u);
   e.J = u > 1.f ? 1.f - e.I : u * e.I;
   e.alpha_raw = o * e.I;
   e.alpha = fminf(e.alpha_raw, (float)kAlphaMaxD);
@@ -1236,12 +1252,12 @@ __device__ __forceinline__ void bwd_pair(const float4 *rec, float qx, float qy0,
   L.load(rec, __float_as_int(h2.z));
   float z0[N], z1[N];
   const float s0 = line_sum_z(L, qx, qy0, z0), s1 = line_sum_z(L, qx, qy0 + 4.f, z1);
-  float phi0 = acc_lg2(s0), phi1 = acc_lg2(s1);
+  float phi0 = flg2<Z64, true>(s0), phi1 = flg2<Z64, true>(s1);
   if (!(lse_in_range(s0) && lse_in_range(s1))) {
     if (!lse_in_range(s0)) phi0 = lse_shifted_z(L, z0);
     if (!lse_in_range(s1)) phi1 = lse_shifted_z(L, z1);
   }
-  const Eval e0 = eval_finish_acc(phi0, h0.z, h0.w), e1 = eval_finish_acc(phi1, h0.z, h0.w);
+  const Eval e0 = eval_finish_acc<Z64>(phi0, h0.z, h0.w), e1 = eval_finish_acc<Z64>(phi1, h0.z, h0.w);
   if (STATS) n_lines += (unsigned)L.nl * ((act0 ? 1u : 0u) + (act1 ? 1u : 0u));
   ok0 = act0 && e0.alpha >= cutoff;
   ok1 = act1 && e1.alpha >= cutoff;
