@@ -18,13 +18,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "synccheck", "initcheck"])
-def test_sanitizer_clean(tool):
+@pytest.mark.parametrize("tool,mode", [("memcheck", "depth"), ("synccheck", "depth"), ("initcheck", "depth"),
+                                       ("memcheck", "depth2")])   # depth2: the float64-line kernels
+def test_sanitizer_clean(tool, mode):
     exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(exe):
         pytest.skip("compute-sanitizer not available")
     out = subprocess.run([exe, "--tool", tool, "--error-exitcode", "9", sys.executable,
-                          os.path.join(ROOT, "tools", "fwd_small.py"), "2000", "320", "200"],
+                          os.path.join(ROOT, "tools", "fwd_small.py"), "2000", "320", "200", mode],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, (out.stdout + out.stderr)[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out.stdout + out.stderr
