@@ -1411,7 +1411,14 @@ __global__ void __launch_bounds__(pipe_threads<8 / PPL>(), CS_BWD_MINB) backward
 #ifdef CS_BWD_PAIR_ONLY
           const bool pair = PPL == 2;   // one code path (the idle pixel's terms are predicated off)
 #else
-          const bool pair = PPL == 2 && __any_sync(0xffffffffu, act[0]) && __any_sync(0xffffffffu, act[PPL - 1]);
+          bool pair = PPL == 2 && __any_sync(0xffffffffu, act[0]) && __any_sync(0xffffffffu, act[PPL - 1]);
+#ifndef CS_BWD_PAIR_NL0   // MAXK = 8: pair only the specialised line counts (the generic
+                          // instance's registers spilled everywhere: 652 -> 641 us without it)
+          if (MAXK == 8) {
+            const int nl_ = __float_as_int(rec[2].z);
+            pair = pair && nl_ >= 4 && nl_ <= 6;
+          }
+#endif
 #endif
 #else
           const bool pair = false;
